@@ -1,0 +1,225 @@
+/*
+ * jet.h — C-ABI of the B200-native Jet multilevel k-way partitioner.
+ *
+ * This is the drop-in boundary for the reference package `jetpart`
+ * (/root/reference/pkg/src/jetpart). The reference has no native code and no
+ * FFI: its public hot-path surface is a set of Python functions. Each entry
+ * point below replaces exactly one of them; the Python package
+ * `paper_2304_13194_b200` binds these through ctypes and
+ * re-exposes the reference's function names, argument meaning and errors.
+ *
+ * Conventions
+ *   - All host arrays use the reference's int64 dtype unless a dtype code is
+ *     given (JET_I32 / JET_I64) so callers holding int32 data avoid a copy.
+ *   - Every function returns a jet_status; on failure jet_last_error()
+ *     (thread-local) holds a one-line message. The Python layer maps
+ *     JET_EINVAL -> ValueError, JET_EBALANCE -> BalanceInfeasibleError,
+ *     JET_EREBALANCE -> RebalanceInfeasibleError, others -> JetpartError.
+ *   - A jet_ctx owns one CUDA device, one stream and a stream-ordered memory
+ *     pool. Calls on one context are serialised by the caller.
+ *   - No torch types and no CUDA types cross this boundary.
+ */
+#ifndef JET_H
+#define JET_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define JET_API_VERSION 1
+
+typedef enum {
+  JET_OK = 0,
+  JET_EINVAL = 1,       /* invalid argument (ValueError in Python) */
+  JET_EBALANCE = 2,     /* BalanceInfeasibleError (driver.py:61-71) */
+  JET_ECUDA = 3,        /* CUDA runtime / launch error */
+  JET_ENOMEM = 4,       /* device allocation failed */
+  JET_EREBALANCE = 5,   /* RebalanceInfeasibleError (rebalance.py:153-156) */
+  JET_EINTERNAL = 6,    /* internal invariant violated */
+  JET_EUNSUPPORTED = 7  /* input outside the GPU path's supported range */
+} jet_status;
+
+#define JET_I32 4
+#define JET_I64 8
+
+typedef struct jet_ctx jet_ctx;
+typedef struct jet_graph jet_graph;         /* device-resident CSR level */
+typedef struct jet_hierarchy jet_hierarchy; /* device-resident level stack */
+
+/* numpy PCG64 bit-generator state (Generator.bit_generator.state). */
+typedef struct {
+  uint64_t state_hi, state_lo; /* 128-bit LCG state */
+  uint64_t inc_hi, inc_lo;     /* 128-bit increment (odd) */
+  int32_t has_uint32;          /* buffered upper half pending */
+  uint32_t uinteger;           /* the buffered half */
+} jet_pcg64;
+
+/* RefinerConfig (refine.py:34-75) plus the scalars the Python driver derives
+ * with exact rational arithmetic (graph.py:203-212, rebalance.py:26-32,
+ * refine.py:117-121). */
+typedef struct {
+  int32_t k;
+  double imbalance;
+  int64_t limit;           /* part_weight_limit(W, k, imbalance) */
+  int64_t sigma;           /* rebalance_thresholds(...) */
+  int64_t c_finest_num, c_finest_den; /* Fraction(str(c_finest)) */
+  int64_t c_other_num, c_other_den;   /* Fraction(str(c_other)) */
+  double c_finest, c_other;           /* used when den > 10**6 */
+  int32_t c_finest_float, c_other_float;
+  double phi;
+  int32_t no_improve_limit;
+  int32_t sub_buckets;
+  uint64_t seed;
+  int32_t coarse_target;
+  int32_t restarts;
+  int32_t afterburner;
+  int32_t locking;
+  int32_t deterministic; /* 1: bit-exact reference semantics (only mode in v1) */
+  int32_t verbose;
+} jet_config;
+
+typedef struct {
+  int32_t level;
+  int64_t n, m;
+  int64_t cut_in, cut_out;
+  int32_t balanced_in, balanced;
+  int32_t iterations, lp_passes, weak_passes, strong_passes, rebalance_stuck;
+  int64_t moves;
+  double seconds;
+} jet_level_stats;
+
+#define JET_MAX_LEVELS 64
+
+typedef struct {
+  double t_upload, t_coarsen, t_initial, t_uncoarsen, t_total, t_download;
+  int32_t n_levels;
+  int64_t cutsize;
+  int32_t balanced;
+  int64_t max_part_weight;
+  int64_t kernel_launches; /* device kernels launched by this call */
+  jet_level_stats levels[JET_MAX_LEVELS]; /* refinement order: top .. 0 */
+} jet_run_stats;
+
+/* ---- context --------------------------------------------------------- */
+int jet_create(int device, jet_ctx** out);
+void jet_destroy(jet_ctx* ctx);
+const char* jet_last_error(void);
+int jet_api_version(void);
+/* Device-time accounting for the roofline: per-kernel-class CUDA-event
+ * totals (ms) and launch counts since the last reset. */
+int jet_profile_enable(jet_ctx* ctx, int on);
+int jet_profile_reset(jet_ctx* ctx);
+/* Writes up to cap records "name\tlaunches\tms\tbytes\n" into buf. */
+int jet_profile_report(jet_ctx* ctx, char* buf, int64_t cap);
+int jet_synchronize(jet_ctx* ctx);
+
+/* ---- graphs (Graph, graph.py:17-100) -------------------------------- */
+/* Uploads a CSR graph. row_offsets is int64[n+1]; adjacency/edge_weights
+ * have nnz = row_offsets[n] entries; vertex_weights has n entries. */
+int jet_graph_upload(jet_ctx* ctx, int64_t n, const int64_t* row_offsets,
+                     const void* adjacency, int adj_dtype,
+                     const void* edge_weights, int ew_dtype,
+                     const void* vertex_weights, int vw_dtype,
+                     jet_graph** out);
+int jet_graph_info(const jet_graph* g, int64_t* n, int64_t* nnz,
+                   int64_t* total_vertex_weight);
+int jet_graph_download(jet_ctx* ctx, const jet_graph* g, int64_t* row_offsets,
+                       int64_t* adjacency, int64_t* edge_weights,
+                       int64_t* vertex_weights);
+void jet_graph_free(jet_graph* g);
+
+/* ---- metrics ---------------------------------------------------------- */
+/* cutsize(graph, parts)  graph.py:215-221 */
+int jet_cutsize(jet_ctx* ctx, const jet_graph* g, const int64_t* parts,
+                int64_t* cut_out);
+/* PartitionState.from_parts weights  graph.py:240-242 */
+int jet_part_weights(jet_ctx* ctx, const jet_graph* g, const int64_t* parts,
+                     int32_t k, int64_t* pw_out);
+
+/* ---- coarsening (coarsen.py) ------------------------------------------ */
+/* match_vertices(graph)  coarsen.py:47-107 */
+int jet_match(jet_ctx* ctx, const jet_graph* g, int64_t* partner_out);
+/* contract(graph, matching)  coarsen.py:110-138 */
+int jet_contract(jet_ctx* ctx, const jet_graph* g, const int64_t* partner,
+                 jet_graph** coarse_out, int64_t* vmap_out);
+/* build_hierarchy(graph, target)  coarsen.py:141-161 (levels[0] = g) */
+int jet_hierarchy_build(jet_ctx* ctx, const jet_graph* g, int64_t target,
+                        jet_hierarchy** out);
+int jet_hierarchy_levels(const jet_hierarchy* h);
+const jet_graph* jet_hierarchy_level(const jet_hierarchy* h, int i);
+int jet_hierarchy_map(jet_ctx* ctx, const jet_hierarchy* h, int i,
+                      int64_t* vmap_out);
+void jet_hierarchy_free(jet_hierarchy* h);
+
+/* project(coarse_state, vmap, fine)  driver.py:32-45 (parts only) */
+int jet_project(jet_ctx* ctx, int64_t n_coarse, const int64_t* coarse_parts,
+                int64_t n_fine, const int64_t* vmap, int64_t* fine_parts_out);
+
+/* ---- Jet refinement (refine.py) --------------------------------------- */
+/* select_destinations  refine.py:78-105. Any output may be NULL. */
+int jet_select_destinations(jet_ctx* ctx, const jet_graph* g,
+                            const int64_t* parts, int32_t k, int64_t* dest,
+                            int64_t* gain, uint8_t* is_boundary,
+                            int64_t* conn_self);
+/* afterburner  refine.py:127-156 */
+int jet_afterburner(jet_ctx* ctx, const jet_graph* g, const int64_t* cand,
+                    int64_t n_cand, const int64_t* parts, const int64_t* dests,
+                    const int64_t* gains, int64_t* out);
+/* jetlp_pass  refine.py:159-183. locks is read and (when locking) rewritten.
+ * Moves are returned in ascending vertex order. */
+int jet_jetlp_pass(jet_ctx* ctx, const jet_graph* g, const int64_t* parts,
+                   int32_t k, uint8_t* locks, int64_t c_num, int64_t c_den,
+                   double c_float, int32_t c_use_float, int32_t afterburner,
+                   int32_t locking, int64_t* move_vertices,
+                   int64_t* move_dests, int64_t* move_gains,
+                   int64_t* n_moves);
+/* weak_rebalance_pass / strong_rebalance_pass  rebalance.py:139-240.
+ * rng is advanced exactly as numpy would. Moves come out in the reference
+ * order (oversized parts ascending, bucket order inside each part).
+ * move_gains = -loss (int-valued for weak, float64 for strong). */
+int jet_rebalance_pass(jet_ctx* ctx, const jet_graph* g, const int64_t* parts,
+                       int32_t k, const int64_t* part_weights, int64_t limit,
+                       int64_t sigma, int32_t sub_buckets, int32_t strong,
+                       jet_pcg64* rng, int64_t* move_vertices,
+                       int64_t* move_dests, double* move_gains,
+                       int64_t* n_moves);
+/* jet_refine(graph, state, config, finest, seed_path=(level,))
+ * refine.py:190-294. parts_out receives the returned state's parts. */
+int jet_refine(jet_ctx* ctx, const jet_graph* g, const int64_t* parts_in,
+               const jet_config* cfg, int32_t finest, int32_t level,
+               int64_t* parts_out, int64_t* pw_out, int64_t* cut_out,
+               jet_level_stats* stats);
+
+/* ---- initial partitioning (initpart.py:70-94; host C++) --------------- */
+int jet_initial_partition(int64_t n, const int64_t* row_offsets,
+                          const int64_t* adjacency, const int64_t* edge_weights,
+                          const int64_t* vertex_weights, int32_t k,
+                          int64_t limit, uint64_t seed, int32_t restarts,
+                          int64_t* parts_out);
+
+/* ---- whole pipeline: partition(graph, config)  driver.py:48-126 -------- */
+int jet_partition(jet_ctx* ctx, int64_t n, const int64_t* row_offsets,
+                  const void* adjacency, int adj_dtype,
+                  const void* edge_weights, int ew_dtype,
+                  const void* vertex_weights, int vw_dtype,
+                  const jet_config* cfg, int64_t* parts_out,
+                  int64_t* part_weights_out, jet_run_stats* stats);
+/* Same pipeline on an already-resident graph (device-timed benchmark leg).
+ * parts_out / part_weights_out may be NULL. */
+int jet_partition_graph(jet_ctx* ctx, const jet_graph* g, const jet_config* cfg,
+                        int64_t* parts_out, int64_t* part_weights_out,
+                        jet_run_stats* stats);
+
+/* ---- numpy RNG restatement (host; used by the controller) ------------- */
+/* default_rng(entropy words).bit_generator.state */
+int jet_rng_seed(const uint32_t* words, int32_t n_words, jet_pcg64* out);
+/* Generator.integers(0, high, size=count) into out (int64). */
+int jet_rng_integers(jet_pcg64* rng, int64_t high, int64_t count,
+                     int64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* JET_H */

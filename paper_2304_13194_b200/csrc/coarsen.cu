@@ -1,0 +1,845 @@
+// coarsen.cu — heavy-edge + two-hop matching and CSR contraction.
+//
+// match_vertices (coarsen.py:47-107) is sequential in the reference: phase 1
+// resolves the proposal snapshot with an ascending-id scan, phase 2 walks
+// (centre, vertex) pairs in lexicographic order. Both are reproduced exactly
+// by parallel rounds:
+//   phase 1: a proposal edge (v -> u) is accepted iff its proposer id v is
+//            the minimum over all live proposal edges touching v or u
+//            (greedy matching in a fixed priority order == local-minimum
+//            rounds);
+//   phase 2: a centre is processed once it is the smallest unprocessed centre
+//            of every still-unmatched leftover it holds; centres holding at
+//            most one unmatched leftover can never pair anything and retire.
+// contract (coarsen.py:110-138): coarse ids ascending by lowest member,
+// rows merged per coarse vertex, sorted by neighbour and de-duplicated with
+// summed weights, self loops dropped.
+#include "coarsen.cuh"
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_run_length_encode.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+#include <cub/block/block_scan.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+
+namespace jet {
+
+constexpr int INF32 = 0x7f7f7f7f;  // memset(0x7f) pattern, > any vertex id
+
+// ---------------------------------------------------------------------------
+// Phase 1: proposals. score = (w, -u) maximised over free neighbours
+// (coarsen.py:68-73).
+template <int G, bool UNIT>
+__global__ void __launch_bounds__(256)
+    k_propose(GView g, const int32_t* __restrict__ list, int64_t cnt,
+              const int32_t* __restrict__ partner, int32_t* prop, int32_t* elist,
+              unsigned long long* ecnt) {
+  const unsigned gm = group_mask<G>();
+  const int gl = threadIdx.x & (G - 1);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x / G;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G; i < cnt; i += stride) {
+    const int v = list ? list[i] : (int)i;
+    if (partner[v] >= 0) continue;  // uniform per group
+    const int64_t b = g.offs[v], e = g.offs[v + 1];
+    unsigned long long best = 0;
+    for (int64_t j = b + gl; j < e; j += G) {
+      const int u = g.adj[j];
+      if (partner[u] < 0) {
+        const unsigned long long w = UNIT ? 1ull : (unsigned long long)g.ew[j];
+        const unsigned long long key = (w << 32) | (unsigned)(0xffffffffu - (unsigned)u);
+        best = key > best ? key : best;
+      }
+    }
+    best = gmax<G>(best, gm);
+    if (gl == 0) {
+      const int u = best ? (int)(0xffffffffu - (unsigned)(best & 0xffffffffu)) : -1;
+      prop[v] = u;
+      warp_append(u >= 0, v, elist, ecnt);
+    }
+  }
+}
+
+// One resolution round, part A: reset last round's minima, test liveness,
+// scatter proposer ids to both endpoints with atomicMin.
+__global__ void k_round_a(const int32_t* __restrict__ prop, const int32_t* __restrict__ partner,
+                          const int32_t* __restrict__ in, const unsigned long long* __restrict__ in_cnt,
+                          int32_t* mn_cur, int32_t* mn_prev, int32_t* out,
+                          unsigned long long* out_cnt) {
+  const int64_t cnt = (int64_t)*in_cnt;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t lim = (cnt + blockDim.x - 1) / blockDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < lim; i += stride) {
+    bool alive = false;
+    int v = 0;
+    if (i < cnt) {
+      v = in[i];
+      const int u = prop[v];
+      mn_prev[v] = INF32;
+      mn_prev[u] = INF32;
+      alive = partner[v] < 0 && partner[u] < 0;
+      if (alive) {
+        atomicMin(&mn_cur[v], v);
+        atomicMin(&mn_cur[u], v);
+      }
+    }
+    warp_append(alive, v, out, out_cnt);
+  }
+}
+
+// Part B: accept edges that are the minimum at both endpoints.
+__global__ void k_round_b(const int32_t* __restrict__ prop, int32_t* partner,
+                          const int32_t* __restrict__ list,
+                          const unsigned long long* __restrict__ cnt_ptr,
+                          const int32_t* __restrict__ mn_cur, unsigned long long* reset_cnt) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *reset_cnt = 0;
+  const int64_t cnt = (int64_t)*cnt_ptr;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += stride) {
+    const int v = list[i];
+    const int u = prop[v];
+    if (mn_cur[v] == v && mn_cur[u] == v) {
+      partner[v] = u;
+      partner[u] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Phase 2 (two-hop): members of each centre are its leftover neighbours in
+// ascending id order.
+__global__ void k_leftover_deg(const int32_t* __restrict__ left, int64_t nl,
+                               const int64_t* __restrict__ offs, int64_t* deg) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl; i += stride) {
+    const int v = left[i];
+    deg[i] = offs[v + 1] - offs[v];
+  }
+}
+
+__global__ void k_leftover_pairs(const int32_t* __restrict__ left, int64_t nl,
+                                 GView g, const int64_t* __restrict__ poff,
+                                 int32_t* keys, int32_t* vals) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = w0; i < nl; i += ws) {
+    const int v = left[i];
+    const int64_t b = g.offs[v], e = g.offs[v + 1], o = poff[i];
+    for (int64_t j = b + lane; j < e; j += 32) {
+      keys[o + (j - b)] = g.adj[j];
+      vals[o + (j - b)] = v;
+    }
+  }
+}
+
+struct TwoHop {
+  int32_t* partner;
+  const int32_t* centres;   // centre vertex id per centre index
+  const int64_t* coff;      // member offsets per centre index (nc + 1)
+  const int32_t* members;   // leftover ids, ascending within each centre
+  uint8_t* cact;            // per vertex id: 1 while the centre is active
+  uint8_t* ready;           // per centre index
+  int32_t* minc;            // per vertex id (leftovers only)
+  int64_t nc;
+};
+
+// Retire centres with <= 1 unmatched member; count the remaining active.
+__global__ void k_th_retire(TwoHop t, unsigned long long* active) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  long long act = 0;
+  for (int64_t ci = w0; ci < t.nc; ci += ws) {
+    const int c = t.centres[ci];
+    if (!t.cact[c]) continue;
+    const int64_t b = t.coff[ci], e = t.coff[ci + 1];
+    int un = 0;
+    for (int64_t j0 = b; j0 < e && un < 2; j0 += 32) {
+      const int64_t j = j0 + lane;
+      const bool u = j < e && t.partner[t.members[j]] < 0;
+      un += __popc(__ballot_sync(0xffffffffu, u));
+    }
+    if (un <= 1) {
+      if (lane == 0) t.cact[c] = 0;
+    } else if (lane == 0) {
+      act++;
+    }
+  }
+  if (lane == 0 && act) atomicAdd(active, (unsigned long long)act);
+}
+
+// minc[v] = smallest active centre adjacent to unmatched leftover v.
+__global__ void k_th_minc(TwoHop t, GView g, const int32_t* __restrict__ left, int64_t nl) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = w0; i < nl; i += ws) {
+    const int v = left[i];
+    if (t.partner[v] >= 0) continue;
+    const int64_t b = g.offs[v], e = g.offs[v + 1];
+    int m = INF32;
+    for (int64_t j = b + lane; j < e; j += 32) {
+      const int c = g.adj[j];
+      if (t.cact[c] && c < m) m = c;
+    }
+    m = gmin<32>(m, 0xffffffffu);
+    if (lane == 0) t.minc[v] = m;
+  }
+}
+
+__global__ void k_th_ready(TwoHop t) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t ci = w0; ci < t.nc; ci += ws) {
+    const int c = t.centres[ci];
+    bool ok = t.cact[c] != 0;
+    if (ok) {
+      const int64_t b = t.coff[ci], e = t.coff[ci + 1];
+      for (int64_t j0 = b; j0 < e && ok; j0 += 32) {
+        const int64_t j = j0 + lane;
+        bool bad = false;
+        if (j < e) {
+          const int v = t.members[j];
+          bad = t.partner[v] < 0 && t.minc[v] != c;
+        }
+        ok = !__any_sync(0xffffffffu, bad);
+      }
+    }
+    if (lane == 0) t.ready[ci] = ok;
+  }
+}
+
+// Ready centres pair their unmatched members consecutively (coarsen.py:95-103).
+__global__ void k_th_pair(TwoHop t) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t ci = w0; ci < t.nc; ci += ws) {
+    if (!t.ready[ci]) continue;
+    const int c = t.centres[ci];
+    const int64_t b = t.coff[ci], e = t.coff[ci + 1];
+    int pending = -1;
+    for (int64_t j0 = b; j0 < e; j0 += 32) {
+      const int64_t j = j0 + lane;
+      int v = -1;
+      bool un = false;
+      if (j < e) {
+        v = t.members[j];
+        un = t.partner[v] < 0;
+      }
+      const unsigned um = __ballot_sync(0xffffffffu, un);
+      const int off = pending >= 0 ? 1 : 0;
+      const unsigned below = um & lanemask_lt();
+      const int pos = __popc(below) + off;  // position in (pending, unmatched...)
+      int mate = -1;
+      const int src = below ? 31 - __clz(below) : lane;
+      const int vprev = __shfl_sync(0xffffffffu, v, src);
+      if (un && (pos & 1)) mate = below ? vprev : pending;
+      __syncwarp();
+      if (mate >= 0) {
+        t.partner[v] = mate;
+        t.partner[mate] = v;
+      }
+      const int total = __popc(um) + off;
+      if (total & 1) {
+        const int last = um ? 31 - __clz(um) : -1;
+        const int lv = __shfl_sync(0xffffffffu, v, last >= 0 ? last : 0);
+        pending = last >= 0 ? lv : pending;
+      } else {
+        pending = -1;
+      }
+      __syncwarp();
+    }
+    if (lane == 0) t.cact[c] = 0;
+  }
+}
+
+__global__ void k_singletons(int32_t* partner, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride)
+    if (partner[v] < 0) partner[v] = (int32_t)v;
+}
+
+__global__ void k_fill(int32_t* p, int64_t n, int32_t val) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) p[i] = val;
+}
+
+struct IsFree {
+  const int32_t* partner;
+  __device__ __forceinline__ bool operator()(const int32_t& v) const { return partner[v] < 0; }
+};
+
+__global__ void k_th_mark(const int32_t* __restrict__ cs, int64_t nc, uint8_t* cact) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc; i += stride) cact[cs[i]] = 1;
+}
+void th_mark(Ctx& c, const int32_t* cs, int64_t nc, uint8_t* cact) {
+  launch(c, "th_mark", 5.0 * nc, [&] {
+    k_th_mark<<<grid_for(c, nc, 256), 256, 0, c.stream>>>(cs, nc, cact);
+  });
+}
+
+static int bits_for(int64_t x) {
+  int b = 1;
+  while ((1LL << b) <= x) ++b;
+  return b;
+}
+
+static void two_hop(Ctx& c, const DGraph& g, int32_t* partner) {
+  const int64_t n = g.n;
+  DBuf<int32_t> left(n, c.stream);
+  DBuf<int64_t> nsel(1, c.stream);
+  {
+    cub::CountingInputIterator<int32_t> it(0);
+    IsFree op{partner};
+    size_t tmp = 0;
+    CK(cub::DeviceSelect::If(nullptr, tmp, it, left.get(), nsel.get(), (int)n, op, c.stream));
+    void* p = c.cub_scratch(tmp);
+    launch(c, "th_leftovers", 8.0 * n, [&] {
+      CK(cub::DeviceSelect::If(p, tmp, it, left.get(), nsel.get(), (int)n, op, c.stream));
+    });
+  }
+  int64_t nl = 0;
+  d2h(c, &nl, nsel.get(), 1);
+  c.sync();
+  if (nl == 0) return;
+  DBuf<int64_t> deg(nl + 1, c.stream), poff(nl + 1, c.stream);
+  dzero(c, deg.get() + nl, 1);
+  launch(c, "th_deg", 20.0 * nl, [&] {
+    k_leftover_deg<<<grid_for(c, nl, 256), 256, 0, c.stream>>>(left.get(), nl, g.offs.get(), deg.get());
+  });
+  {
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, deg.get(), poff.get(), (int)(nl + 1), c.stream));
+    void* p = c.cub_scratch(tmp);
+    launch(c, "th_scan", 16.0 * nl, [&] {
+      CK(cub::DeviceScan::ExclusiveSum(p, tmp, deg.get(), poff.get(), (int)(nl + 1), c.stream));
+    });
+  }
+  int64_t np = 0;
+  d2h(c, &np, poff.get() + nl, 1);
+  c.sync();
+  if (np == 0) return;
+  const GView gv = view(g);
+  DBuf<int32_t> k0(np, c.stream), v0(np, c.stream), k1(np, c.stream), v1(np, c.stream);
+  launch(c, "th_pairs", 16.0 * np, [&] {
+    k_leftover_pairs<<<grid_for(c, nl * 32, 256), 256, 0, c.stream>>>(left.get(), nl, gv, poff.get(),
+                                                                     k0.get(), v0.get());
+  });
+  {
+    size_t tmp = 0;
+    const int eb = bits_for(n);
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k0.get(), k1.get(), v0.get(), v1.get(), (int)np, 0,
+                                       eb, c.stream));
+    void* p = c.cub_scratch(tmp);
+    launch(c, "th_sort", 32.0 * np, [&] {
+      CK(cub::DeviceRadixSort::SortPairs(p, tmp, k0.get(), k1.get(), v0.get(), v1.get(), (int)np, 0, eb,
+                                         c.stream));
+    });
+  }
+  // centres = runs of equal keys
+  DBuf<int32_t> centres(np, c.stream);
+  DBuf<int64_t> ccnt(np + 1, c.stream), coff(np + 1, c.stream);
+  DBuf<int64_t> nruns(1, c.stream);
+  {
+    size_t tmp = 0;
+    CK(cub::DeviceRunLengthEncode::Encode(nullptr, tmp, k1.get(), centres.get(), ccnt.get(), nruns.get(),
+                                          (int)np, c.stream));
+    void* p = c.cub_scratch(tmp);
+    launch(c, "th_rle", 12.0 * np, [&] {
+      CK(cub::DeviceRunLengthEncode::Encode(p, tmp, k1.get(), centres.get(), ccnt.get(), nruns.get(),
+                                            (int)np, c.stream));
+    });
+  }
+  int64_t nc = 0;
+  d2h(c, &nc, nruns.get(), 1);
+  c.sync();
+  dzero(c, ccnt.get() + nc, 1);
+  {
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ccnt.get(), coff.get(), (int)(nc + 1), c.stream));
+    void* p = c.cub_scratch(tmp);
+    launch(c, "th_scan", 16.0 * nc, [&] {
+      CK(cub::DeviceScan::ExclusiveSum(p, tmp, ccnt.get(), coff.get(), (int)(nc + 1), c.stream));
+    });
+  }
+  DBuf<uint8_t> cact(n, c.stream), ready(nc, c.stream);
+  DBuf<int32_t> minc(n, c.stream);
+  dzero(c, cact.get(), n);
+  th_mark(c, centres.get(), nc, cact.get());
+  TwoHop t{partner, centres.get(), coff.get(), v1.get(), cact.get(), ready.get(), minc.get(), nc};
+  DBuf<unsigned long long> act(1, c.stream);
+  const unsigned gw = grid_for(c, nc * 32, 256);
+  const unsigned gl = grid_for(c, nl * 32, 256);
+  int batch = 1;
+  while (true) {
+    for (int r = 0; r < batch; ++r) {
+      dzero(c, act.get(), 1);
+      launch(c, "th_retire", 0.0, [&] { k_th_retire<<<gw, 256, 0, c.stream>>>(t, act.get()); });
+      launch(c, "th_minc", 0.0, [&] { k_th_minc<<<gl, 256, 0, c.stream>>>(t, gv, left.get(), nl); });
+      launch(c, "th_ready", 0.0, [&] { k_th_ready<<<gw, 256, 0, c.stream>>>(t); });
+      launch(c, "th_pair", 0.0, [&] { k_th_pair<<<gw, 256, 0, c.stream>>>(t); });
+    }
+    unsigned long long h = 0;
+    d2h(c, &h, act.get(), 1);
+    c.sync();
+    if (h == 0) break;
+    batch = batch < 16 ? batch * 2 : 16;
+  }
+}
+
+void device_match(Ctx& c, const DGraph& g, int32_t* partner) {
+  const int64_t n = g.n;
+  launch(c, "fill", 4.0 * n, [&] {
+    k_fill<<<grid_for(c, n, 256), 256, 0, c.stream>>>(partner, n, -1);
+  });
+  if (g.nnz > 0) {
+    DBuf<int32_t> prop(n, c.stream), lists(2 * n, c.stream), mn(2 * n, c.stream);
+    DBuf<unsigned long long> cnt(2, c.stream);
+    CK(cudaMemsetAsync(mn.get(), 0x7f, 2 * n * sizeof(int32_t), c.stream));
+    const GView gv = view(g);
+    while (true) {
+      dzero(c, cnt.get(), 2);
+      for (int t = 0; t < NBINS; ++t) {
+        const int64_t bc = g.bin_cnt[t];
+        if (!bc) continue;
+        const int G = t < 4 ? TIER_G[t] : 32;
+        const int32_t* list = tier_list(g, t);
+        const unsigned grid = grid_for(c, bc * G, 256);
+        launch(c, "propose", (g.unit_ew ? 8.0 : 12.0) * g.bin_nnz[t] + 12.0 * bc, [&] {
+          JET_TIER_LAUNCH(k_propose, G, g.unit_ew, grid, 256, 0, c.stream, gv, list, bc, partner,
+                          prop.get(), lists.get(), cnt.get());
+        });
+      }
+      unsigned long long ne = 0;
+      d2h(c, &ne, cnt.get(), 1);
+      c.sync();
+      if (ne == 0) break;
+      // resolution rounds: list r%2 holds the live edges of round r
+      int r = 1, batch = 1;
+      const unsigned grid = grid_for(c, (int64_t)ne, 256);
+      while (true) {
+        for (int q = 0; q < batch; ++q, ++r) {
+          const int in = (r - 1) & 1, out = r & 1;
+          int32_t* mcur = mn.get() + (size_t)out * n;
+          int32_t* mprev = mn.get() + (size_t)in * n;
+          launch(c, "match_round", 0.0, [&] {
+            k_round_a<<<grid, 256, 0, c.stream>>>(prop.get(), partner, lists.get() + (size_t)in * n,
+                                                  cnt.get() + in, mcur, mprev,
+                                                  lists.get() + (size_t)out * n, cnt.get() + out);
+          });
+          launch(c, "match_round", 0.0, [&] {
+            k_round_b<<<grid, 256, 0, c.stream>>>(prop.get(), partner, lists.get() + (size_t)out * n,
+                                                  cnt.get() + out, mcur, cnt.get() + in);
+          });
+        }
+        unsigned long long live = 0;
+        d2h(c, &live, cnt.get() + ((r - 1) & 1), 1);
+        c.sync();
+        if (live == 0) break;
+        batch = batch < 16 ? batch * 2 : 16;
+      }
+      // one more A-pass with an empty list is not needed: the last round
+      // that produced live edges was followed by a round that reset them.
+    }
+    two_hop(c, g, partner);
+  }
+  launch(c, "singletons", 8.0 * n, [&] {
+    k_singletons<<<grid_for(c, n, 256), 256, 0, c.stream>>>(partner, n);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Contraction
+__global__ void k_is_rep(const int32_t* __restrict__ partner, int64_t n, int32_t* flag) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride)
+    flag[v] = partner[v] >= v ? 1 : 0;
+}
+
+struct CoarseMap {
+  const int32_t* partner;
+  const int32_t* cid;  // exclusive scan of rep flags
+  const int64_t* offs;
+  const int32_t* vw;
+  int32_t* vmap;
+  int32_t* cvw;
+  int32_t* mem_a;
+  int32_t* mem_b;
+  int64_t* rowlen;  // deg(a) + deg(b)
+  unsigned* overflow;
+};
+
+__global__ void k_coarse_map(CoarseMap m, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride) {
+    const int p = m.partner[v];
+    const int rep = p < v ? p : (int)v;
+    const int c = m.cid[rep];
+    m.vmap[v] = c;
+    if (rep == v) {
+      long long w = m.vw[v];
+      int64_t d = m.offs[v + 1] - m.offs[v];
+      if (p != v) {
+        w += m.vw[p];
+        d += m.offs[p + 1] - m.offs[p];
+      }
+      if (w > 2147483647LL) atomicOr(m.overflow, 1u);
+      m.cvw[c] = (int32_t)w;
+      m.mem_a[c] = (int32_t)v;
+      m.mem_b[c] = p;
+      m.rowlen[c] = d;
+    }
+  }
+}
+
+template <int E>
+__device__ __forceinline__ void warp_bitonic(unsigned long long (&x)[E]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32 * E; size <<= 1) {
+#pragma unroll
+    for (int stride = size / 2; stride > 0; stride >>= 1) {
+      if (stride >= 32) {
+        const int rs = stride / 32;
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const int pr = r ^ rs;
+          if (pr > r) {
+            const bool asc = (((r * 32 + lane) & size) == 0);
+            const unsigned long long a = x[r], b = x[pr];
+            if ((a > b) == asc) {
+              x[r] = b;
+              x[pr] = a;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const unsigned long long y = __shfl_xor_sync(0xffffffffu, x[r], stride);
+          const bool asc = (((r * 32 + lane) & size) == 0);
+          const bool lower = (lane & stride) == 0;
+          const unsigned long long lo = x[r] < y ? x[r] : y, hi = x[r] < y ? y : x[r];
+          x[r] = (lower == asc) ? lo : hi;
+        }
+      }
+    }
+  }
+}
+
+struct RowMerge {
+  const int64_t* offs;
+  const int32_t* adj;
+  const int32_t* ew;
+  const int32_t* vmap;
+  const int32_t* mem_a;
+  const int32_t* mem_b;
+  const int64_t* toff;  // staging offsets (exclusive scan of rowlen)
+  const int64_t* rowlen;
+  int32_t* tadj;
+  int32_t* tew;
+  int64_t* cdeg;
+  int32_t* big;  // rows longer than 256 entries
+  unsigned long long* big_cnt;
+  unsigned* overflow;
+  int64_t nc;
+};
+
+// gather row entries of member x of coarse vertex c as sort keys
+__device__ __forceinline__ unsigned long long merged_key(const RowMerge& m, int c, int64_t idx,
+                                                         int a, int b, int64_t da) {
+  const int x = idx < da ? a : b;
+  const int64_t j = m.offs[x] + (idx < da ? idx : idx - da);
+  const int cv = m.vmap[m.adj[j]];
+  if (cv == c) return ~0ull;  // contraction self loop (coarsen.py:133)
+  return ((unsigned long long)(unsigned)cv << 32) | (unsigned)m.ew[j];
+}
+
+template <int E>
+__device__ void merge_row_warp(const RowMerge& m, int c, unsigned long long* sbuf) {
+  const int lane = threadIdx.x & 31;
+  const int a = m.mem_a[c], b = m.mem_b[c];
+  const int64_t da = m.offs[a + 1] - m.offs[a];
+  const int64_t d = m.rowlen[c];
+  unsigned long long x[E];
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const int64_t idx = r * 32 + lane;
+    x[r] = idx < d ? merged_key(m, c, idx, a, b, da) : ~0ull;
+  }
+  warp_bitonic<E>(x);
+#pragma unroll
+  for (int r = 0; r < E; ++r) sbuf[r * 32 + lane] = x[r];
+  __syncwarp();
+  const int64_t base = m.toff[c];
+  int outn = 0;
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const int i = r * 32 + lane;
+    const unsigned long long k = sbuf[i];
+    const unsigned cv = (unsigned)(k >> 32);
+    const bool head = k != ~0ull && (i == 0 || (unsigned)(sbuf[i - 1] >> 32) != cv);
+    long long sum = 0;
+    if (head) {
+      for (int q = i; q < 32 * E && sbuf[q] != ~0ull && (unsigned)(sbuf[q] >> 32) == cv; ++q)
+        sum += (long long)(sbuf[q] & 0xffffffffu);
+    }
+    const unsigned hm = __ballot_sync(0xffffffffu, head);
+    if (head) {
+      const int pos = outn + __popc(hm & lanemask_lt());
+      m.tadj[base + pos] = (int32_t)cv;
+      if (sum > 2147483647LL) atomicOr(m.overflow, 2u);
+      m.tew[base + pos] = (int32_t)sum;
+    }
+    outn += __popc(hm);
+  }
+  if (lane == 0) m.cdeg[c] = outn;
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(256) k_merge_rows(RowMerge m) {
+  __shared__ unsigned long long sbuf[8][256];
+  const int wib = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = w0; c < m.nc; c += ws) {
+    const int64_t d = m.rowlen[c];
+    if (d <= 32) merge_row_warp<1>(m, (int)c, sbuf[wib]);
+    else if (d <= 64) merge_row_warp<2>(m, (int)c, sbuf[wib]);
+    else if (d <= 128) merge_row_warp<4>(m, (int)c, sbuf[wib]);
+    else if (d <= 256) merge_row_warp<8>(m, (int)c, sbuf[wib]);
+    else {
+      if (lane == 0) {
+        const unsigned long long i = atomicAdd(m.big_cnt, 1ull);
+        m.big[i] = (int32_t)c;
+      }
+    }
+  }
+}
+
+// long rows: gather keys into a segmented buffer for a library segmented sort
+__global__ void k_big_gather(RowMerge m, const int32_t* __restrict__ big, int64_t nbig,
+                             const int64_t* __restrict__ boff, unsigned long long* keys) {
+  for (int64_t i = blockIdx.x; i < nbig; i += gridDim.x) {
+    const int c = big[i];
+    const int a = m.mem_a[c], b = m.mem_b[c];
+    const int64_t da = m.offs[a + 1] - m.offs[a];
+    const int64_t d = m.rowlen[c];
+    const int64_t o = boff[i];
+    for (int64_t idx = threadIdx.x; idx < d; idx += blockDim.x) keys[o + idx] = merged_key(m, c, idx, a, b, da);
+  }
+}
+
+__global__ void k_big_len(const int32_t* __restrict__ big, int64_t nbig,
+                          const int64_t* __restrict__ rowlen, int64_t* len) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nbig; i += stride)
+    len[i] = rowlen[big[i]];
+}
+
+__global__ void __launch_bounds__(256)
+    k_big_dedup(RowMerge m, const int32_t* __restrict__ big, int64_t nbig,
+                const int64_t* __restrict__ boff, const unsigned long long* __restrict__ keys) {
+  typedef cub::BlockScan<int, 256> BS;
+  __shared__ typename BS::TempStorage ts;
+  __shared__ int s_out;
+  for (int64_t i = blockIdx.x; i < nbig; i += gridDim.x) {
+    const int c = big[i];
+    const int64_t o = boff[i], d = m.rowlen[c];
+    const int64_t base = m.toff[c];
+    if (threadIdx.x == 0) s_out = 0;
+    __syncthreads();
+    for (int64_t j0 = 0; j0 < d; j0 += 256) {
+      const int64_t j = j0 + threadIdx.x;
+      bool head = false;
+      unsigned cv = 0;
+      long long sum = 0;
+      if (j < d) {
+        const unsigned long long k = keys[o + j];
+        cv = (unsigned)(k >> 32);
+        head = k != ~0ull && (j == 0 || (unsigned)(keys[o + j - 1] >> 32) != cv);
+        if (head)
+          for (int64_t q = j; q < d && keys[o + q] != ~0ull && (unsigned)(keys[o + q] >> 32) == cv; ++q)
+            sum += (long long)(keys[o + q] & 0xffffffffu);
+      }
+      int rank, total;
+      BS(ts).ExclusiveSum(head ? 1 : 0, rank, total);
+      const int run = s_out;
+      if (head) {
+        m.tadj[base + run + rank] = (int32_t)cv;
+        if (sum > 2147483647LL) atomicOr(m.overflow, 2u);
+        m.tew[base + run + rank] = (int32_t)sum;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) s_out = run + total;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) m.cdeg[c] = s_out;
+    __syncthreads();
+  }
+}
+
+__global__ void k_copy_rows(const int64_t* __restrict__ toff, const int64_t* __restrict__ coffs,
+                            const int32_t* __restrict__ tadj, const int32_t* __restrict__ tew,
+                            int32_t* cadj, int32_t* cew, int64_t nc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = w0; c < nc; c += ws) {
+    const int64_t s = toff[c], o = coffs[c], d = coffs[c + 1] - o;
+    for (int64_t j = lane; j < d; j += 32) {
+      cadj[o + j] = tadj[s + j];
+      cew[o + j] = tew[s + j];
+    }
+  }
+}
+
+std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* partner,
+                                        int32_t* vmap) {
+  const int64_t n = g.n;
+  DBuf<int32_t> flag(n, c.stream), cid(n, c.stream);
+  launch(c, "is_rep", 8.0 * n, [&] {
+    k_is_rep<<<grid_for(c, n, 256), 256, 0, c.stream>>>(partner, n, flag.get());
+  });
+  {
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag.get(), cid.get(), (int)n, c.stream));
+    void* p = c.cub_scratch(tmp);
+    launch(c, "rep_scan", 8.0 * n, [&] {
+      CK(cub::DeviceScan::ExclusiveSum(p, tmp, flag.get(), cid.get(), (int)n, c.stream));
+    });
+  }
+  int32_t last[2];
+  d2h(c, &last[0], cid.get() + n - 1, 1);
+  d2h(c, &last[1], flag.get() + n - 1, 1);
+  c.sync();
+  const int64_t nc = (int64_t)last[0] + last[1];
+  auto cg_ = std::make_unique<DGraph>();
+  cg_->n = nc;
+  cg_->vw.alloc(nc, c.stream);
+  DBuf<int32_t> mem_a(nc, c.stream), mem_b(nc, c.stream);
+  DBuf<int64_t> rowlen(nc + 1, c.stream), toff(nc + 1, c.stream), cdeg(nc + 1, c.stream);
+  DBuf<unsigned> ovf(1, c.stream);
+  dzero(c, ovf.get(), 1);
+  CoarseMap cm{partner, cid.get(), g.offs.get(), g.vw.get(), vmap, cg_->vw.get(),
+               mem_a.get(), mem_b.get(), rowlen.get(), ovf.get()};
+  launch(c, "coarse_map", 24.0 * n, [&] {
+    k_coarse_map<<<grid_for(c, n, 256), 256, 0, c.stream>>>(cm, n);
+  });
+  dzero(c, rowlen.get() + nc, 1);
+  dzero(c, cdeg.get() + nc, 1);
+  {
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, rowlen.get(), toff.get(), (int)(nc + 1), c.stream));
+    void* p = c.cub_scratch(tmp);
+    launch(c, "rowlen_scan", 16.0 * nc, [&] {
+      CK(cub::DeviceScan::ExclusiveSum(p, tmp, rowlen.get(), toff.get(), (int)(nc + 1), c.stream));
+    });
+  }
+  int64_t T = 0;
+  d2h(c, &T, toff.get() + nc, 1);
+  c.sync();
+  DBuf<int32_t> tadj(T > 0 ? T : 1, c.stream), tew(T > 0 ? T : 1, c.stream), big(nc, c.stream);
+  DBuf<unsigned long long> big_cnt(1, c.stream);
+  dzero(c, big_cnt.get(), 1);
+  RowMerge rm{g.offs.get(), g.adj.get(), g.ew.get(), vmap, mem_a.get(), mem_b.get(), toff.get(),
+              rowlen.get(), tadj.get(), tew.get(), cdeg.get(), big.get(), big_cnt.get(), ovf.get(), nc};
+  launch(c, "contract_rows", 12.0 * g.nnz + 8.0 * T + 16.0 * nc, [&] {
+    k_merge_rows<<<grid_for(c, nc * 32, 256), 256, 0, c.stream>>>(rm);
+  });
+  unsigned long long nbig = 0;
+  d2h(c, &nbig, big_cnt.get(), 1);
+  c.sync();
+  if (nbig > 0) {
+    const int64_t nb = (int64_t)nbig;
+    DBuf<int64_t> blen(nb + 1, c.stream), boff(nb + 1, c.stream);
+    dzero(c, blen.get() + nb, 1);
+    launch(c, "big_len", 16.0 * nb, [&] {
+      k_big_len<<<grid_for(c, nb, 256), 256, 0, c.stream>>>(big.get(), nb, rowlen.get(), blen.get());
+    });
+    {
+      size_t tmp = 0;
+      CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, blen.get(), boff.get(), (int)(nb + 1), c.stream));
+      void* p = c.cub_scratch(tmp);
+      launch(c, "big_scan", 16.0 * nb, [&] {
+        CK(cub::DeviceScan::ExclusiveSum(p, tmp, blen.get(), boff.get(), (int)(nb + 1), c.stream));
+      });
+    }
+    int64_t BT = 0;
+    d2h(c, &BT, boff.get() + nb, 1);
+    c.sync();
+    DBuf<unsigned long long> bk(BT, c.stream), bk2(BT, c.stream);
+    launch(c, "big_gather", 20.0 * BT, [&] {
+      k_big_gather<<<grid_for(c, nb * 256, 256), 256, 0, c.stream>>>(rm, big.get(), nb, boff.get(), bk.get());
+    });
+    {
+      size_t tmp = 0;
+      CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, bk.get(), bk2.get(), (int)BT, (int)nb, boff.get(),
+                                            boff.get() + 1, c.stream));
+      void* p = c.cub_scratch(tmp);
+      launch(c, "big_sort", 32.0 * BT, [&] {
+        CK(cub::DeviceSegmentedSort::SortKeys(p, tmp, bk.get(), bk2.get(), (int)BT, (int)nb, boff.get(),
+                                              boff.get() + 1, c.stream));
+      });
+    }
+    launch(c, "big_dedup", 16.0 * BT, [&] {
+      k_big_dedup<<<grid_for(c, nb * 256, 256), 256, 0, c.stream>>>(rm, big.get(), nb, boff.get(), bk2.get());
+    });
+  }
+  // final offsets
+  cg_->offs.alloc(nc + 1, c.stream);
+  {
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cdeg.get(), cg_->offs.get(), (int)(nc + 1), c.stream));
+    void* p = c.cub_scratch(tmp);
+    launch(c, "cdeg_scan", 16.0 * nc, [&] {
+      CK(cub::DeviceScan::ExclusiveSum(p, tmp, cdeg.get(), cg_->offs.get(), (int)(nc + 1), c.stream));
+    });
+  }
+  int64_t cnnz = 0;
+  unsigned hovf = 0;
+  d2h(c, &cnnz, cg_->offs.get() + nc, 1);
+  d2h(c, &hovf, ovf.get(), 1);
+  c.sync();
+  JET_REQUIRE(!(hovf & 1u), JET_EUNSUPPORTED, "coarse vertex weight exceeds int32");
+  JET_REQUIRE(!(hovf & 2u), JET_EUNSUPPORTED, "coarse edge weight exceeds int32");
+  cg_->nnz = cnnz;
+  cg_->adj.alloc(cnnz > 0 ? cnnz : 1, c.stream);
+  cg_->ew.alloc(cnnz > 0 ? cnnz : 1, c.stream);
+  launch(c, "copy_rows", 16.0 * cnnz + 16.0 * nc, [&] {
+    k_copy_rows<<<grid_for(c, nc * 32, 256), 256, 0, c.stream>>>(toff.get(), cg_->offs.get(), tadj.get(),
+                                                                tew.get(), cg_->adj.get(), cg_->ew.get(), nc);
+  });
+  finalize_graph(c, *cg_);
+  return cg_;
+}
+
+// build_hierarchy (coarsen.py:141-161; MAX_LEVELS 64, stagnation 0.95 twice)
+void device_build_hierarchy(Ctx& c, const DGraph& g0, int64_t target, Hierarchy& h) {
+  h.base = &g0;
+  h.owned.clear();
+  h.maps.clear();
+  int stagnant = 0;
+  const DGraph* fine = &g0;
+  DBuf<int32_t> partner;
+  while (fine->n > target && (int)h.owned.size() + 1 < 64) {
+    partner.ensure(fine->n, c.stream);
+    device_match(c, *fine, partner.get());
+    DBuf<int32_t> vmap(fine->n, c.stream);
+    auto coarse = device_contract(c, *fine, partner.get(), vmap.get());
+    if (coarse->n == fine->n) break;
+    const bool stag = (double)coarse->n > 0.95 * (double)fine->n;
+    h.maps.push_back(std::move(vmap));
+    h.owned.push_back(std::move(coarse));
+    fine = h.owned.back().get();
+    stagnant = stag ? stagnant + 1 : 0;
+    if (stagnant >= 2) break;
+  }
+}
+
+}  // namespace jet

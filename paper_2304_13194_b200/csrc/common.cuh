@@ -1,0 +1,305 @@
+// common.cuh — shared infrastructure for the sm_100a Jet partitioner.
+//
+// Layout in HBM (one CSR level):
+//   offs  int64[n+1]   row offsets (int64: R-MAT-27 has > 2^31 entries)
+//   adj   int32[nnz]   neighbour ids, rows sorted ascending (graph.py:109)
+//   ew    int32[nnz]   edge weights (>= 1)
+//   vw    int32[n]     vertex weights (>= 1)
+// Sums (conn, gains, part weights, cut) are int64, matching the reference's
+// int64 numpy arithmetic (_arrays.py:5).
+#pragma once
+#include <cuda_runtime.h>
+#include <cooperative_groups.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+#include <map>
+#include <stdexcept>
+#include <utility>
+#include "../../include/jet.h"
+
+namespace cg = cooperative_groups;
+
+namespace jet {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file,
+                             int line);
+
+#define CK(x)                                                     \
+  do {                                                            \
+    cudaError_t e_ = (x);                                         \
+    if (e_ != cudaSuccess) ::jet::throw_cuda(e_, #x, __FILE__, __LINE__); \
+  } while (0)
+
+#define JET_REQUIRE(cond, code, msg)          \
+  do {                                        \
+    if (!(cond)) throw ::jet::Error(code, msg); \
+  } while (0)
+
+// Sentinel gain for interior vertices (refine.py:31).
+constexpr long long NO_GAIN = -(1LL << 62);
+// Part ids are packed in the low bits of 64-bit max keys (refine.py:93-98
+// encodes vals*(k+1)+(k-p); we use (conn << KBITS) | (KMASK - p)).
+constexpr int KBITS = 21;
+constexpr int KMASK = (1 << KBITS) - 1;
+
+// Degree tiers. Tiers 0-3 give each vertex a G-lane group (G = 4,8,16,32)
+// that holds the whole row in registers; tier 4 gives a row to one warp with
+// a per-warp shared-memory part table; tier 5 gives a row to a whole block.
+constexpr int NBINS = 6;
+constexpr int BIN_WARP = 4, BIN_BLOCK = 5;
+constexpr int64_t WARP_TIER_MAX_DEG = 2048;
+__host__ __device__ inline int tier_of_degree(int64_t d) {
+  return d <= 4 ? 0 : d <= 8 ? 1 : d <= 16 ? 2 : d <= 32 ? 3
+       : d <= WARP_TIER_MAX_DEG ? 4 : 5;
+}
+constexpr int TIER_G[4] = {4, 8, 16, 32};
+
+// ---------------------------------------------------------------------------
+// Device memory: stream-ordered allocations from the device's default pool
+// (release threshold raised at context creation so freed blocks are reused).
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = 0;
+  DBuf() = default;
+  DBuf(size_t count, cudaStream_t st) { alloc(count, st); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    if (count) {
+      cudaError_t e = cudaMallocAsync((void**)&p, count * sizeof(T), st);
+      if (e != cudaSuccess) {
+        p = nullptr;
+        n = 0;
+        cudaGetLastError();
+        throw Error(JET_ENOMEM, "device allocation of " +
+                                    std::to_string(count * sizeof(T)) +
+                                    " bytes failed: " + cudaGetErrorString(e));
+      }
+    }
+  }
+  // Grow to at least `count` elements; contents are not preserved.
+  void ensure(size_t count, cudaStream_t st) {
+    if (count > n || p == nullptr) alloc(count > 0 ? count : 1, st);
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  T* get() const { return p; }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// ---------------------------------------------------------------------------
+// Device CSR level.
+struct DGraph {
+  int64_t n = 0, nnz = 0, total_vw = 0;
+  int64_t max_deg = 0, max_wdeg = 0, max_ew = 0, max_vw = 0;
+  bool unit_ew = true;
+  DBuf<int64_t> offs;
+  DBuf<int32_t> adj, ew, vw;
+  // degree tiers: ascending vertex lists, or identity when one tier holds all
+  DBuf<int32_t> bin_store;
+  const int32_t* bin_list[NBINS] = {};
+  int64_t bin_cnt[NBINS] = {};
+  int64_t bin_nnz[NBINS] = {};
+  bool identity = false;
+  int identity_bin = -1;
+};
+
+struct Ctx;
+
+// Per-launch profiling record (CUDA events on the context stream).
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+  double bytes;
+};
+struct ProfAgg {
+  std::string name;
+  int64_t launches = 0;
+  double ms = 0, bytes = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int max_smem_optin = 0;
+  int64_t launches = 0;
+  // pinned host mirror for per-iteration scalars
+  int64_t* pinned = nullptr;
+  size_t pinned_elems = 0;
+  // scratch for CUB device-wide primitives
+  DBuf<uint8_t> cub_tmp;
+  // profiling
+  bool prof = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> event_pool;
+  std::vector<ProfAgg> agg;
+  std::map<std::string, int> cls_index;
+  int32_t lock_epoch = 0;
+
+  cudaEvent_t take_event();
+  int prof_class(const char* name);
+  void flush_prof();
+  void ensure_pinned(size_t elems);
+  void sync() { CK(cudaStreamSynchronize(stream)); }
+  void* cub_scratch(size_t bytes) {
+    cub_tmp.ensure(bytes, stream);
+    return cub_tmp.get();
+  }
+};
+
+// Launch wrapper: counts the launch, brackets it with events when profiling,
+// and checks the launch status. `bytes` = algorithmic bytes of the launch.
+template <class F>
+inline void launch(Ctx& c, const char* name, double bytes, F&& f) {
+  ProfRec r{};
+  if (c.prof) {
+    r.cls = c.prof_class(name);
+    r.a = c.take_event();
+    r.b = c.take_event();
+    r.bytes = bytes;
+    CK(cudaEventRecord(r.a, c.stream));
+  }
+  f();
+  CK(cudaGetLastError());
+  c.launches++;
+  if (c.prof) {
+    CK(cudaEventRecord(r.b, c.stream));
+    c.recs.push_back(r);
+  }
+}
+
+// Grid for a grid-stride kernel: enough blocks for `work_threads`, capped at
+// `per_sm` resident blocks on every SM.
+inline unsigned grid_for(const Ctx& c, int64_t work_threads, int block,
+                         int per_sm = 8) {
+  int64_t b = (work_threads + block - 1) / block;
+  int64_t cap = (int64_t)c.num_sms * per_sm;
+  if (b < 1) b = 1;
+  return (unsigned)(b < cap ? b : cap);
+}
+
+template <class T>
+inline void h2d(Ctx& c, T* dst, const T* src, size_t count) {
+  if (count) CK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, c.stream));
+}
+template <class T>
+inline void d2h(Ctx& c, T* dst, const T* src, size_t count) {
+  if (count) CK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, c.stream));
+}
+template <class T>
+inline void d2d(Ctx& c, T* dst, const T* src, size_t count) {
+  if (count) CK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToDevice, c.stream));
+}
+template <class T>
+inline void dzero(Ctx& c, T* dst, size_t count) {
+  if (count) CK(cudaMemsetAsync(dst, 0, count * sizeof(T), c.stream));
+}
+
+// ---------------------------------------------------------------------------
+// Warp-group helpers (groups of G lanes, G | 32, aligned).
+template <int G>
+__device__ __forceinline__ unsigned group_mask() {
+  if (G == 32) return 0xffffffffu;
+  const unsigned lane = threadIdx.x & 31u;
+  return ((1u << G) - 1u) << (lane & ~(unsigned)(G - 1));
+}
+template <int G, class T>
+__device__ __forceinline__ T gsum(T x, unsigned m) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) x += __shfl_xor_sync(m, x, o);
+  return x;
+}
+template <int G, class T>
+__device__ __forceinline__ T gmax(T x, unsigned m) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    T y = __shfl_xor_sync(m, x, o);
+    x = y > x ? y : x;
+  }
+  return x;
+}
+template <int G, class T>
+__device__ __forceinline__ T gmin(T x, unsigned m) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    T y = __shfl_xor_sync(m, x, o);
+    x = y < x ? y : x;
+  }
+  return x;
+}
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned r;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
+}
+
+// Sum of `w` over the lanes in `peers` (a __match_any_sync group). Narrow
+// weights use the single-instruction REDUX; wide ones walk the peer bits.
+__device__ __forceinline__ long long peer_sum(unsigned peers, int w, bool wide) {
+  if (!wide) return (long long)__reduce_add_sync(peers, (unsigned)w);
+  long long s = 0;
+  unsigned m = peers;
+  while (m) {
+    int l = __ffs(m) - 1;
+    m &= m - 1;
+    s += __shfl_sync(peers, w, l);
+  }
+  return s;
+}
+
+// Warp-aggregated append of `v` into list[*cnt] for lanes where `take`.
+__device__ __forceinline__ void warp_append(bool take, int32_t v, int32_t* list,
+                                            unsigned long long* cnt) {
+  const unsigned am = __activemask();
+  const unsigned m = __ballot_sync(am, take);
+  if (m == 0) return;
+  const int leader = __ffs(m) - 1;
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(cnt, (unsigned long long)__popc(m));
+  base = __shfl_sync(am, base, leader);
+  if (take) list[base + __popc(m & lanemask_lt())] = v;
+}
+
+// Block-wide int64 sum into *out (one atomic per block).
+template <int BLOCK>
+__device__ __forceinline__ void block_sum_atomic(long long x, unsigned long long* out) {
+  __shared__ long long red[BLOCK / 32];
+  x = gsum<32>(x, 0xffffffffu);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    long long y = l < BLOCK / 32 ? red[l] : 0;
+    y = gsum<32>(y, 0xffffffffu);
+    if (l == 0 && y != 0) atomicAdd(out, (unsigned long long)y);
+  }
+}
+
+}  // namespace jet

@@ -1,0 +1,185 @@
+// context.cu — jet_ctx lifetime, error reporting and launch profiling.
+#include "common.cuh"
+#include <cstring>
+
+namespace jet {
+
+static thread_local std::string g_last_error;
+
+void set_last_error(const std::string& s) { g_last_error = s; }
+
+void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  cudaGetLastError();
+  std::string m = std::string("CUDA error '") + cudaGetErrorString(e) + "' in " +
+                  what + " at " + file + ":" + std::to_string(line);
+  throw Error(e == cudaErrorMemoryAllocation ? JET_ENOMEM : JET_ECUDA, m);
+}
+
+cudaEvent_t Ctx::take_event() {
+  if (!event_pool.empty()) {
+    cudaEvent_t e = event_pool.back();
+    event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CK(cudaEventCreate(&e));
+  return e;
+}
+
+int Ctx::prof_class(const char* name) {
+  auto it = cls_index.find(name);
+  if (it != cls_index.end()) return it->second;
+  int id = (int)agg.size();
+  cls_index[name] = id;
+  ProfAgg a;
+  a.name = name;
+  agg.push_back(a);
+  return id;
+}
+
+// Resolve pending event pairs into per-class totals.
+void Ctx::flush_prof() {
+  if (recs.empty()) return;
+  CK(cudaStreamSynchronize(stream));
+  for (auto& r : recs) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, r.a, r.b));
+    ProfAgg& a = agg[r.cls];
+    a.launches++;
+    a.ms += ms;
+    a.bytes += r.bytes;
+    event_pool.push_back(r.a);
+    event_pool.push_back(r.b);
+  }
+  recs.clear();
+}
+
+void Ctx::ensure_pinned(size_t elems) {
+  if (elems <= pinned_elems) return;
+  if (pinned) cudaFreeHost(pinned);
+  pinned = nullptr;
+  size_t want = elems < 4096 ? 4096 : elems;
+  CK(cudaMallocHost((void**)&pinned, want * sizeof(int64_t)));
+  pinned_elems = want;
+}
+
+}  // namespace jet
+
+using namespace jet;
+
+extern "C" {
+
+const char* jet_last_error(void) { return g_last_error.c_str(); }
+int jet_api_version(void) { return JET_API_VERSION; }
+
+int jet_create(int device, jet_ctx** out) {
+  try {
+    JET_REQUIRE(out, JET_EINVAL, "out is NULL");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    JET_REQUIRE(device >= 0 && device < ndev, JET_EINVAL,
+                "device index out of range");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    JET_REQUIRE(prop.major >= 10, JET_EUNSUPPORTED,
+                std::string("this build targets sm_100a (B200); found ") + prop.name);
+    Ctx* c = new Ctx();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    c->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = ~0ULL;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    c->ensure_pinned(1 << 16);
+    *out = reinterpret_cast<jet_ctx*>(c);
+    return JET_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return JET_EINTERNAL;
+  }
+}
+
+void jet_destroy(jet_ctx* ctx) {
+  if (!ctx) return;
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  c->cub_tmp.release();
+  for (auto& r : c->recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : c->event_pool) cudaEventDestroy(e);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  cudaStreamSynchronize(c->stream);
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int jet_synchronize(jet_ctx* ctx) {
+  try {
+    Ctx* c = reinterpret_cast<Ctx*>(ctx);
+    c->sync();
+    return JET_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  }
+}
+
+int jet_profile_enable(jet_ctx* ctx, int on) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  c->prof = on != 0;
+  return JET_OK;
+}
+
+int jet_profile_reset(jet_ctx* ctx) {
+  try {
+    Ctx* c = reinterpret_cast<Ctx*>(ctx);
+    c->flush_prof();
+    for (auto& a : c->agg) {
+      a.launches = 0;
+      a.ms = 0;
+      a.bytes = 0;
+    }
+    c->launches = 0;
+    return JET_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  }
+}
+
+int jet_profile_report(jet_ctx* ctx, char* buf, int64_t cap) {
+  try {
+    Ctx* c = reinterpret_cast<Ctx*>(ctx);
+    c->flush_prof();
+    std::string s;
+    char line[256];
+    snprintf(line, sizeof line, "__total__\t%lld\t0\t0\n", (long long)c->launches);
+    s += line;
+    for (auto& a : c->agg) {
+      if (!a.launches) continue;
+      snprintf(line, sizeof line, "%s\t%lld\t%.6f\t%.0f\n", a.name.c_str(),
+               (long long)a.launches, a.ms, a.bytes);
+      s += line;
+    }
+    if (buf && cap > 0) {
+      size_t n = s.size() < (size_t)(cap - 1) ? s.size() : (size_t)(cap - 1);
+      memcpy(buf, s.data(), n);
+      buf[n] = 0;
+    }
+    return (int)s.size();
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return -e.code;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,233 @@
+// controller.cu — the Jet refinement controller (refine.py:190-294) and the
+// multilevel driver (driver.py:48-126) as native host code driving the
+// device passes. Per iteration the only device->host traffic is the counter
+// block (move counts, doubled cut delta) plus the k part weights.
+#include "controller.cuh"
+#include "coarsen.cuh"
+#include "initpart.h"
+#include "rng.h"
+#include <algorithm>
+#include <chrono>
+
+namespace jet {
+
+static double now_s() {
+  using namespace std::chrono;
+  return duration<double>(steady_clock::now().time_since_epoch()).count();
+}
+
+void refine_level(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, int64_t& cut,
+                  const jet_config& cfg, bool finest, int level, jet_level_stats& st,
+                  DBuf<int32_t>& keep) {
+  const int k = cfg.k;
+  const int64_t limit = cfg.limit, sigma = cfg.sigma;
+  w.ensure(c, g.n, k);
+  w.bind_level(g);
+  h2d(c, w.d_pw(), w.h_pw.data(), k);
+  keep.ensure(g.n, c.stream);
+
+  LpParams lp;
+  lp.c_num = finest ? cfg.c_finest_num : cfg.c_other_num;
+  lp.c_den = finest ? cfg.c_finest_den : cfg.c_other_den;
+  lp.c_f = finest ? cfg.c_finest : cfg.c_other;
+  lp.c_use_float = finest ? cfg.c_finest_float : cfg.c_other_float;
+  lp.afterburner = cfg.afterburner;
+  lp.locking = cfg.locking;
+
+  auto balanced = [&] {
+    for (int p = 0; p < k; ++p)
+      if (w.h_pw[p] > limit) return false;
+    return true;
+  };
+  auto worst = [&] { return *std::max_element(w.h_pw.begin(), w.h_pw.end()); };
+
+  // `keep` holds the best balanced state, or while none exists the least
+  // imbalanced fallback (refine.py:212-214, 274-283)
+  bool has_best = balanced();
+  int64_t best_cut = cut, keep_worst = worst();
+  std::vector<int64_t> keep_pw = w.h_pw;
+  int64_t keep_cut = cut;
+  d2d(c, keep.get(), parts, g.n);
+
+  int no_improve = 0, rebal_streak = 0, pass_index = 0;
+  int64_t locked = 0;
+  int32_t epoch = ++c.lock_epoch;  // fresh table: no vertex locked
+  while (no_improve < cfg.no_improve_limit) {
+    bool is_lp = false, locks_all_clear = false;
+    if (balanced()) {
+      rebal_streak = 0;
+      locks_all_clear = !cfg.locking || locked == 0;
+      lp.lock_epoch = epoch;
+      lp_pass(c, w, g, parts, k, lp, nullptr);
+      is_lp = true;
+      st.lp_passes++;
+    } else {
+      if (rebal_streak >= 2 + k) {
+        st.rebalance_stuck = 1;
+        break;
+      }
+      epoch = ++c.lock_epoch;  // table.reset_locks()
+      locked = 0;
+      // default_rng([seed, *seed_path, pass_index]); level < 0 = empty path
+      Pcg64 rng = level >= 0 ? default_rng({cfg.seed, (uint64_t)level, (uint64_t)pass_index})
+                             : default_rng({cfg.seed, (uint64_t)pass_index});
+      const bool strong = rebal_streak >= 2;
+      if (!rebalance_pass(c, w, g, parts, k, limit, sigma, cfg.sub_buckets, strong, rng, nullptr)) {
+        st.rebalance_stuck = 1;
+        break;
+      }
+      if (strong) st.strong_passes++;
+      else st.weak_passes++;
+      rebal_streak++;
+    }
+    const bool set_lock = is_lp && cfg.locking;
+    const int32_t new_epoch = set_lock ? ++c.lock_epoch : epoch;
+    const ApplyResult ar = apply_moves(c, w, g, parts, k, set_lock, new_epoch);
+    if (set_lock) {
+      epoch = new_epoch;
+      locked = ar.n_moves;
+    }
+    const bool fixed_point = is_lp && ar.n_moves == 0 && locks_all_clear;
+    cut += ar.cut_delta;
+    pass_index++;
+    st.iterations++;
+    st.moves += ar.n_moves;
+    no_improve++;
+    if (balanced()) {
+      if (!has_best || cut < best_cut) {
+        if (!has_best || (double)cut < cfg.phi * (double)best_cut) no_improve = 0;
+        d2d(c, keep.get(), parts, g.n);
+        best_cut = cut;
+        keep_cut = cut;
+        keep_pw = w.h_pw;
+        has_best = true;
+      }
+    } else if (!has_best) {
+      const int64_t wv = worst();
+      if (wv < keep_worst) {
+        d2d(c, keep.get(), parts, g.n);
+        keep_worst = wv;
+        keep_cut = cut;
+        keep_pw = w.h_pw;
+      }
+    }
+    if (fixed_point) break;
+  }
+  d2d(c, parts, keep.get(), g.n);
+  cut = keep_cut;
+  w.h_pw = keep_pw;
+  st.balanced = has_best ? 1 : 0;
+}
+
+static void download_host_graph(Ctx& c, const DGraph& g, HostGraph& h) {
+  h.n = g.n;
+  h.offs.resize(g.n + 1);
+  std::vector<int32_t> a(g.nnz), e(g.nnz), v(g.n);
+  d2h(c, h.offs.data(), g.offs.get(), g.n + 1);
+  d2h(c, a.data(), g.adj.get(), g.nnz);
+  d2h(c, e.data(), g.ew.get(), g.nnz);
+  d2h(c, v.data(), g.vw.get(), g.n);
+  c.sync();
+  h.adj.assign(a.begin(), a.end());
+  h.ew.assign(e.begin(), e.end());
+  h.vw.assign(v.begin(), v.end());
+}
+
+void check_partition_args(const DGraph& g, const jet_config& cfg) {
+  JET_REQUIRE(cfg.k >= 1, JET_EINVAL, "k must be >= 1");
+  JET_REQUIRE(cfg.k <= g.n, JET_EINVAL,
+              "k=" + std::to_string(cfg.k) + " exceeds vertex count " + std::to_string(g.n));
+  JET_REQUIRE(cfg.k <= KMASK, JET_EUNSUPPORTED, "k too large");
+  JET_REQUIRE(g.max_vw <= cfg.limit, JET_EBALANCE,
+              "vertex weight " + std::to_string(g.max_vw) + " exceeds the part weight limit " +
+                  std::to_string(cfg.limit));
+  JET_REQUIRE((double)cfg.k * (double)cfg.limit >= (double)g.total_vw, JET_EBALANCE,
+              "k * limit cannot hold the total vertex weight");
+  JET_REQUIRE(cfg.no_improve_limit >= 1 && cfg.sub_buckets >= 1 && cfg.restarts >= 1, JET_EINVAL,
+              "invalid refiner configuration");
+}
+
+void run_partition(Ctx& c, const DGraph& g0, const jet_config& cfg, int32_t* parts_out,
+                   int64_t* pw_out, jet_run_stats* st) {
+  check_partition_args(g0, cfg);
+  const int k = cfg.k;
+  const double t0 = now_s();
+  jet_run_stats local{};
+  jet_run_stats& S = st ? *st : local;
+  const double t_up = S.t_upload;
+  memset(&S, 0, sizeof(S));
+  S.t_upload = t_up;
+  if (k == 1) {
+    dzero(c, parts_out, g0.n);
+    c.sync();
+    S.t_total = now_s() - t0;
+    S.n_levels = 1;
+    S.cutsize = 0;
+    S.balanced = 1;
+    S.max_part_weight = g0.total_vw;
+    if (pw_out) pw_out[0] = g0.total_vw;
+    return;
+  }
+  const int64_t target = std::max<int64_t>(std::max<int64_t>(cfg.coarse_target, 2LL * k), 32);
+  Hierarchy h;
+  device_build_hierarchy(c, g0, target, h);
+  c.sync();
+  const double t1 = now_s();
+  S.t_coarsen = t1 - t0;
+
+  const int top = h.size() - 1;
+  const DGraph& gc = h.level(top);
+  HostGraph hg;
+  download_host_graph(c, gc, hg);
+  std::vector<int32_t> ip = host_initial_partition(hg, k, cfg.limit, cfg.seed, cfg.restarts);
+  Workspace w;
+  w.ensure(c, g0.n, k);
+  w.h_pw.assign(k, 0);
+  int64_t cut2 = 0;
+  for (int64_t v = 0; v < hg.n; ++v) {
+    w.h_pw[ip[v]] += hg.vw[v];
+    for (int64_t j = hg.offs[v]; j < hg.offs[v + 1]; ++j)
+      if (ip[v] != ip[hg.adj[j]]) cut2 += hg.ew[j];
+  }
+  int64_t cut = cut2 / 2;
+  DBuf<int32_t> pa(g0.n, c.stream), pb(g0.n, c.stream), keep(g0.n, c.stream);
+  h2d(c, pa.get(), ip.data(), hg.n);
+  const double t2 = now_s();
+  S.t_initial = t2 - t1;
+
+  int32_t* cur = pa.get();
+  int32_t* nxt = pb.get();
+  int li = 0;
+  for (int level = top; level >= 0; --level) {
+    const DGraph& g = h.level(level);
+    if (level != top) {
+      device_project(c, h.maps[level].get(), cur, nxt, g.n);
+      std::swap(cur, nxt);
+    }
+    jet_level_stats& L = S.levels[li++];
+    memset(&L, 0, sizeof(L));
+    L.level = level;
+    L.n = g.n;
+    L.m = g.nnz / 2;
+    L.cut_in = cut;
+    L.balanced_in = *std::max_element(w.h_pw.begin(), w.h_pw.end()) <= cfg.limit;
+    const double tl = now_s();
+    refine_level(c, w, g, cur, cut, cfg, level == 0, level, L, keep);
+    c.sync();
+    L.seconds = now_s() - tl;
+    L.cut_out = cut;
+    L.balanced = *std::max_element(w.h_pw.begin(), w.h_pw.end()) <= cfg.limit;
+  }
+  d2d(c, parts_out, cur, g0.n);
+  c.sync();
+  const double t3 = now_s();
+  S.t_uncoarsen = t3 - t2;
+  S.t_total = t3 - t0;
+  S.n_levels = h.size();
+  S.cutsize = cut;
+  S.max_part_weight = *std::max_element(w.h_pw.begin(), w.h_pw.end());
+  S.balanced = S.max_part_weight <= cfg.limit;
+  if (pw_out) std::copy(w.h_pw.begin(), w.h_pw.end(), pw_out);
+}
+
+}  // namespace jet

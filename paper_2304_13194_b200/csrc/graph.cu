@@ -1,0 +1,338 @@
+// graph.cu — device CSR levels: upload + validation, degree tiers, and the
+// per-level metrics kernels (cutsize graph.py:215-221, part weights
+// graph.py:240-242, projection driver.py:32-45).
+#include "common.cuh"
+#include "graph.cuh"
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+
+namespace jet {
+
+// ---------------------------------------------------------------------------
+// Upload: host arrays (int32 or int64) -> int32 device arrays, with range
+// checks the reference performs implicitly through numpy indexing.
+enum { BAD_ADJ = 1, BAD_EW = 2, BAD_VW = 4, BAD_OFFS = 8 };
+
+template <class T>
+__global__ void k_narrow(const T* __restrict__ in, int32_t* __restrict__ out,
+                         int64_t count, long long lo, long long hi, int flag,
+                         unsigned* bad) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  bool b = false;
+  for (; i < count; i += stride) {
+    long long x = (long long)in[i];
+    b |= (x < lo) | (x > hi);
+    out[i] = (int32_t)x;
+  }
+  if (__any_sync(__activemask(), b) && b) atomicOr(bad, (unsigned)flag);
+}
+
+__global__ void k_check_offsets(const int64_t* __restrict__ offs, int64_t n,
+                                int64_t nnz, unsigned* bad) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  bool b = false;
+  for (; i < n; i += stride) b |= offs[i + 1] < offs[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) b |= (offs[0] != 0) | (offs[n] != nnz);
+  if (b) atomicOr(bad, (unsigned)BAD_OFFS);
+}
+
+// Per-level statistics: total/max vertex weight, max degree, max edge weight
+// and the tier histogram (vertex counts and entry counts per tier).
+struct LevelStats {
+  unsigned long long total_vw, max_vw, max_deg, max_ew;
+  unsigned long long bin_cnt[NBINS], bin_nnz[NBINS];
+};
+
+__global__ void k_level_stats(const int64_t* __restrict__ offs,
+                              const int32_t* __restrict__ vw,
+                              const int32_t* __restrict__ ew, int64_t n,
+                              int64_t nnz, LevelStats* st) {
+  __shared__ unsigned long long s_cnt[NBINS], s_nnz[NBINS];
+  if (threadIdx.x < NBINS) {
+    s_cnt[threadIdx.x] = 0;
+    s_nnz[threadIdx.x] = 0;
+  }
+  __syncthreads();
+  unsigned long long tv = 0, mv = 0, md = 0, me = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride) {
+    int64_t d = offs[v + 1] - offs[v];
+    unsigned long long w = (unsigned long long)vw[v];
+    tv += w;
+    mv = w > mv ? w : mv;
+    md = (unsigned long long)d > md ? (unsigned long long)d : md;
+    int t = tier_of_degree(d);
+    atomicAdd(&s_cnt[t], 1ull);
+    atomicAdd(&s_nnz[t], (unsigned long long)d);
+  }
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += stride) {
+    unsigned long long w = (unsigned long long)ew[e];
+    me = w > me ? w : me;
+  }
+  tv = gsum<32>(tv, 0xffffffffu);
+  mv = gmax<32>(mv, 0xffffffffu);
+  md = gmax<32>(md, 0xffffffffu);
+  me = gmax<32>(me, 0xffffffffu);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&st->total_vw, tv);
+    atomicMax(&st->max_vw, mv);
+    atomicMax(&st->max_deg, md);
+    atomicMax(&st->max_ew, me);
+  }
+  __syncthreads();
+  if (threadIdx.x < NBINS) {
+    atomicAdd(&st->bin_cnt[threadIdx.x], s_cnt[threadIdx.x]);
+    atomicAdd(&st->bin_nnz[threadIdx.x], s_nnz[threadIdx.x]);
+  }
+}
+
+struct TierIs {
+  const int64_t* offs;
+  int t;
+  __device__ __forceinline__ bool operator()(const int32_t& v) const {
+    return tier_of_degree(offs[v + 1] - offs[v]) == t;
+  }
+};
+
+void finalize_graph(Ctx& c, DGraph& g) {
+  DBuf<LevelStats> st(1, c.stream);
+  dzero(c, st.get(), 1);
+  if (g.n > 0) {
+    launch(c, "level_stats", 8.0 * g.n + 4.0 * g.n + 4.0 * g.nnz, [&] {
+      k_level_stats<<<grid_for(c, g.n > g.nnz ? g.n : g.nnz, 256), 256, 0, c.stream>>>(
+          g.offs.get(), g.vw.get(), g.ew.get(), g.n, g.nnz, st.get());
+    });
+  }
+  LevelStats h;
+  d2h(c, &h, st.get(), 1);
+  c.sync();
+  g.total_vw = (int64_t)h.total_vw;
+  g.max_vw = (int64_t)h.max_vw;
+  g.max_deg = (int64_t)h.max_deg;
+  g.max_ew = (int64_t)h.max_ew;
+  g.unit_ew = g.nnz == 0 || h.max_ew <= 1;
+  g.max_wdeg = g.max_deg * (g.max_ew > 0 ? g.max_ew : 1);  // upper bound
+  JET_REQUIRE(g.max_wdeg < (1LL << (63 - KBITS)), JET_EUNSUPPORTED,
+              "weighted degree too large for 64-bit gain keys");
+  int nonempty = 0, last = -1;
+  for (int t = 0; t < NBINS; ++t) {
+    g.bin_cnt[t] = (int64_t)h.bin_cnt[t];
+    g.bin_nnz[t] = (int64_t)h.bin_nnz[t];
+    g.bin_list[t] = nullptr;
+    if (g.bin_cnt[t]) {
+      nonempty++;
+      last = t;
+    }
+  }
+  g.identity = nonempty <= 1;
+  g.identity_bin = last;
+  if (g.identity) return;
+  g.bin_store.alloc((size_t)g.n, c.stream);
+  DBuf<int64_t> nsel(1, c.stream);
+  int64_t base = 0;
+  for (int t = 0; t < NBINS; ++t) {
+    if (!g.bin_cnt[t]) continue;
+    int32_t* out = g.bin_store.get() + base;
+    cub::CountingInputIterator<int32_t> it(0);
+    TierIs op{g.offs.get(), t};
+    size_t tmp = 0;
+    CK(cub::DeviceSelect::If(nullptr, tmp, it, out, nsel.get(), (int)g.n, op, c.stream));
+    void* p = c.cub_scratch(tmp);
+    launch(c, "tier_select", 16.0 * g.n, [&] {
+      CK(cub::DeviceSelect::If(p, tmp, it, out, nsel.get(), (int)g.n, op, c.stream));
+    });
+    g.bin_list[t] = out;
+    base += g.bin_cnt[t];
+  }
+}
+
+std::unique_ptr<DGraph> upload_graph(Ctx& c, int64_t n, const int64_t* offs,
+                                     const void* adj, int adt, const void* ew,
+                                     int edt, const void* vw, int vdt) {
+  JET_REQUIRE(n >= 1, JET_EINVAL, "graph must have at least one vertex");
+  JET_REQUIRE(n < (1LL << 31) - 1, JET_EUNSUPPORTED, "n must be < 2^31");
+  JET_REQUIRE(offs, JET_EINVAL, "row_offsets is NULL");
+  auto dt_ok = [](int d) { return d == JET_I32 || d == JET_I64; };
+  JET_REQUIRE(dt_ok(adt) && dt_ok(edt) && dt_ok(vdt), JET_EINVAL, "bad dtype code");
+  const int64_t nnz = offs[n];
+  JET_REQUIRE(offs[0] == 0 && nnz >= 0, JET_EINVAL, "row_offsets must start at 0");
+  auto g = std::make_unique<DGraph>();
+  g->n = n;
+  g->nnz = nnz;
+  g->offs.alloc(n + 1, c.stream);
+  g->adj.alloc(nnz > 0 ? nnz : 1, c.stream);
+  g->ew.alloc(nnz > 0 ? nnz : 1, c.stream);
+  g->vw.alloc(n, c.stream);
+  DBuf<unsigned> bad(1, c.stream);
+  dzero(c, bad.get(), 1);
+  h2d(c, g->offs.get(), offs, n + 1);
+  launch(c, "check_offsets", 8.0 * (n + 1), [&] {
+    k_check_offsets<<<grid_for(c, n, 256), 256, 0, c.stream>>>(g->offs.get(), n, nnz, bad.get());
+  });
+  // staging for int64 -> int32 narrowing, chunked to bound the footprint
+  const int64_t CH = 1LL << 26;
+  DBuf<int64_t> stage;
+  auto put = [&](const void* src, int dt, int32_t* dst, int64_t count, long long lo,
+                 long long hi, int flag) {
+    if (count == 0) return;
+    if (dt == JET_I32) {
+      h2d(c, dst, (const int32_t*)src, count);
+      launch(c, "validate_i32", 4.0 * count, [&] {
+        k_narrow<int32_t><<<grid_for(c, count, 256), 256, 0, c.stream>>>(
+            dst, dst, count, lo, hi, flag, bad.get());
+      });
+      return;
+    }
+    stage.ensure(count < CH ? count : CH, c.stream);
+    for (int64_t b = 0; b < count; b += CH) {
+      int64_t m = count - b < CH ? count - b : CH;
+      h2d(c, stage.get(), (const int64_t*)src + b, m);
+      launch(c, "narrow_i64", 12.0 * m, [&] {
+        k_narrow<int64_t><<<grid_for(c, m, 256), 256, 0, c.stream>>>(
+            stage.get(), dst + b, m, lo, hi, flag, bad.get());
+      });
+    }
+  };
+  const long long I32MAX = 2147483647LL;
+  put(adj, adt, g->adj.get(), nnz, 0, n - 1, BAD_ADJ);
+  put(ew, edt, g->ew.get(), nnz, 1, I32MAX, BAD_EW);
+  put(vw, vdt, g->vw.get(), n, 1, I32MAX, BAD_VW);
+  unsigned hbad = 0;
+  d2h(c, &hbad, bad.get(), 1);
+  c.sync();
+  JET_REQUIRE(!(hbad & BAD_OFFS), JET_EINVAL, "row_offsets must be non-decreasing from 0 to nnz");
+  JET_REQUIRE(!(hbad & BAD_ADJ), JET_EINVAL, "neighbor id out of range");
+  JET_REQUIRE(!(hbad & BAD_EW), JET_EINVAL, "edge weights must be in [1, 2^31)");
+  JET_REQUIRE(!(hbad & BAD_VW), JET_EINVAL, "vertex weights must be in [1, 2^31)");
+  finalize_graph(c, *g);
+  return g;
+}
+
+// ---------------------------------------------------------------------------
+// cutsize: sum over entries with part(u) != part(v), halved (graph.py:215-221)
+template <int G, bool UNIT>
+__global__ void __launch_bounds__(256) k_cut(GView g, const int32_t* __restrict__ list,
+                                             int64_t cnt, const int32_t* __restrict__ parts,
+                                             unsigned long long* out) {
+  const unsigned gm = group_mask<G>();
+  const int gl = threadIdx.x & (G - 1);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x / G;
+  long long acc = 0;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G; i < cnt; i += stride) {
+    const int v = list ? list[i] : (int)i;
+    const int64_t b = g.offs[v], e = g.offs[v + 1];
+    const int pv = parts[v];
+    for (int64_t j = b + gl; j < e; j += G) {
+      int u = g.adj[j];
+      if (parts[u] != pv) acc += UNIT ? 1 : g.ew[j];
+    }
+  }
+  (void)gm;
+  block_sum_atomic<256>(acc, out);
+}
+
+int64_t device_cutsize(Ctx& c, const DGraph& g, const int32_t* parts) {
+  DBuf<unsigned long long> acc(1, c.stream);
+  dzero(c, acc.get(), 1);
+  for (int t = 0; t < NBINS; ++t) {
+    const int64_t cnt = g.bin_cnt[t];
+    if (!cnt) continue;
+    const int G = t < 4 ? TIER_G[t] : 32;
+    const int32_t* list = tier_list(g, t);
+    const unsigned grid = grid_for(c, cnt * G, 256);
+    const GView v = view(g);
+    launch(c, "cutsize", (g.unit_ew ? 8.0 : 12.0) * g.bin_nnz[t] + 12.0 * cnt, [&] {
+      JET_TIER_LAUNCH(k_cut, G, g.unit_ew, grid, 256, 0, c.stream, v, list, cnt, parts, acc.get());
+    });
+  }
+  unsigned long long h = 0;
+  d2h(c, &h, acc.get(), 1);
+  c.sync();
+  return (int64_t)(h / 2);
+}
+
+// ---------------------------------------------------------------------------
+// part weights: weighted bincount (graph.py:240-242)
+__global__ void k_part_weights(const int32_t* __restrict__ parts,
+                               const int32_t* __restrict__ vw, int64_t n, int k,
+                               unsigned long long* pw) {
+  extern __shared__ unsigned long long s_pw[];
+  const bool use_smem = k <= 4096;
+  if (use_smem)
+    for (int i = threadIdx.x; i < k; i += blockDim.x) s_pw[i] = 0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride) {
+    int p = parts[v];
+    if (use_smem) atomicAdd(&s_pw[p], (unsigned long long)vw[v]);
+    else atomicAdd(&pw[p], (unsigned long long)vw[v]);
+  }
+  __syncthreads();
+  if (use_smem)
+    for (int i = threadIdx.x; i < k; i += blockDim.x)
+      if (s_pw[i]) atomicAdd(&pw[i], s_pw[i]);
+}
+
+void device_part_weights(Ctx& c, const DGraph& g, const int32_t* parts, int k,
+                         int64_t* d_pw) {
+  dzero(c, d_pw, k);
+  size_t smem = k <= 4096 ? (size_t)k * 8 : 0;
+  launch(c, "part_weights", 8.0 * g.n + 8.0 * k, [&] {
+    k_part_weights<<<grid_for(c, g.n, 256, 4), 256, smem, c.stream>>>(
+        parts, g.vw.get(), g.n, k, (unsigned long long*)d_pw);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// projection: parts_f[v] = parts_c[vmap[v]]  (driver.py:32-45)
+__global__ void k_project(const int32_t* __restrict__ vmap,
+                          const int32_t* __restrict__ pc, int32_t* __restrict__ pf,
+                          int64_t nf) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nf; v += stride)
+    pf[v] = pc[vmap[v]];
+}
+
+void device_project(Ctx& c, const int32_t* vmap, const int32_t* pc, int32_t* pf,
+                    int64_t nf) {
+  launch(c, "project", 12.0 * nf, [&] {
+    k_project<<<grid_for(c, nf, 256), 256, 0, c.stream>>>(vmap, pc, pf, nf);
+  });
+}
+
+// int64 <-> int32 helpers for the per-kernel entry points
+__global__ void k_widen(const int32_t* __restrict__ in, int64_t* __restrict__ out, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = in[i];
+}
+
+void upload_i64_as_i32(Ctx& c, const int64_t* host, int64_t n, int32_t* dst,
+                       long long lo, long long hi, const char* what) {
+  if (n <= 0) return;
+  DBuf<int64_t> s(n, c.stream);
+  DBuf<unsigned> bad(1, c.stream);
+  dzero(c, bad.get(), 1);
+  h2d(c, s.get(), host, n);
+  launch(c, "narrow_i64", 12.0 * n, [&] {
+    k_narrow<int64_t><<<grid_for(c, n, 256), 256, 0, c.stream>>>(s.get(), dst, n, lo, hi, 1, bad.get());
+  });
+  unsigned hb = 0;
+  d2h(c, &hb, bad.get(), 1);
+  c.sync();
+  JET_REQUIRE(!hb, JET_EINVAL, std::string(what) + " out of range");
+}
+
+void download_i32_as_i64(Ctx& c, const int32_t* dsrc, int64_t n, int64_t* host) {
+  if (n <= 0) return;
+  DBuf<int64_t> s(n, c.stream);
+  launch(c, "widen", 12.0 * n, [&] {
+    k_widen<<<grid_for(c, n, 256), 256, 0, c.stream>>>(dsrc, s.get(), n);
+  });
+  d2h(c, host, s.get(), n);
+  c.sync();
+}
+
+}  // namespace jet
