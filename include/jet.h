@@ -114,6 +114,15 @@ int jet_profile_reset(jet_ctx* ctx);
 /* Writes up to cap records "name\tlaunches\tms\tbytes\n" into buf. */
 int jet_profile_report(jet_ctx* ctx, char* buf, int64_t cap);
 int jet_synchronize(jet_ctx* ctx);
+/* Record events only for launches whose class name equals `name` (NULL or
+ * "" = every class). Keeps timed-region profiling cheap. */
+int jet_profile_filter(jet_ctx* ctx, const char* name);
+/* CUDA-event stopwatch on the context stream: start, then stop returns the
+ * elapsed device milliseconds (synchronises). */
+int jet_timer_start(jet_ctx* ctx);
+int jet_timer_stop(jet_ctx* ctx, double* ms);
+/* Overwrite a buffer larger than L2 (flush between timed iterations). */
+int jet_flush_l2(jet_ctx* ctx);
 
 /* ---- graphs (Graph, graph.py:17-100) -------------------------------- */
 /* Uploads a CSR graph. row_offsets is int64[n+1]; adjacency/edge_weights

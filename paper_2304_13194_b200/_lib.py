@@ -82,6 +82,10 @@ _SIGS = {
     "jet_profile_reset": (C.c_int, [P]),
     "jet_profile_report": (C.c_int, [P, C.c_char_p, i64]),
     "jet_synchronize": (C.c_int, [P]),
+    "jet_profile_filter": (C.c_int, [P, C.c_char_p]),
+    "jet_timer_start": (C.c_int, [P]),
+    "jet_timer_stop": (C.c_int, [P, C.POINTER(C.c_double)]),
+    "jet_flush_l2": (C.c_int, [P]),
     "jet_graph_upload": (C.c_int, [P, i64, P, P, C.c_int, P, C.c_int, P, C.c_int, C.POINTER(P)]),
     "jet_graph_info": (C.c_int, [P, P, P, P]),
     "jet_graph_download": (C.c_int, [P, P, P, P, P, P]),
@@ -215,6 +219,20 @@ class Context:
 
     def synchronize(self):
         check(lib().jet_synchronize(self.handle))
+
+    def profile_only(self, name: str | None):
+        check(lib().jet_profile_filter(self.handle, (name or "").encode()))
+
+    def timer_start(self):
+        check(lib().jet_timer_start(self.handle))
+
+    def timer_stop(self) -> float:
+        ms = C.c_double()
+        check(lib().jet_timer_stop(self.handle, C.byref(ms)))
+        return ms.value
+
+    def flush_l2(self):
+        check(lib().jet_flush_l2(self.handle))
 
 
 class DeviceGraph:

@@ -22,10 +22,22 @@
 #include <cub/device/device_segmented_sort.cuh>
 #include <cub/block/block_scan.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
+#include <algorithm>
 
 namespace jet {
 
 constexpr int INF32 = 0x7f7f7f7f;  // memset(0x7f) pattern, > any vertex id
+
+__device__ __forceinline__ unsigned long long vload(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+static int coop_blocks(Ctx& c, const void* kern, int block) {
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, 0));
+  JET_REQUIRE(per_sm >= 1, JET_EINTERNAL, "cooperative kernel does not fit on an SM");
+  return per_sm * c.num_sms;
+}
 
 // ---------------------------------------------------------------------------
 // Phase 1: proposals. score = (w, -u) maximised over free neighbours
@@ -35,15 +47,80 @@ __global__ void __launch_bounds__(256)
     k_propose(GView g, const int32_t* __restrict__ list, int64_t cnt,
               const int32_t* __restrict__ partner, int32_t* prop, int32_t* elist,
               unsigned long long* ecnt) {
+  // same warp-owns-32-rows batching as the refinement sweeps (refine.cu)
+  constexpr int RPS = 32 / G;
+  constexpr int U = G >= 8 ? 8 : G;
   const unsigned gm = group_mask<G>();
-  const int gl = threadIdx.x & (G - 1);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x / G;
-  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G; i < cnt; i += stride) {
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1), grp = lane / G;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = w0 * 32; base < cnt; base += nw * 32) {
+    const int64_t idx = base + lane;
+    int v = 0, deg = 0;
+    bool live = false;
+    int64_t beg = 0;
+    if (idx < cnt) {
+      v = list ? list[idx] : (int)idx;
+      live = partner[v] < 0;
+      if (live) {
+        beg = g.offs[v];
+        deg = (int)(g.offs[v + 1] - beg);
+      }
+    }
+    unsigned long long mine = 0;
+#pragma unroll
+    for (int s0 = 0; s0 < G; s0 += U) {
+      int uu[U], ww[U], fr[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int r = (s0 + q) * RPS + grp;
+        const int64_t rb = __shfl_sync(0xffffffffu, beg, r);
+        const int rd = __shfl_sync(0xffffffffu, deg, r);
+        uu[q] = -1;
+        ww[q] = 0;
+        if (gl < rd) {
+          uu[q] = g.adj[rb + gl];
+          ww[q] = UNIT ? 1 : g.ew[rb + gl];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) fr[q] = uu[q] >= 0 ? partner[uu[q]] : 0;
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int st = s0 + q;
+        unsigned long long key = 0;
+        if (uu[q] >= 0 && fr[q] < 0)
+          key = ((unsigned long long)ww[q] << 32) | (unsigned)(0xffffffffu - (unsigned)uu[q]);
+        key = gmax<G>(key, gm);
+        const int src = ((lane - st * RPS) & (RPS - 1)) * G;
+        key = __shfl_sync(0xffffffffu, key, src);
+        if (lane / RPS == st) mine = key;
+      }
+    }
+    int u = -1;
+    if (live) {
+      u = mine ? (int)(0xffffffffu - (unsigned)(mine & 0xffffffffu)) : -1;
+      prop[v] = u;
+    }
+    warp_append(u >= 0, v, elist, ecnt);
+  }
+}
+
+// Rows longer than 32 (tiers 4/5): one warp per row, looping over the row.
+template <bool UNIT>
+__global__ void __launch_bounds__(256)
+    k_propose_long(GView g, const int32_t* __restrict__ list, int64_t cnt,
+                   const int32_t* __restrict__ partner, int32_t* prop, int32_t* elist,
+                   unsigned long long* ecnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = w0; i < cnt; i += nw) {
     const int v = list ? list[i] : (int)i;
-    if (partner[v] >= 0) continue;  // uniform per group
+    if (partner[v] >= 0) continue;
     const int64_t b = g.offs[v], e = g.offs[v + 1];
     unsigned long long best = 0;
-    for (int64_t j = b + gl; j < e; j += G) {
+    for (int64_t j = b + lane; j < e; j += 32) {
       const int u = g.adj[j];
       if (partner[u] < 0) {
         const unsigned long long w = UNIT ? 1ull : (unsigned long long)g.ew[j];
@@ -51,8 +128,8 @@ __global__ void __launch_bounds__(256)
         best = key > best ? key : best;
       }
     }
-    best = gmax<G>(best, gm);
-    if (gl == 0) {
+    best = gmax<32>(best, 0xffffffffu);
+    if (lane == 0) {
       const int u = best ? (int)(0xffffffffu - (unsigned)(best & 0xffffffffu)) : -1;
       prop[v] = u;
       warp_append(u >= 0, v, elist, ecnt);
@@ -145,10 +222,8 @@ struct TwoHop {
 };
 
 // Retire centres with <= 1 unmatched member; count the remaining active.
-__global__ void k_th_retire(TwoHop t, unsigned long long* active) {
+__device__ void th_retire(const TwoHop& t, unsigned long long* active, int64_t w0, int64_t ws) {
   const int lane = threadIdx.x & 31;
-  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
   long long act = 0;
   for (int64_t ci = w0; ci < t.nc; ci += ws) {
     const int c = t.centres[ci];
@@ -170,10 +245,9 @@ __global__ void k_th_retire(TwoHop t, unsigned long long* active) {
 }
 
 // minc[v] = smallest active centre adjacent to unmatched leftover v.
-__global__ void k_th_minc(TwoHop t, GView g, const int32_t* __restrict__ left, int64_t nl) {
+__device__ void th_minc(const TwoHop& t, const GView& g, const int32_t* __restrict__ left,
+                        int64_t nl, int64_t w0, int64_t ws) {
   const int lane = threadIdx.x & 31;
-  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = w0; i < nl; i += ws) {
     const int v = left[i];
     if (t.partner[v] >= 0) continue;
@@ -188,10 +262,8 @@ __global__ void k_th_minc(TwoHop t, GView g, const int32_t* __restrict__ left, i
   }
 }
 
-__global__ void k_th_ready(TwoHop t) {
+__device__ void th_ready(const TwoHop& t, int64_t w0, int64_t ws) {
   const int lane = threadIdx.x & 31;
-  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t ci = w0; ci < t.nc; ci += ws) {
     const int c = t.centres[ci];
     bool ok = t.cact[c] != 0;
@@ -212,10 +284,8 @@ __global__ void k_th_ready(TwoHop t) {
 }
 
 // Ready centres pair their unmatched members consecutively (coarsen.py:95-103).
-__global__ void k_th_pair(TwoHop t) {
+__device__ void th_pair(const TwoHop& t, int64_t w0, int64_t ws) {
   const int lane = threadIdx.x & 31;
-  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t ci = w0; ci < t.nc; ci += ws) {
     if (!t.ready[ci]) continue;
     const int c = t.centres[ci];
@@ -253,6 +323,28 @@ __global__ void k_th_pair(TwoHop t) {
       __syncwarp();
     }
     if (lane == 0) t.cact[c] = 0;
+  }
+}
+
+// All two-hop rounds in one cooperative launch: retire / minc / ready /
+// pair, separated by grid-wide barriers, until no active centre remains.
+__global__ void __launch_bounds__(1024)
+    k_two_hop(TwoHop t, GView g, const int32_t* __restrict__ left, int64_t nl,
+              unsigned long long* active) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  while (true) {
+    th_retire(t, active, w0, ws);
+    grid.sync();
+    if (vload(active) == 0) return;
+    th_minc(t, g, left, nl, w0, ws);
+    grid.sync();
+    th_ready(t, w0, ws);
+    grid.sync();
+    if (w0 == 0 && (threadIdx.x & 31) == 0) *active = 0;
+    th_pair(t, w0, ws);
+    grid.sync();
   }
 }
 
@@ -372,22 +464,101 @@ static void two_hop(Ctx& c, const DGraph& g, int32_t* partner) {
   th_mark(c, centres.get(), nc, cact.get());
   TwoHop t{partner, centres.get(), coff.get(), v1.get(), cact.get(), ready.get(), minc.get(), nc};
   DBuf<unsigned long long> act(1, c.stream);
-  const unsigned gw = grid_for(c, nc * 32, 256);
-  const unsigned gl = grid_for(c, nl * 32, 256);
-  int batch = 1;
-  while (true) {
-    for (int r = 0; r < batch; ++r) {
-      dzero(c, act.get(), 1);
-      launch(c, "th_retire", 0.0, [&] { k_th_retire<<<gw, 256, 0, c.stream>>>(t, act.get()); });
-      launch(c, "th_minc", 0.0, [&] { k_th_minc<<<gl, 256, 0, c.stream>>>(t, gv, left.get(), nl); });
-      launch(c, "th_ready", 0.0, [&] { k_th_ready<<<gw, 256, 0, c.stream>>>(t); });
-      launch(c, "th_pair", 0.0, [&] { k_th_pair<<<gw, 256, 0, c.stream>>>(t); });
+  dzero(c, act.get(), 1);
+  const int64_t want = std::max<int64_t>(nc, nl);
+  const int blocks = std::min<int64_t>(coop_blocks(c, (const void*)k_two_hop, 1024),
+                                       std::max<int64_t>(1, (want * 32 + 1023) / 1024));
+  const int32_t* lp = left.get();
+  unsigned long long* ap = act.get();
+  void* args[] = {&t, (void*)&gv, (void*)&lp, (void*)&nl, (void*)&ap};
+  launch(c, "two_hop", 0.0, [&] {
+    CK(cudaLaunchCooperativeKernel((const void*)k_two_hop, dim3(blocks), dim3(1024), args, 0,
+                                   c.stream));
+  });
+}
+
+// ---------------------------------------------------------------------------
+// All resolution rounds of one proposal snapshot in a single cooperative
+// launch: grid-wide rounds while many edges are live, then block 0 finishes
+// the long tail of short chains alone (SURVEY §7 hard part 1: up to ~N/2
+// rounds on lattices). Lists/counters ping-pong as in the two-kernel form.
+struct Resolve {
+  const int32_t* prop;
+  int32_t* partner;
+  int32_t* lists;  // 2 x n
+  unsigned long long* cnt;  // 2
+  int32_t* mn;     // 2 x n
+  int64_t n;
+  unsigned long long small;
+};
+
+__device__ void resolve_a(const Resolve& R, int in, int out, int64_t t0, int64_t nt) {
+  const int64_t cnt = (int64_t)vload(R.cnt + in);
+  const int32_t* lin = R.lists + (size_t)in * R.n;
+  int32_t* lout = R.lists + (size_t)out * R.n;
+  int32_t* mcur = R.mn + (size_t)out * R.n;
+  int32_t* mprev = R.mn + (size_t)in * R.n;
+  const int64_t lim = (cnt + 31) / 32 * 32;
+  for (int64_t i = t0; i < lim; i += nt) {
+    bool alive = false;
+    int v = 0;
+    if (i < cnt) {
+      v = lin[i];
+      const int u = R.prop[v];
+      mprev[v] = INF32;
+      mprev[u] = INF32;
+      alive = R.partner[v] < 0 && R.partner[u] < 0;
+      if (alive) {
+        atomicMin(&mcur[v], v);
+        atomicMin(&mcur[u], v);
+      }
     }
-    unsigned long long h = 0;
-    d2h(c, &h, act.get(), 1);
-    c.sync();
-    if (h == 0) break;
-    batch = batch < 16 ? batch * 2 : 16;
+    warp_append(alive, v, lout, R.cnt + out);
+  }
+}
+
+__device__ void resolve_b(const Resolve& R, int in, int out, int64_t t0, int64_t nt) {
+  if (t0 == 0) R.cnt[in] = 0;
+  const int64_t cnt = (int64_t)vload(R.cnt + out);
+  const int32_t* lst = R.lists + (size_t)out * R.n;
+  const int32_t* mcur = R.mn + (size_t)out * R.n;
+  for (int64_t i = t0; i < cnt; i += nt) {
+    const int v = lst[i];
+    const int u = R.prop[v];
+    if (mcur[v] == v && mcur[u] == v) {
+      R.partner[v] = u;
+      R.partner[u] = v;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_resolve(Resolve R) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  int r = 1;
+  while (true) {
+    const int in = (r - 1) & 1, out = r & 1;
+    const unsigned long long live = vload(R.cnt + in);
+    if (live == 0) return;
+    if (live <= R.small) break;
+    resolve_a(R, in, out, t0, nt);
+    grid.sync();
+    resolve_b(R, in, out, t0, nt);
+    grid.sync();
+    ++r;
+  }
+  if (blockIdx.x != 0) return;
+  while (true) {
+    const int in = (r - 1) & 1, out = r & 1;
+    const unsigned long long live = vload(R.cnt + in);
+    __syncthreads();
+    if (live == 0) return;
+    resolve_a(R, in, out, threadIdx.x, blockDim.x);
+    __syncthreads();
+    resolve_b(R, in, out, threadIdx.x, blockDim.x);
+    __syncthreads();
+    ++r;
   }
 }
 
@@ -408,42 +579,32 @@ void device_match(Ctx& c, const DGraph& g, int32_t* partner) {
         if (!bc) continue;
         const int G = t < 4 ? TIER_G[t] : 32;
         const int32_t* list = tier_list(g, t);
-        const unsigned grid = grid_for(c, bc * G, 256);
+        const unsigned grid = grid_for(c, t < 4 ? bc : bc * 32, 256);
         launch(c, "propose", (g.unit_ew ? 8.0 : 12.0) * g.bin_nnz[t] + 12.0 * bc, [&] {
-          JET_TIER_LAUNCH(k_propose, G, g.unit_ew, grid, 256, 0, c.stream, gv, list, bc, partner,
-                          prop.get(), lists.get(), cnt.get());
+          if (t < 4)
+            JET_TIER_LAUNCH(k_propose, G, g.unit_ew, grid, 256, 0, c.stream, gv, list, bc, partner,
+                            prop.get(), lists.get(), cnt.get());
+          else if (g.unit_ew)
+            k_propose_long<true><<<grid, 256, 0, c.stream>>>(gv, list, bc, partner, prop.get(),
+                                                            lists.get(), cnt.get());
+          else
+            k_propose_long<false><<<grid, 256, 0, c.stream>>>(gv, list, bc, partner, prop.get(),
+                                                             lists.get(), cnt.get());
         });
       }
       unsigned long long ne = 0;
       d2h(c, &ne, cnt.get(), 1);
       c.sync();
       if (ne == 0) break;
-      // resolution rounds: list r%2 holds the live edges of round r
-      int r = 1, batch = 1;
-      const unsigned grid = grid_for(c, (int64_t)ne, 256);
-      while (true) {
-        for (int q = 0; q < batch; ++q, ++r) {
-          const int in = (r - 1) & 1, out = r & 1;
-          int32_t* mcur = mn.get() + (size_t)out * n;
-          int32_t* mprev = mn.get() + (size_t)in * n;
-          launch(c, "match_round", 0.0, [&] {
-            k_round_a<<<grid, 256, 0, c.stream>>>(prop.get(), partner, lists.get() + (size_t)in * n,
-                                                  cnt.get() + in, mcur, mprev,
-                                                  lists.get() + (size_t)out * n, cnt.get() + out);
-          });
-          launch(c, "match_round", 0.0, [&] {
-            k_round_b<<<grid, 256, 0, c.stream>>>(prop.get(), partner, lists.get() + (size_t)out * n,
-                                                  cnt.get() + out, mcur, cnt.get() + in);
-          });
-        }
-        unsigned long long live = 0;
-        d2h(c, &live, cnt.get() + ((r - 1) & 1), 1);
-        c.sync();
-        if (live == 0) break;
-        batch = batch < 16 ? batch * 2 : 16;
-      }
-      // one more A-pass with an empty list is not needed: the last round
-      // that produced live edges was followed by a round that reset them.
+      // all resolution rounds in one cooperative launch (k_resolve)
+      Resolve R{prop.get(), partner, lists.get(), cnt.get(), mn.get(), n, 4096ull};
+      const int blocks = std::min<int64_t>(coop_blocks(c, (const void*)k_resolve, 1024),
+                                           std::max<int64_t>(1, ((int64_t)ne + 1023) / 1024));
+      void* args[] = {&R};
+      launch(c, "match_resolve", 0.0, [&] {
+        CK(cudaLaunchCooperativeKernel((const void*)k_resolve, dim3(blocks), dim3(1024), args, 0,
+                                       c.stream));
+      });
     }
     two_hop(c, g, partner);
   }

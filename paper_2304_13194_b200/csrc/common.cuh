@@ -152,6 +152,8 @@ struct Ctx {
   // pinned host mirror for per-iteration scalars
   int64_t* pinned = nullptr;
   size_t pinned_elems = 0;
+  uint8_t* pinned_up = nullptr;  // host->device staging (per-pass scalars)
+  size_t pinned_up_bytes = 0;
   // scratch for CUB device-wide primitives
   DBuf<uint8_t> cub_tmp;
   // profiling
@@ -160,12 +162,16 @@ struct Ctx {
   std::vector<cudaEvent_t> event_pool;
   std::vector<ProfAgg> agg;
   std::map<std::string, int> cls_index;
+  std::string prof_only;  // empty: record every class
+  cudaEvent_t timer_a = nullptr, timer_b = nullptr;
+  DBuf<uint8_t> flush_buf;
   int32_t lock_epoch = 0;
 
   cudaEvent_t take_event();
   int prof_class(const char* name);
   void flush_prof();
   void ensure_pinned(size_t elems);
+  void ensure_pinned_up(size_t bytes);
   void sync() { CK(cudaStreamSynchronize(stream)); }
   void* cub_scratch(size_t bytes) {
     cub_tmp.ensure(bytes, stream);
@@ -178,7 +184,8 @@ struct Ctx {
 template <class F>
 inline void launch(Ctx& c, const char* name, double bytes, F&& f) {
   ProfRec r{};
-  if (c.prof) {
+  const bool rec = c.prof && (c.prof_only.empty() || c.prof_only == name);
+  if (rec) {
     r.cls = c.prof_class(name);
     r.a = c.take_event();
     r.b = c.take_event();
@@ -188,7 +195,7 @@ inline void launch(Ctx& c, const char* name, double bytes, F&& f) {
   f();
   CK(cudaGetLastError());
   c.launches++;
-  if (c.prof) {
+  if (rec) {
     CK(cudaEventRecord(r.b, c.stream));
     c.recs.push_back(r);
   }

@@ -63,6 +63,15 @@ void Ctx::ensure_pinned(size_t elems) {
   pinned_elems = want;
 }
 
+void Ctx::ensure_pinned_up(size_t bytes) {
+  if (bytes <= pinned_up_bytes) return;
+  if (pinned_up) cudaFreeHost(pinned_up);
+  pinned_up = nullptr;
+  size_t want = bytes < (1 << 20) ? (1 << 20) : bytes * 2;
+  CK(cudaMallocHost((void**)&pinned_up, want));
+  pinned_up_bytes = want;
+}
+
 }  // namespace jet
 
 using namespace jet;
@@ -111,12 +120,16 @@ void jet_destroy(jet_ctx* ctx) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   c->cub_tmp.release();
+  c->flush_buf.release();
+  if (c->timer_a) cudaEventDestroy(c->timer_a);
+  if (c->timer_b) cudaEventDestroy(c->timer_b);
   for (auto& r : c->recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
   }
   for (auto e : c->event_pool) cudaEventDestroy(e);
   if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->pinned_up) cudaFreeHost(c->pinned_up);
   cudaStreamSynchronize(c->stream);
   cudaStreamDestroy(c->stream);
   delete c;
@@ -137,6 +150,59 @@ int jet_profile_enable(jet_ctx* ctx, int on) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   c->prof = on != 0;
   return JET_OK;
+}
+
+int jet_profile_filter(jet_ctx* ctx, const char* name) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  c->prof_only = name ? name : "";
+  return JET_OK;
+}
+
+int jet_timer_start(jet_ctx* ctx) {
+  try {
+    Ctx* c = reinterpret_cast<Ctx*>(ctx);
+    CK(cudaSetDevice(c->device));
+    if (!c->timer_a) {
+      CK(cudaEventCreate(&c->timer_a));
+      CK(cudaEventCreate(&c->timer_b));
+    }
+    CK(cudaEventRecord(c->timer_a, c->stream));
+    return JET_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  }
+}
+
+int jet_timer_stop(jet_ctx* ctx, double* ms) {
+  try {
+    Ctx* c = reinterpret_cast<Ctx*>(ctx);
+    JET_REQUIRE(c->timer_a, JET_EINVAL, "timer not started");
+    CK(cudaEventRecord(c->timer_b, c->stream));
+    CK(cudaEventSynchronize(c->timer_b));
+    float f = 0;
+    CK(cudaEventElapsedTime(&f, c->timer_a, c->timer_b));
+    *ms = f;
+    return JET_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  }
+}
+
+int jet_flush_l2(jet_ctx* ctx) {
+  try {
+    Ctx* c = reinterpret_cast<Ctx*>(ctx);
+    CK(cudaSetDevice(c->device));
+    const size_t bytes = (size_t)256 << 20;  // 2x the 126 MB L2
+    c->flush_buf.ensure(bytes, c->stream);
+    CK(cudaMemsetAsync(c->flush_buf.get(), (int)(c->launches & 0xff), bytes, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return JET_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  }
 }
 
 int jet_profile_reset(jet_ctx* ctx) {

@@ -160,35 +160,85 @@ struct RbOp {
   static __device__ __forceinline__ void block_done(const Args&, long long) {}
 };
 
+// Tiers 0-3. A warp owns 32 consecutive list entries: vertex ids, offsets
+// and own parts are loaded once, coalesced. Rows are then swept in G steps
+// of 32/G rows (one G-lane group per row); U steps are batched so their
+// adjacency loads and neighbour-part gathers are all in flight together
+// (the single-row-per-warp form is latency-bound at ~300 GB/s). The result
+// of row r is shuffled to lane r, which finishes vertex r.
 template <class Op, int G, bool UNIT>
 __global__ void __launch_bounds__(256)
     k_agg_small(typename Op::Args a, GView g, const int32_t* __restrict__ parts,
-                const int32_t* __restrict__ list, int64_t cnt, bool wide) {
+                const int32_t* __restrict__ list, int64_t cnt, bool wide,
+                const unsigned long long* __restrict__ dcnt) {
+  if (dcnt) cnt = (int64_t)*dcnt;
+  constexpr int RPS = 32 / G;         // rows per step
+  constexpr int U = G >= 8 ? 8 : G;   // steps per batch (G steps in total)
   const unsigned gm = group_mask<G>();
-  const int lane = threadIdx.x & 31, gl = lane & (G - 1);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x / G;
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1), grp = lane / G;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   long long acc = 0;
-  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G; i < cnt; i += stride) {
-    const int v = list ? list[i] : (int)i;
-    const int own = parts[v];
-    if (Op::skip(a, v, own)) continue;  // uniform across the group
-    const int64_t b = g.offs[v];
-    const int deg = (int)(g.offs[v + 1] - b);
-    int p = -1, w = 0;
-    if (gl < deg) {
-      p = parts[g.adj[b + gl]];
-      w = UNIT ? 1 : g.ew[b + gl];
+  for (int64_t base = w0 * 32; base < cnt; base += nw * 32) {
+    const int64_t idx = base + lane;
+    int v = 0, own = -1, deg = 0;
+    int64_t beg = 0;
+    if (idx < cnt) {
+      v = list ? list[idx] : (int)idx;
+      own = parts[v];
+      if (Op::skip(a, v, own)) {
+        own = -1;
+      } else {
+        beg = g.offs[v];
+        deg = (int)(g.offs[v + 1] - beg);
+      }
     }
-    const unsigned peers = __match_any_sync(gm, p);
-    const long long s = UNIT ? (long long)__popc(peers) : peer_sum(peers, w, wide);
-    const bool lead = p >= 0 && (__ffs(peers) - 1) == lane;
-    long long self_c = (lead && p == own) ? s : 0;
-    unsigned long long key = (lead && p != own && Op::competes(a, p, own)) ? pack_best(s, p) : 0ull;
-    long long ex = p >= 0 ? Op::extra(a, p, w) : 0;
-    self_c = gsum<G>(self_c, gm);
-    key = gmax<G>(key, gm);
-    ex = gsum<G>(ex, gm);
-    if (gl == 0) Op::finish(a, v, own, self_c, key, ex, acc);
+    long long my_self = 0, my_ex = 0;
+    unsigned long long my_key = 0;
+#pragma unroll
+    for (int s0 = 0; s0 < G; s0 += U) {
+      int uu[U], ww[U], pp[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int r = (s0 + q) * RPS + grp;
+        const int64_t rb = __shfl_sync(0xffffffffu, beg, r);
+        const int rd = __shfl_sync(0xffffffffu, deg, r);
+        uu[q] = -1;
+        ww[q] = 0;
+        if (gl < rd) {
+          uu[q] = g.adj[rb + gl];
+          ww[q] = UNIT ? 1 : g.ew[rb + gl];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) pp[q] = uu[q] >= 0 ? parts[uu[q]] : -1;
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int st = s0 + q;
+        const int rown = __shfl_sync(0xffffffffu, own, st * RPS + grp);
+        const int p = pp[q];
+        const unsigned peers = __match_any_sync(gm, p);
+        const long long sm = UNIT ? (long long)__popc(peers) : peer_sum(peers, ww[q], wide);
+        const bool lead = p >= 0 && (__ffs(peers) - 1) == lane;
+        long long sc = (lead && p == rown) ? sm : 0;
+        unsigned long long key =
+            (lead && p != rown && Op::competes(a, p, rown)) ? pack_best(sm, p) : 0ull;
+        long long ex = p >= 0 ? Op::extra(a, p, ww[q]) : 0;
+        sc = gsum<G>(sc, gm);
+        key = gmax<G>(key, gm);
+        ex = gsum<G>(ex, gm);
+        const int src = ((lane - st * RPS) & (RPS - 1)) * G;
+        sc = __shfl_sync(0xffffffffu, sc, src);
+        key = __shfl_sync(0xffffffffu, key, src);
+        ex = __shfl_sync(0xffffffffu, ex, src);
+        if (lane / RPS == st) {
+          my_self = sc;
+          my_key = key;
+          my_ex = ex;
+        }
+      }
+    }
+    if (own >= 0) Op::finish(a, v, own, my_self, my_key, my_ex, acc);
   }
   Op::block_done(a, acc);
 }
@@ -199,7 +249,8 @@ template <class Op, bool UNIT>
 __global__ void __launch_bounds__(256)
     k_agg_warp(typename Op::Args a, GView g, const int32_t* __restrict__ parts,
                const int32_t* __restrict__ list, int64_t cnt, bool wide, int k,
-               int tl_cap) {
+               int tl_cap, const unsigned long long* __restrict__ dcnt) {
+  if (dcnt) cnt = (int64_t)*dcnt;
   extern __shared__ unsigned long long smem[];
   const int wib = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
   const size_t per = (size_t)k + (size_t)(tl_cap + 3) / 2;
@@ -261,7 +312,9 @@ __global__ void __launch_bounds__(256)
 template <class Op, bool UNIT>
 __global__ void __launch_bounds__(256)
     k_agg_block(typename Op::Args a, GView g, const int32_t* __restrict__ parts,
-                const int32_t* __restrict__ list, int64_t cnt, bool wide, int k) {
+                const int32_t* __restrict__ list, int64_t cnt, bool wide, int k,
+                const unsigned long long* __restrict__ dcnt) {
+  if (dcnt) cnt = (int64_t)*dcnt;
   extern __shared__ unsigned long long smem[];
   unsigned long long* tab = smem;
   int* tl = reinterpret_cast<int*>(tab + k);
@@ -344,9 +397,13 @@ static int warp_tier_warps(const Ctx& c, int k, int tl_cap, size_t* smem_out) {
 
 // Launch an aggregation Op over every non-empty tier of g; mk(t) returns the
 // Op arguments for tier t (per-tier output lists).
+// dlists/dcnts (optional): per-tier vertex lists with device-side lengths
+// replace the level's tier lists (the host bound stays g.bin_cnt[t]).
 template <class Op, class MakeArgs>
 static void run_agg(Ctx& c, const DGraph& g, MakeArgs mk, const int32_t* parts,
-                    int k, const char* name, double bytes_per_vertex) {
+                    int k, const char* name, double bytes_per_vertex,
+                    int32_t* const* dlists = nullptr,
+                    const unsigned long long* dcnts = nullptr) {
   const bool wide = g.max_ew >= (1LL << 26);
   const GView gv = view(g);
   const double bpe = g.unit_ew ? 8.0 : 12.0;  // adj + gathered part (+ weight)
@@ -354,26 +411,28 @@ static void run_agg(Ctx& c, const DGraph& g, MakeArgs mk, const int32_t* parts,
     const int64_t cnt = g.bin_cnt[t];
     if (!cnt) continue;
     const typename Op::Args a = mk(t);
-    const int32_t* list = tier_list(g, t);
-    const double bytes = bpe * g.bin_nnz[t] + (bytes_per_vertex + (list ? 4.0 : 0.0)) * cnt;
+    const int32_t* list = dlists ? dlists[t] : tier_list(g, t);
+    const unsigned long long* dc = dcnts ? dcnts + t : nullptr;
+    const double bytes =
+        dlists ? 0.0 : bpe * g.bin_nnz[t] + (bytes_per_vertex + (list ? 4.0 : 0.0)) * cnt;
     if (t < 4) {
       const int G = TIER_G[t];
-      const unsigned grid = grid_for(c, cnt * G, 256);
+      const unsigned grid = grid_for(c, cnt, 256);
       launch(c, name, bytes, [&] {
 #define AGG_K(GG, UU) k_agg_small<Op, GG, UU>
         if (g.unit_ew) {
           switch (G) {
-            case 4: AGG_K(4, true)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide); break;
-            case 8: AGG_K(8, true)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide); break;
-            case 16: AGG_K(16, true)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide); break;
-            default: AGG_K(32, true)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide); break;
+            case 4: AGG_K(4, true)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
+            case 8: AGG_K(8, true)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
+            case 16: AGG_K(16, true)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
+            default: AGG_K(32, true)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
           }
         } else {
           switch (G) {
-            case 4: AGG_K(4, false)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide); break;
-            case 8: AGG_K(8, false)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide); break;
-            case 16: AGG_K(16, false)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide); break;
-            default: AGG_K(32, false)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide); break;
+            case 4: AGG_K(4, false)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
+            case 8: AGG_K(8, false)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
+            case 16: AGG_K(16, false)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
+            default: AGG_K(32, false)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
           }
         }
 #undef AGG_K
@@ -386,7 +445,7 @@ static void run_agg(Ctx& c, const DGraph& g, MakeArgs mk, const int32_t* parts,
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       const unsigned grid = grid_for(c, cnt * 32, nw * 32, 2048 / (nw * 32));
       launch(c, name, bytes, [&] {
-        kern<<<grid, nw * 32, smem, c.stream>>>(a, gv, parts, list, cnt, wide, k, tl_cap);
+        kern<<<grid, nw * 32, smem, c.stream>>>(a, gv, parts, list, cnt, wide, k, tl_cap, dc);
       });
     } else {
       const size_t smem = (size_t)k * 12;
@@ -396,7 +455,7 @@ static void run_agg(Ctx& c, const DGraph& g, MakeArgs mk, const int32_t* parts,
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       const unsigned grid = grid_for(c, cnt * 256, 256, 2);
       launch(c, name, bytes, [&] {
-        kern<<<grid, 256, smem, c.stream>>>(a, gv, parts, list, cnt, wide, k);
+        kern<<<grid, 256, smem, c.stream>>>(a, gv, parts, list, cnt, wide, k, dc);
       });
     }
   }
@@ -408,6 +467,10 @@ static void run_agg(Ctx& c, const DGraph& g, MakeArgs mk, const int32_t* parts,
 // The list length lives on the device (written by the preceding kernel).
 // ===========================================================================
 
+struct RbSegsDev {
+  int64_t b[NBINS];
+};
+
 struct AbArgs {
   const int32_t* parts;
   const int32_t* cdest;
@@ -418,38 +481,49 @@ struct AbArgs {
   long long* f2_out;  // optional (parity entry point)
 };
 
-template <int G, bool UNIT>
+// Segmented vertex lists (one per tier) with device-side lengths.
+struct SegLists {
+  const int32_t* list[NBINS];
+  const unsigned long long* cnt;  // NBINS consecutive counters
+};
+
+// One warp per candidate over all tiers (candidate sets are small).
+template <bool UNIT>
 __global__ void __launch_bounds__(256)
-    k_afterburner(AbArgs a, GView g, const int32_t* __restrict__ list,
-                  const unsigned long long* __restrict__ cnt_ptr) {
-  const unsigned gm = group_mask<G>();
-  const int gl = threadIdx.x & (G - 1);
-  const int64_t cnt = (int64_t)*cnt_ptr;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x / G;
-  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G; i < cnt; i += stride) {
-    const int v = list[i];
-    const int own = a.parts[v];
-    const int dv = a.cdest[v];
-    const long long Fv = a.F[v];
-    const int64_t b = g.offs[v], e = g.offs[v + 1];
-    long long f2 = 0;
-    for (int64_t j = b + gl; j < e; j += G) {
-      const int u = g.adj[j];
-      int eff = a.parts[u];
-      const int cu = a.cdest[u];
-      if (cu >= 0) {
-        const long long Fu = a.F[u];
-        if (Fu > Fv || (Fu == Fv && u < v)) eff = cu;
+    k_afterburner(AbArgs a, GView g, SegLists sl, RbSegsDev mseg) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int t = 0; t < NBINS; ++t) {
+    const int64_t cnt = (int64_t)sl.cnt[t];
+    const int32_t* list = sl.list[t];
+    for (int64_t i = w0; i < cnt; i += ws) {
+      const int v = list[i];
+      const int own = a.parts[v];
+      const int dv = a.cdest[v];
+      const long long Fv = a.F[v];
+      const int64_t b = g.offs[v], e = g.offs[v + 1];
+      long long f2 = 0;
+      for (int64_t j = b + lane; j < e; j += 32) {
+        const int u = g.adj[j];
+        int eff = a.parts[u];
+        const int cu = a.cdest[u];
+        if (cu >= 0) {
+          const long long Fu = a.F[u];
+          if (Fu > Fv || (Fu == Fv && u < v)) eff = cu;
+        }
+        const int w = UNIT ? 1 : g.ew[j];
+        f2 += (eff == dv) ? w : (eff == own) ? -w : 0;
       }
-      const int w = UNIT ? 1 : g.ew[j];
-      f2 += (eff == dv) ? w : (eff == own) ? -w : 0;
-    }
-    f2 = gsum<G>(f2, gm);
-    if (gl == 0) {
-      if (a.f2_out) a.f2_out[v] = f2;
-      const bool mvv = f2 >= 0;
-      if (mvv && a.move_list) a.mv[v] = dv;
-      if (a.move_list) warp_append(mvv, v, a.move_list, a.move_cnt);
+      f2 = gsum<32>(f2, 0xffffffffu);
+      if (lane == 0) {
+        if (a.f2_out) a.f2_out[v] = f2;
+        if (a.move_list && f2 >= 0) {
+          a.mv[v] = dv;
+          const unsigned long long q = atomicAdd(a.move_cnt + t, 1ull);
+          a.move_list[mseg.b[t] + q] = v;
+        }
+      }
     }
   }
 }
@@ -465,36 +539,37 @@ struct ApArgs {
 // Exact cut delta of a move batch (conn.py:231-248): for a moved v and
 // neighbour u, c = w([p'(u) != dest] - [p(u) != old]); edges with both ends
 // moved appear twice and are halved, so we sum 2c / c and halve at the end.
-template <int G, bool UNIT>
-__global__ void __launch_bounds__(256)
-    k_apply_delta(ApArgs a, GView g, const int32_t* __restrict__ list,
-                  const unsigned long long* __restrict__ cnt_ptr) {
-  const unsigned gm = group_mask<G>();
-  const int gl = threadIdx.x & (G - 1);
-  const int64_t cnt = (int64_t)*cnt_ptr;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x / G;
+template <bool UNIT>
+__global__ void __launch_bounds__(256) k_apply_delta(ApArgs a, GView g, SegLists sl) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
   long long acc = 0;
-  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G; i < cnt; i += stride) {
-    const int v = list[i];
-    const int old = a.parts[v];
-    const int dst = a.mv[v];
-    const int64_t b = g.offs[v], e = g.offs[v + 1];
-    long long d = 0;
-    for (int64_t j = b + gl; j < e; j += G) {
-      const int u = g.adj[j];
-      const int pu = a.parts[u];
-      const int mu = a.mv[u];
-      const int nu = mu >= 0 ? mu : pu;
-      const long long w = UNIT ? 1 : g.ew[j];
-      const long long cc = w * ((long long)(nu != dst) - (long long)(pu != old));
-      d += mu >= 0 ? cc : 2 * cc;
-    }
-    d = gsum<G>(d, gm);
-    if (gl == 0) {
-      acc += d;
-      const unsigned long long wv = (unsigned long long)g.vw[v];
-      atomicAdd(&a.pw[dst], wv);
-      atomicAdd(&a.pw[old], (unsigned long long)(-(long long)wv));
+  for (int t = 0; t < NBINS; ++t) {
+    const int64_t cnt = (int64_t)sl.cnt[t];
+    const int32_t* list = sl.list[t];
+    for (int64_t i = w0; i < cnt; i += ws) {
+      const int v = list[i];
+      const int old = a.parts[v];
+      const int dst = a.mv[v];
+      const int64_t b = g.offs[v], e = g.offs[v + 1];
+      long long d = 0;
+      for (int64_t j = b + lane; j < e; j += 32) {
+        const int u = g.adj[j];
+        const int pu = a.parts[u];
+        const int mu = a.mv[u];
+        const int nu = mu >= 0 ? mu : pu;
+        const long long w = UNIT ? 1 : g.ew[j];
+        const long long cc = w * ((long long)(nu != dst) - (long long)(pu != old));
+        d += mu >= 0 ? cc : 2 * cc;
+      }
+      d = gsum<32>(d, 0xffffffffu);
+      if (lane == 0) {
+        acc += d;
+        const unsigned long long wv = (unsigned long long)g.vw[v];
+        atomicAdd(&a.pw[dst], wv);
+        atomicAdd(&a.pw[old], (unsigned long long)(-(long long)wv));
+      }
     }
   }
   block_sum_atomic<256>(acc, a.cut2d);
@@ -586,28 +661,28 @@ void Workspace::bind_level(const DGraph& g) {
 // ===========================================================================
 // Jetlp pass
 // ===========================================================================
-struct RbSegs {
-  int64_t b[NBINS];
-};
+static SegLists seg_lists(Workspace& w, bool moves) {
+  SegLists sl;
+  for (int t = 0; t < NBINS; ++t) sl.list[t] = moves ? w.move_list(t) : w.cand_list(t);
+  sl.cnt = w.ctr.get() + (moves ? CTR_MOVE : CTR_CAND);
+  return sl;
+}
 
 static void launch_rows_reduce_ab(Ctx& c, Workspace& w, const DGraph& g, const AbArgs& a) {
   const GView gv = view(g);
-  const double bpe = g.unit_ew ? 21.0 : 25.0;  // adj, w, part, cdest(+F) per entry
-  for (int t = 0; t < NBINS; ++t) {
-    if (!g.bin_cnt[t]) continue;
-    const int G = t < 4 ? TIER_G[t] : 32;
-    const int32_t* list = w.cand_list(t);
-    const unsigned long long* cnt = w.ctr.get() + CTR_CAND + t;
-    AbArgs at = a;
-    at.move_list = a.move_list ? w.move_list(t) : nullptr;
-    at.move_cnt = w.ctr.get() + CTR_MOVE + t;
-    const unsigned grid = grid_for(c, g.bin_cnt[t] * G, 256);
-    // bytes: candidates are unknown on the host; account for the tier's
-    // rows scaled by the candidate fraction measured later (profiling only)
-    launch(c, "afterburner", bpe * g.bin_nnz[t] * 0.0, [&] {
-      JET_TIER_LAUNCH(k_afterburner, G, g.unit_ew, grid, 256, 0, c.stream, at, gv, list, cnt);
-    });
+  AbArgs at = a;
+  RbSegsDev ms;
+  for (int t = 0; t < NBINS; ++t) ms.b[t] = w.seg_base[t];
+  if (a.move_list) {
+    at.move_list = w.lists.get() + w.cap_n;
+    at.move_cnt = w.ctr.get() + CTR_MOVE;
   }
+  const SegLists sl = seg_lists(w, false);
+  const unsigned grid = grid_for(c, g.n * 32, 256, 4);
+  launch(c, "afterburner", 0.0, [&] {
+    if (g.unit_ew) k_afterburner<true><<<grid, 256, 0, c.stream>>>(at, gv, sl, ms);
+    else k_afterburner<false><<<grid, 256, 0, c.stream>>>(at, gv, sl, ms);
+  });
 }
 
 void lp_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts, int k,
@@ -646,7 +721,7 @@ void lp_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts, int k,
 // the per-tier candidate lists.
 __global__ void k_distribute(const int32_t* __restrict__ cand, int64_t ncand,
                              const int64_t* __restrict__ offs, int32_t* lists,
-                             RbSegs segs, unsigned long long* cnts) {
+                             RbSegsDev segs, unsigned long long* cnts) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t lim = (ncand + blockDim.x - 1) / blockDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < lim; i += stride) {
@@ -663,7 +738,7 @@ __global__ void k_distribute(const int32_t* __restrict__ cand, int64_t ncand,
 void afterburner_only(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
                       const int32_t* cand, int64_t ncand, long long* out_f2) {
   dzero(c, w.ctr.get(), CTR_PW);
-  RbSegs segs;
+  RbSegsDev segs;
   for (int t = 0; t < NBINS; ++t) segs.b[t] = w.seg_base[t];
   if (ncand > 0) {
     launch(c, "distribute", 8.0 * ncand, [&] {
@@ -688,16 +763,12 @@ ApplyResult apply_moves(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts,
                         int k, bool set_lock, int32_t epoch) {
   const GView gv = view(g);
   ApArgs a{parts, w.mv.get(), w.ctr.get() + CTR_PW, w.ctr.get() + CTR_CUT2D, k};
-  for (int t = 0; t < NBINS; ++t) {
-    if (!g.bin_cnt[t]) continue;
-    const int G = t < 4 ? TIER_G[t] : 32;
-    const int32_t* list = w.move_list(t);
-    const unsigned long long* cnt = w.ctr.get() + CTR_MOVE + t;
-    const unsigned grid = grid_for(c, g.bin_cnt[t] * G, 256);
-    launch(c, "apply_delta", 0.0, [&] {
-      JET_TIER_LAUNCH(k_apply_delta, G, g.unit_ew, grid, 256, 0, c.stream, a, gv, list, cnt);
-    });
-  }
+  const SegLists sl = seg_lists(w, true);
+  const unsigned grid = grid_for(c, g.n * 32, 256, 4);
+  launch(c, "apply_delta", 0.0, [&] {
+    if (g.unit_ew) k_apply_delta<true><<<grid, 256, 0, c.stream>>>(a, gv, sl);
+    else k_apply_delta<false><<<grid, 256, 0, c.stream>>>(a, gv, sl);
+  });
   CommitArgs ca{};
   ca.parts = parts;
   ca.mv = w.mv.get();
@@ -864,27 +935,208 @@ __global__ void k_rb_find(RbSel s, const long long* __restrict__ deficit,
   }
 }
 
+// Selected iff (bucket, id) < the part's threshold (select_prefix). Weak
+// passes with direct=1 commit vertices that have a valid destination right
+// away (their order is unobservable); everything else (weak: vertices that
+// need a random destination; strong: all) goes to the evict list.
 __global__ void k_rb_select(RbSel s, const int32_t* __restrict__ rcand,
-                            const unsigned long long* __restrict__ cnt_ptr, int nb,
-                            int32_t* evict, unsigned long long* evict_cnt,
-                            unsigned long long* keys) {
+                            const unsigned long long* __restrict__ cnt_ptr,
+                            const int32_t* __restrict__ rbest, int strong, int direct,
+                            int32_t* evict, unsigned long long* evict_cnt, int32_t* mv,
+                            const int64_t* __restrict__ offs, int32_t* move_lists,
+                            RbSegsDev mseg, unsigned long long* move_cnt) {
   const int64_t cnt = (int64_t)*cnt_ptr;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t lim = (cnt + blockDim.x - 1) / blockDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < lim; i += stride) {
-    bool sel = false;
-    int v = 0;
+    bool sel = false, now = false;
+    int v = 0, t = -1;
     if (i < cnt) {
       v = rcand[i];
       const int op = s.opidx[s.parts[v]];
       const int rk = s.rkey[v];
       const int bs = s.bstar[op];
       sel = rk < bs || (rk == bs && v < s.thr[op]);
+      if (sel && !strong && direct) {
+        const int bp = rbest[v];
+        if (bp >= 0) {
+          now = true;
+          mv[v] = bp;
+          t = tier_of_degree(offs[v + 1] - offs[v]);
+        }
+      }
     }
-    warp_append(sel, v, evict, evict_cnt);
+    warp_append(sel && !now, v, evict, evict_cnt);
+    for (int tt = 0; tt < NBINS; ++tt)
+      warp_append(t == tt, v, move_lists + mseg.b[tt], move_cnt + tt);
   }
-  (void)nb;
-  (void)keys;
+}
+
+// Collect the vertices of oversized parts into per-tier candidate lists.
+__global__ void k_rb_collect(const int32_t* __restrict__ parts, const int32_t* __restrict__ opidx,
+                             const int64_t* __restrict__ offs, int64_t n, int32_t* lists,
+                             RbSegsDev seg, unsigned long long* cnts) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t lim = (n + blockDim.x - 1) / blockDim.x * blockDim.x;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < lim; v += stride) {
+    int t = -1;
+    if (v < n && opidx[parts[v]] >= 0) t = tier_of_degree(offs[v + 1] - offs[v]);
+    if (__ballot_sync(0xffffffffu, t >= 0) == 0) continue;
+    for (int tt = 0; tt < NBINS; ++tt) warp_append(t == tt, (int32_t)v, lists + seg.b[tt], cnts + tt);
+  }
+}
+
+// Single-block tail for small evicted sets (length read on device, bounded
+// on the host by sum(deficit) <= cap): bitonic sort of (part, bucket, id)
+// keys in shared memory, then weak: valid[draw[i]] in order; strong:
+// next-fit (rebalance.py:224-236); then commit the moves.
+struct RbTail {
+  const int32_t* evict;
+  const unsigned long long* evict_cnt;
+  const int32_t* parts;
+  const int32_t* opidx;
+  const int32_t* rkey;
+  const int32_t* vw;
+  const int64_t* offs;
+  const int32_t* valid_list;
+  const int32_t* draws;
+  const long long* spare;
+  int nvalid;
+  int nb;
+  int strong;
+  int32_t* mv;
+  int32_t* move_lists;
+  RbSegsDev mseg;
+  unsigned long long* move_cnt;
+};
+
+__global__ void __launch_bounds__(1024) k_rb_tail(RbTail a) {
+  extern __shared__ unsigned long long sk[];
+  __shared__ long long s_room;
+  __shared__ int s_di, s_done;
+  __shared__ long long s_wsum[32];
+  const int tid = threadIdx.x;
+  const int L = (int)*a.evict_cnt;
+  int P2 = 1;
+  while (P2 < L) P2 <<= 1;
+  for (int i = tid; i < P2; i += blockDim.x) {
+    unsigned long long key = ~0ull;
+    if (i < L) {
+      const int v = a.evict[i];
+      const unsigned long long grp =
+          (unsigned long long)a.opidx[a.parts[v]] * (unsigned)a.nb + (unsigned)a.rkey[v];
+      key = (grp << 32) | (unsigned)v;
+    }
+    sk[i] = key;
+  }
+  __syncthreads();
+  for (int size = 2; size <= P2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < P2; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool asc = (i & size) == 0;
+          const unsigned long long x = sk[i], y = sk[j];
+          if ((x > y) == asc) {
+            sk[i] = y;
+            sk[j] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (!a.strong) {
+    for (int i = tid; i < L; i += blockDim.x) {
+      const int v = (int)(sk[i] & 0xffffffffu);
+      a.mv[v] = a.valid_list[a.draws[i]];
+      const int t = tier_of_degree(a.offs[v + 1] - a.offs[v]);
+      const unsigned long long q = atomicAdd(a.move_cnt + t, 1ull);
+      a.move_lists[a.mseg.b[t] + q] = v;
+    }
+    return;
+  }
+  // next-fit; sequential over runs but each run is a parallel prefix test
+  if (tid == 0) {
+    s_di = 0;
+    s_room = a.nvalid > 0 ? a.spare[0] : 0;
+    s_done = a.nvalid <= 0;
+  }
+  __syncthreads();
+  for (int base = 0; base < L; base += blockDim.x) {
+    const int i = base + tid;
+    const long long w = i < L ? (long long)a.vw[(int)(sk[i] & 0xffffffffu)] : 0;
+    // block inclusive scan of w
+    long long ps = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, ps, o);
+      if ((tid & 31) >= o) ps += y;
+    }
+    if ((tid & 31) == 31) s_wsum[tid >> 5] = ps;
+    __syncthreads();
+    if (tid < 32) {
+      long long x = s_wsum[tid];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (tid >= o) x += y;
+      }
+      s_wsum[tid] = x;
+    }
+    __syncthreads();
+    if (tid >= 32) ps += s_wsum[(tid >> 5) - 1];
+    const int lim = L - base < (int)blockDim.x ? L - base : (int)blockDim.x;
+    // stash inclusive sums in the (already consumed) key slots' upper half:
+    // keep them in a dedicated region after the keys instead
+    long long* pbuf = reinterpret_cast<long long*>(sk + P2);
+    pbuf[tid] = ps;
+    __syncthreads();
+    int pos = 0;
+    long long before = 0;
+    while (true) {
+      if (s_done) break;
+      const long long room = s_room;
+      const bool fits = tid >= pos && tid < lim && ps - before <= room;
+      __shared__ int s_first;
+      if (tid == 0) s_first = lim;
+      __syncthreads();
+      if (tid >= pos && tid < lim && !fits) atomicMin(&s_first, tid);
+      __syncthreads();
+      const int e = s_first;
+      if (fits) {
+        const int v = (int)(sk[i] & 0xffffffffu);
+        a.mv[v] = a.valid_list[s_di];
+        const int t = tier_of_degree(a.offs[v + 1] - a.offs[v]);
+        const unsigned long long q = atomicAdd(a.move_cnt + t, 1ull);
+        a.move_lists[a.mseg.b[t] + q] = v;
+      }
+      __syncthreads();
+      if (e >= lim) {
+        if (tid == 0) s_room = room - (pbuf[lim - 1] - before);
+        __syncthreads();
+        break;
+      }
+      if (tid == 0) {
+        const long long prev = e > 0 ? pbuf[e - 1] : 0;
+        long long r = room - (prev - before);
+        const long long we = pbuf[e] - prev;
+        int di = s_di;
+        while (di < a.nvalid && r < we) {
+          di++;
+          r = di < a.nvalid ? a.spare[di] : 0;
+        }
+        s_di = di;
+        s_room = r;
+        if (di >= a.nvalid) s_done = 1;
+      }
+      __syncthreads();
+      pos = e;
+      before = e > 0 ? pbuf[e - 1] : 0;
+    }
+    __syncthreads();
+    if (s_done) break;
+  }
 }
 
 __global__ void k_rb_keys(const int32_t* __restrict__ evict, int64_t L,
@@ -1051,6 +1303,25 @@ static int ceil_log2(int64_t x) {
   return r;
 }
 
+constexpr int TAIL_CAP = 24576;  // evicted vertices ordered by the single-block tail
+
+namespace {
+// Packs per-pass host scalars into one pinned buffer for a single H2D copy.
+struct Packer {
+  std::vector<uint8_t>* host;
+  size_t off = 0;
+  template <class T>
+  size_t put(const T* src, size_t count) {
+    off = (off + 15) & ~size_t(15);
+    const size_t at = off;
+    off += count * sizeof(T);
+    if (host->size() < off) host->resize(off);
+    if (count) memcpy(host->data() + at, src, count * sizeof(T));
+    return at;
+  }
+};
+}  // namespace
+
 bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
                     int k, int64_t limit, int64_t sigma, int sub_buckets,
                     bool strong, Pcg64& rng, RebalanceOut* out) {
@@ -1075,15 +1346,18 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
   // scalars in the reference's own float64 expressions (rebalance.py:127-131)
   const int64_t W = g.total_vw;
   std::vector<double> h_hb(nover);
-  std::vector<long long> h_def(nover), h_req(nover);
+  std::vector<long long> h_def(nover), h_req(nover), h_spare(nvalid);
+  long long sum_def = 0;
   for (int i = 0; i < nover; ++i) {
     const int64_t pwp = pw[h_opart[i]];
     h_def[i] = pwp - (sigma + 1);
     h_req[i] = pwp - limit;
+    sum_def += h_def[i];
     volatile double ideal = (double)W / (double)k;
     volatile double diff = (double)pwp - ideal;
     h_hb[i] = 1.5 * diff;
   }
+  for (int i = 0; i < nvalid; ++i) h_spare[i] = sigma - pw[h_valid_list[i]];
   int rho = sub_buckets;
   if ((int64_t)rho >= g.n) rho = 1;  // (slot, v % rho, v) == (slot, v)
   JET_REQUIRE(rho <= 4096, JET_EUNSUPPORTED, "sub_buckets > 4096 is not supported on the GPU path");
@@ -1091,25 +1365,56 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
   const int ns = 34 - slot_min;
   const int nb = ns * rho;
   const int nch = (int)(((g.n + rho - 1) / rho + 31) / 32);
+  // at most sum(deficit) vertices leave (every selected weight is >= 1)
+  const bool fast = out == nullptr && sum_def <= TAIL_CAP;
+  const bool direct = out == nullptr;
+
+  std::vector<uint8_t>& up = w.h_up;
+  Packer pk{&up};
+  const size_t o_opidx = pk.put(h_opidx.data(), k);
+  const size_t o_valid = pk.put(h_valid.data(), k);
+  const size_t o_vlist = pk.put(h_valid_list.data(), nvalid);
+  const size_t o_opart = pk.put(h_opart.data(), nover);
+  const size_t o_hb = pk.put(h_hb.data(), nover);
+  const size_t o_def = pk.put(h_def.data(), nover);
+  const size_t o_req = pk.put(h_req.data(), nover);
+  const size_t o_spare = pk.put(h_spare.data(), nvalid);
+  const size_t up_bytes = (pk.off + 15) & ~size_t(15);
+  c.ensure_pinned_up(up_bytes + (size_t)std::max<long long>(sum_def, 1) * 4 + 64);
+  memcpy(c.pinned_up, up.data(), up_bytes);
+  w.up.ensure(up_bytes + 64, c.stream);
+  uint8_t* U = w.up.get();
+  h2d(c, U, c.pinned_up, up_bytes);
+  const int32_t* d_opidx = (const int32_t*)(U + o_opidx);
+  const uint8_t* d_valid = U + o_valid;
+  const int32_t* d_vlist = (const int32_t*)(U + o_vlist);
+  const int32_t* d_opart = (const int32_t*)(U + o_opart);
+  const double* d_hb = (const double*)(U + o_hb);
+  const long long* d_def = (const long long*)(U + o_def);
+  const long long* d_req = (const long long*)(U + o_req);
+  const long long* d_spare = (const long long*)(U + o_spare);
+
   w.H.ensure((size_t)nover * nb, c.stream);
   w.CH.ensure((size_t)nover * nch, c.stream);
   dzero(c, w.H.get(), (size_t)nover * nb);
   dzero(c, w.CH.get(), (size_t)nover * nch);
-  h2d(c, w.opidx.get(), h_opidx.data(), k);
-  h2d(c, w.valid.get(), h_valid.data(), k);
-  h2d(c, w.valid_list.get(), h_valid_list.data(), nvalid);
-  h2d(c, w.hb.get(), h_hb.data(), nover);
-  h2d(c, w.deficit.get(), h_def.data(), nover);
-  h2d(c, w.required.get(), h_req.data(), nover);
-  DBuf<int32_t> d_opart(nover, c.stream);
-  h2d(c, d_opart.get(), h_opart.data(), nover);
 
+  RbSegsDev cseg, mseg;
+  for (int t = 0; t < NBINS; ++t) {
+    cseg.b[t] = w.seg_base[t];
+    mseg.b[t] = w.seg_base[t];
+  }
+  launch(c, "rb_collect", 8.0 * g.n, [&] {
+    k_rb_collect<<<grid_for(c, g.n, 256), 256, 0, c.stream>>>(parts, d_opidx, g.offs.get(), g.n,
+                                                             w.lists.get(), cseg,
+                                                             w.ctr.get() + CTR_CAND);
+  });
   RbOp::Args ra{};
   ra.parts = parts;
   ra.vw = g.vw.get();
-  ra.opidx = w.opidx.get();
-  ra.valid = w.valid.get();
-  ra.hb = w.hb.get();
+  ra.opidx = d_opidx;
+  ra.valid = d_valid;
+  ra.hb = d_hb;
   ra.nvalid = nvalid;
   ra.strong = strong;
   ra.rho = rho;
@@ -1121,27 +1426,67 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
   ra.rcand = w.rcand.get();
   ra.rcand_cnt = w.ctr.get() + CTR_RCAND;
   ra.H = w.H.get();
-  run_agg<RbOp>(c, g, [&](int) { return ra; }, parts, k, "rb_stats", 16.0);
+  int32_t* clists[NBINS];
+  for (int t = 0; t < NBINS; ++t) clists[t] = w.cand_list(t);
+  run_agg<RbOp>(c, g, [&](int) { return ra; }, parts, k, "rb_stats", 16.0, clists,
+                w.ctr.get() + CTR_CAND);
 
+  int32_t* bstar = w.bstar.get();
   launch(c, "rb_scan", 8.0 * nover * nb, [&] {
-    k_rb_scan<<<nover, 256, 0, c.stream>>>(w.H.get(), nb, w.deficit.get(), w.bstar.get(),
-                                           w.cum_before.get());
+    k_rb_scan<<<nover, 256, 0, c.stream>>>(w.H.get(), nb, d_def, bstar, w.cum_before.get());
   });
-  RbSel s{parts, g.vw.get(), w.opidx.get(), w.rkey.get(), w.bstar.get(), w.thr.get(),
-          rho, nch, w.CH.get()};
+  RbSel s{parts, g.vw.get(), d_opidx, w.rkey.get(), bstar, w.thr.get(), rho, nch, w.CH.get()};
   const unsigned long long* rc = w.ctr.get() + CTR_RCAND;
   launch(c, "rb_chunk", 0.0, [&] {
     k_rb_chunk<<<grid_for(c, g.n, 256), 256, 0, c.stream>>>(s, w.rcand.get(), rc);
   });
   launch(c, "rb_find", 8.0 * nover * nch, [&] {
-    k_rb_find<<<nover, 256, 0, c.stream>>>(s, w.deficit.get(), w.required.get(),
-                                           w.cum_before.get(), d_opart.get(), g.n, nb,
+    k_rb_find<<<nover, 256, 0, c.stream>>>(s, d_def, d_req, w.cum_before.get(), d_opart, g.n, nb,
                                            w.thr.get());
   });
+  int32_t* move_base = w.lists.get() + w.cap_n;
   launch(c, "rb_select", 0.0, [&] {
     k_rb_select<<<grid_for(c, g.n, 256), 256, 0, c.stream>>>(
-        s, w.rcand.get(), rc, nb, w.evict.get(), w.ctr.get() + CTR_EVICT, nullptr);
+        s, w.rcand.get(), rc, w.rbest.get(), strong, direct ? 1 : 0, w.evict.get(),
+        w.ctr.get() + CTR_EVICT, w.mv.get(), g.offs.get(), move_base, mseg, w.ctr.get() + CTR_MOVE);
   });
+
+  if (fast) {
+    RbTail tl{};
+    tl.evict = w.evict.get();
+    tl.evict_cnt = w.ctr.get() + CTR_EVICT;
+    tl.parts = parts;
+    tl.opidx = d_opidx;
+    tl.rkey = w.rkey.get();
+    tl.vw = g.vw.get();
+    tl.offs = g.offs.get();
+    tl.valid_list = d_vlist;
+    tl.spare = d_spare;
+    tl.nvalid = nvalid;
+    tl.nb = nb;
+    tl.strong = strong;
+    tl.mv = w.mv.get();
+    tl.move_lists = move_base;
+    tl.mseg = mseg;
+    tl.move_cnt = w.ctr.get() + CTR_MOVE;
+    if (!strong) {
+      // draws for the (at most sum_def) vertices without a valid connection,
+      // generated on the host while the kernels above run
+      const long long D = sum_def;
+      int32_t* hd = reinterpret_cast<int32_t*>(c.pinned_up + up_bytes);
+      for (long long i = 0; i < D; ++i) hd[i] = (int32_t)rng.bounded((uint64_t)nvalid);
+      w.draws.ensure(D > 0 ? D : 1, c.stream);
+      h2d(c, w.draws.get(), hd, D);
+      tl.draws = w.draws.get();
+    }
+    const size_t smem = (size_t)TAIL_CAP * 8 + 1024 * 8;
+    CK(cudaFuncSetAttribute(k_rb_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    launch(c, "rb_tail", 0.0, [&] { k_rb_tail<<<1, 1024, smem, c.stream>>>(tl); });
+    return true;
+  }
+
+  // slow path (large evicted sets, or the parity entry point): order with a
+  // device radix sort after reading the evicted count back
   int64_t L = 0;
   d2h(c, &L, reinterpret_cast<int64_t*>(w.ctr.get() + CTR_EVICT), 1);
   c.sync();
@@ -1153,9 +1498,8 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
     }
     return true;
   }
-  // order the evicted set by (oversized part, bucket, id) — rebalance.py:51
   launch(c, "rb_keys", 16.0 * L, [&] {
-    k_rb_keys<<<grid_for(c, L, 256), 256, 0, c.stream>>>(w.evict.get(), L, parts, w.opidx.get(),
+    k_rb_keys<<<grid_for(c, L, 256), 256, 0, c.stream>>>(w.evict.get(), L, parts, d_opidx,
                                                          w.rkey.get(), nb, w.keys.get());
   });
   const int gbits = ceil_log2((int64_t)nover * nb + 1);
@@ -1171,9 +1515,8 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
   }
   const unsigned long long* sk = w.keys_alt.get();
   if (!strong) {
-    // draws for vertices without a valid connection, in eviction order
-    int64_t need = L;
-    if (out && out->exact_rng) {
+    int64_t need = L;  // with direct commits every evicted vertex needs a draw
+    if (!direct) {
       DBuf<unsigned long long> mc(1, c.stream);
       dzero(c, mc.get(), 1);
       launch(c, "rb_count_missing", 12.0 * L, [&] {
@@ -1188,17 +1531,15 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
     for (int64_t i = 0; i < need; ++i) h_draws[i] = (int32_t)rng.bounded((uint64_t)nvalid);
     w.draws.ensure(need > 0 ? need : 1, c.stream);
     h2d(c, w.draws.get(), h_draws.data(), need);
+    c.sync();
     launch(c, "rb_weak_assign", 16.0 * L, [&] {
-      k_rb_weak_assign<<<1, 1024, 0, c.stream>>>(sk, L, w.rbest.get(), w.valid_list.get(),
-                                                 w.draws.get(), w.dest_sorted.get());
+      k_rb_weak_assign<<<1, 1024, 0, c.stream>>>(sk, L, w.rbest.get(), d_vlist, w.draws.get(),
+                                                 w.dest_sorted.get());
     });
   } else {
-    std::vector<long long> h_spare(nvalid);
-    for (int i = 0; i < nvalid; ++i) h_spare[i] = sigma - pw[h_valid_list[i]];
-    h2d(c, w.spare.get(), h_spare.data(), nvalid);
     launch(c, "rb_nextfit", 16.0 * L, [&] {
-      k_rb_nextfit<<<1, 1024, 0, c.stream>>>(sk, L, g.vw.get(), w.valid_list.get(), w.spare.get(),
-                                             nvalid, w.dest_sorted.get());
+      k_rb_nextfit<<<1, 1024, 0, c.stream>>>(sk, L, g.vw.get(), d_vlist, d_spare, nvalid,
+                                             w.dest_sorted.get());
     });
   }
   RbCommit rcm{};
@@ -1206,7 +1547,7 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
   rcm.dest_sorted = w.dest_sorted.get();
   rcm.mv = w.mv.get();
   rcm.offs = g.offs.get();
-  rcm.lists = w.lists.get() + w.cap_n;
+  rcm.lists = move_base;
   for (int t = 0; t < NBINS; ++t) rcm.seg_base[t] = w.seg_base[t];
   rcm.move_cnt = w.ctr.get() + CTR_MOVE;
   DBuf<int32_t> ov, od;

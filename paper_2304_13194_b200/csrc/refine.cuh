@@ -52,6 +52,8 @@ struct Workspace {
   DBuf<long long> deficit, required, spare, cum_before;
   int64_t seg_base[NBINS] = {};
   std::vector<int64_t> h_pw;  // host mirror of the part weights
+  std::vector<uint8_t> h_up;  // per-pass host scalars (packed)
+  DBuf<uint8_t> up;           // their device copy
 
   void ensure(Ctx& c, int64_t n, int k);
   void bind_level(const DGraph& g);
