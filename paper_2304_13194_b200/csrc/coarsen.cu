@@ -88,13 +88,16 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int q = 0; q < U; ++q) {
         const int st = s0 + q;
-        unsigned long long key = 0;
-        if (uu[q] >= 0 && fr[q] < 0)
-          key = ((unsigned long long)ww[q] << 32) | (unsigned)(0xffffffffu - (unsigned)uu[q]);
-        key = gmax<G>(key, gm);
+        // heaviest free neighbour, ties -> lowest id: two REDUX reductions
+        const bool ok = uu[q] >= 0 && fr[q] < 0;
+        const unsigned mw = __reduce_max_sync(gm, ok ? (unsigned)ww[q] : 0u);
+        const unsigned mu = __reduce_min_sync(gm, (ok && (unsigned)ww[q] == mw) ? (unsigned)uu[q]
+                                                                                : 0xffffffffu);
         const int src = ((lane - st * RPS) & (RPS - 1)) * G;
-        key = __shfl_sync(0xffffffffu, key, src);
-        if (lane / RPS == st) mine = key;
+        const unsigned dmw = __shfl_sync(0xffffffffu, mw, src);
+        const unsigned dmu = __shfl_sync(0xffffffffu, mu, src);
+        if (lane / RPS == st)
+          mine = dmw ? (((unsigned long long)dmw << 32) | (0xffffffffu - dmu)) : 0ull;
       }
     }
     int u = -1;
@@ -532,7 +535,97 @@ __device__ void resolve_b(const Resolve& R, int in, int out, int64_t t0, int64_t
   }
 }
 
+// Shared-memory tail: at most RES_TAIL live edges, their endpoints hashed to
+// local slots; the remaining rounds run on chip (one block).
+constexpr int RES_TAIL = 2048;
+constexpr int RES_HASH = 8192;  // >= 2 endpoints per edge, load <= 1/2
+struct ResTailSmem {
+  int32_t key[RES_HASH];
+  int32_t mn[RES_HASH];
+  uint8_t fr[RES_HASH];
+  int32_t ev[RES_TAIL], eu[RES_TAIL], evid[RES_TAIL], euid[RES_TAIL];
+  int16_t alive[2][RES_TAIL];
+  int nalive[2];
+};
+
+__device__ __forceinline__ int res_slot(ResTailSmem& S, int v) {
+  unsigned h = ((unsigned)v * 2654435761u) & (RES_HASH - 1);
+  while (true) {
+    const int prev = atomicCAS(&S.key[h], -1, v);
+    if (prev == -1 || prev == v) return (int)h;
+    h = (h + 1) & (RES_HASH - 1);
+  }
+}
+
+__device__ void resolve_tail(const Resolve& R, int in, ResTailSmem& S) {
+  const int L = (int)vload(R.cnt + in);
+  const int32_t* lin = R.lists + (size_t)in * R.n;
+  // the global minima written for these edges in the previous grid round
+  // were already reset by that round's successor; keep the global mn clean
+  for (int i = threadIdx.x; i < RES_HASH; i += blockDim.x) {
+    S.key[i] = -1;
+    S.mn[i] = INF32;
+  }
+  if (threadIdx.x == 0) S.nalive[0] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < L; i += blockDim.x) {
+    const int v = lin[i];
+    const int u = R.prop[v];
+    S.ev[i] = res_slot(S, v);
+    S.eu[i] = res_slot(S, u);
+    S.evid[i] = v;
+    S.euid[i] = u;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < RES_HASH; i += blockDim.x) {
+    const int v = S.key[i];
+    S.fr[i] = v >= 0 && R.partner[v] < 0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < L; i += blockDim.x) {
+    if (S.fr[S.ev[i]] && S.fr[S.eu[i]]) S.alive[0][atomicAdd(&S.nalive[0], 1)] = (int16_t)i;
+  }
+  __syncthreads();
+  int cur = 0;
+  while (S.nalive[cur] > 0) {
+    const int na = S.nalive[cur];
+    for (int q = threadIdx.x; q < na; q += blockDim.x) {
+      const int i = S.alive[cur][q];
+      atomicMin(&S.mn[S.ev[i]], S.evid[i]);
+      atomicMin(&S.mn[S.eu[i]], S.evid[i]);
+    }
+    if (threadIdx.x == 0) S.nalive[cur ^ 1] = 0;
+    __syncthreads();
+    for (int q = threadIdx.x; q < na; q += blockDim.x) {
+      const int i = S.alive[cur][q];
+      const int v = S.evid[i];
+      if (S.mn[S.ev[i]] == v && S.mn[S.eu[i]] == v) {
+        S.fr[S.ev[i]] = 0;
+        S.fr[S.eu[i]] = 0;
+        R.partner[v] = S.euid[i];
+        R.partner[S.euid[i]] = v;
+      }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < na; q += blockDim.x) {
+      const int i = S.alive[cur][q];
+      S.mn[S.ev[i]] = INF32;
+      S.mn[S.eu[i]] = INF32;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < na; q += blockDim.x) {
+      const int i = S.alive[cur][q];
+      if (S.fr[S.ev[i]] && S.fr[S.eu[i]])
+        S.alive[cur ^ 1][atomicAdd(&S.nalive[cur ^ 1], 1)] = (int16_t)i;
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+  if (threadIdx.x == 0) R.cnt[in] = 0;
+}
+
 __global__ void __launch_bounds__(1024) k_resolve(Resolve R) {
+  extern __shared__ unsigned char res_smem[];
   cg::grid_group grid = cg::this_grid();
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nt = (int64_t)gridDim.x * blockDim.x;
@@ -549,17 +642,22 @@ __global__ void __launch_bounds__(1024) k_resolve(Resolve R) {
     ++r;
   }
   if (blockIdx.x != 0) return;
-  while (true) {
-    const int in = (r - 1) & 1, out = r & 1;
-    const unsigned long long live = vload(R.cnt + in);
-    __syncthreads();
-    if (live == 0) return;
-    resolve_a(R, in, out, threadIdx.x, blockDim.x);
-    __syncthreads();
-    resolve_b(R, in, out, threadIdx.x, blockDim.x);
-    __syncthreads();
-    ++r;
+  // live edges of list `in` were last scattered into mn[in]; that buffer was
+  // reset by resolve_a of this round only if the round ran, so clear the
+  // entries of the list now (they would otherwise leak into a later call)
+  const int in = (r - 1) & 1;
+  {
+    const int L = (int)vload(R.cnt + in);
+    const int32_t* lin = R.lists + (size_t)in * R.n;
+    int32_t* mprev = R.mn + (size_t)in * R.n;
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+      const int v = lin[i];
+      mprev[v] = INF32;
+      mprev[R.prop[v]] = INF32;
+    }
   }
+  __syncthreads();
+  resolve_tail(R, in, *reinterpret_cast<ResTailSmem*>(res_smem));
 }
 
 void device_match(Ctx& c, const DGraph& g, int32_t* partner) {
@@ -597,12 +695,22 @@ void device_match(Ctx& c, const DGraph& g, int32_t* partner) {
       c.sync();
       if (ne == 0) break;
       // all resolution rounds in one cooperative launch (k_resolve)
-      Resolve R{prop.get(), partner, lists.get(), cnt.get(), mn.get(), n, 4096ull};
-      const int blocks = std::min<int64_t>(coop_blocks(c, (const void*)k_resolve, 1024),
-                                           std::max<int64_t>(1, ((int64_t)ne + 1023) / 1024));
+      Resolve R{prop.get(), partner, lists.get(), cnt.get(), mn.get(), n,
+                (unsigned long long)RES_TAIL};
+      const size_t smem = sizeof(ResTailSmem);
+      static int res_grid = 0;
+      if (!res_grid) {
+        CK(cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resolve, 1024, smem));
+        JET_REQUIRE(per_sm >= 1, JET_EINTERNAL, "k_resolve does not fit on an SM");
+        res_grid = per_sm * c.num_sms;
+      }
+      // fewer, fuller blocks make each grid-wide barrier cheaper
+      const int blocks = std::min<int64_t>(res_grid, std::max<int64_t>(8, ((int64_t)ne + 16383) / 16384));
       void* args[] = {&R};
       launch(c, "match_resolve", 0.0, [&] {
-        CK(cudaLaunchCooperativeKernel((const void*)k_resolve, dim3(blocks), dim3(1024), args, 0,
+        CK(cudaLaunchCooperativeKernel((const void*)k_resolve, dim3(blocks), dim3(1024), args, smem,
                                        c.stream));
       });
     }

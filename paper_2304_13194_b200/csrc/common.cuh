@@ -55,9 +55,21 @@ constexpr int KMASK = (1 << KBITS) - 1;
 constexpr int NBINS = 6;
 constexpr int BIN_WARP = 4, BIN_BLOCK = 5;
 constexpr int64_t WARP_TIER_MAX_DEG = 2048;
-__host__ __device__ inline int tier_of_degree(int64_t d) {
-  return d <= 4 ? 0 : d <= 8 ? 1 : d <= 16 ? 2 : d <= 32 ? 3
-       : d <= WARP_TIER_MAX_DEG ? 4 : 5;
+// Per-level degree -> tier map. Small levels merge every row of <= 32
+// entries into tier 3 (one launch instead of four; launch latency dominates
+// there); large levels use the G = 4/8/16/32 split.
+struct TierMap {
+  int lim[4];
+  __host__ __device__ __forceinline__ int operator()(int64_t d) const {
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (d <= lim[t]) return t;
+    return d <= WARP_TIER_MAX_DEG ? 4 : 5;
+  }
+};
+constexpr int64_t MERGED_TIER_MAX_N = 1 << 18;
+inline TierMap tiers_for(int64_t n) {
+  return n <= MERGED_TIER_MAX_N ? TierMap{{-1, -1, -1, 32}} : TierMap{{4, 8, 16, 32}};
 }
 constexpr int TIER_G[4] = {4, 8, 16, 32};
 
@@ -116,8 +128,9 @@ struct DBuf {
 // Device CSR level.
 struct DGraph {
   int64_t n = 0, nnz = 0, total_vw = 0;
-  int64_t max_deg = 0, max_wdeg = 0, max_ew = 0, max_vw = 0;
+  int64_t max_deg = 0, max_wdeg = 0, max_ew = 0, max_vw = 0, min_vw = 1;
   bool unit_ew = true;
+  TierMap tm{{4, 8, 16, 32}};
   DBuf<int64_t> offs;
   DBuf<int32_t> adj, ew, vw;
   // degree tiers: ascending vertex lists, or identity when one tier holds all
@@ -163,6 +176,8 @@ struct Ctx {
   std::vector<ProfAgg> agg;
   std::map<std::string, int> cls_index;
   std::string prof_only;  // empty: record every class
+  std::string prof_tag;   // prefix for class names (per-level breakdowns)
+  bool prof_by_level = false;
   cudaEvent_t timer_a = nullptr, timer_b = nullptr;
   DBuf<uint8_t> flush_buf;
   int32_t lock_epoch = 0;
@@ -186,7 +201,7 @@ inline void launch(Ctx& c, const char* name, double bytes, F&& f) {
   ProfRec r{};
   const bool rec = c.prof && (c.prof_only.empty() || c.prof_only == name);
   if (rec) {
-    r.cls = c.prof_class(name);
+    r.cls = c.prof_by_level ? c.prof_class((c.prof_tag + name).c_str()) : c.prof_class(name);
     r.a = c.take_event();
     r.b = c.take_event();
     r.bytes = bytes;

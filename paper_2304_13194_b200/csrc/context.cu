@@ -154,7 +154,10 @@ int jet_profile_enable(jet_ctx* ctx, int on) {
 
 int jet_profile_filter(jet_ctx* ctx, const char* name) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
-  c->prof_only = name ? name : "";
+  std::string s = name ? name : "";
+  // "@levels" switches on per-level class names instead of filtering
+  c->prof_by_level = s == "@levels";
+  c->prof_only = c->prof_by_level ? "" : s;
   return JET_OK;
 }
 

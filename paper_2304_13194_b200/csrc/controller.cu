@@ -170,7 +170,9 @@ void run_partition(Ctx& c, const DGraph& g0, const jet_config& cfg, int32_t* par
   }
   const int64_t target = std::max<int64_t>(std::max<int64_t>(cfg.coarse_target, 2LL * k), 32);
   Hierarchy h;
+  c.prof_tag = "coarsen:";
   device_build_hierarchy(c, g0, target, h);
+  c.prof_tag.clear();
   c.sync();
   const double t1 = now_s();
   S.t_coarsen = t1 - t0;
@@ -212,7 +214,9 @@ void run_partition(Ctx& c, const DGraph& g0, const jet_config& cfg, int32_t* par
     L.cut_in = cut;
     L.balanced_in = *std::max_element(w.h_pw.begin(), w.h_pw.end()) <= cfg.limit;
     const double tl = now_s();
+    c.prof_tag = "L" + std::to_string(level) + ":";
     refine_level(c, w, g, cur, cut, cfg, level == 0, level, L, keep);
+    c.prof_tag.clear();
     c.sync();
     L.seconds = now_s() - tl;
     L.cut_out = cut;

@@ -41,29 +41,30 @@ __global__ void k_check_offsets(const int64_t* __restrict__ offs, int64_t n,
 // Per-level statistics: total/max vertex weight, max degree, max edge weight
 // and the tier histogram (vertex counts and entry counts per tier).
 struct LevelStats {
-  unsigned long long total_vw, max_vw, max_deg, max_ew;
+  unsigned long long total_vw, max_vw, max_deg, max_ew, min_vw;
   unsigned long long bin_cnt[NBINS], bin_nnz[NBINS];
 };
 
 __global__ void k_level_stats(const int64_t* __restrict__ offs,
                               const int32_t* __restrict__ vw,
                               const int32_t* __restrict__ ew, int64_t n,
-                              int64_t nnz, LevelStats* st) {
+                              int64_t nnz, TierMap tm, LevelStats* st) {
   __shared__ unsigned long long s_cnt[NBINS], s_nnz[NBINS];
   if (threadIdx.x < NBINS) {
     s_cnt[threadIdx.x] = 0;
     s_nnz[threadIdx.x] = 0;
   }
   __syncthreads();
-  unsigned long long tv = 0, mv = 0, md = 0, me = 0;
+  unsigned long long tv = 0, mv = 0, md = 0, me = 0, mn = ~0ull;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride) {
     int64_t d = offs[v + 1] - offs[v];
     unsigned long long w = (unsigned long long)vw[v];
     tv += w;
     mv = w > mv ? w : mv;
+    mn = w < mn ? w : mn;
     md = (unsigned long long)d > md ? (unsigned long long)d : md;
-    int t = tier_of_degree(d);
+    int t = tm(d);
     atomicAdd(&s_cnt[t], 1ull);
     atomicAdd(&s_nnz[t], (unsigned long long)d);
   }
@@ -75,7 +76,9 @@ __global__ void k_level_stats(const int64_t* __restrict__ offs,
   mv = gmax<32>(mv, 0xffffffffu);
   md = gmax<32>(md, 0xffffffffu);
   me = gmax<32>(me, 0xffffffffu);
+  mn = gmin<32>(mn, 0xffffffffu);
   if ((threadIdx.x & 31) == 0) {
+    atomicMin(&st->min_vw, mn);
     atomicAdd(&st->total_vw, tv);
     atomicMax(&st->max_vw, mv);
     atomicMax(&st->max_deg, md);
@@ -91,18 +94,21 @@ __global__ void k_level_stats(const int64_t* __restrict__ offs,
 struct TierIs {
   const int64_t* offs;
   int t;
+  TierMap tm;
   __device__ __forceinline__ bool operator()(const int32_t& v) const {
-    return tier_of_degree(offs[v + 1] - offs[v]) == t;
+    return tm(offs[v + 1] - offs[v]) == t;
   }
 };
 
 void finalize_graph(Ctx& c, DGraph& g) {
+  g.tm = tiers_for(g.n);
   DBuf<LevelStats> st(1, c.stream);
   dzero(c, st.get(), 1);
+  CK(cudaMemsetAsync(&st.get()->min_vw, 0xff, sizeof(unsigned long long), c.stream));
   if (g.n > 0) {
     launch(c, "level_stats", 8.0 * g.n + 4.0 * g.n + 4.0 * g.nnz, [&] {
       k_level_stats<<<grid_for(c, g.n > g.nnz ? g.n : g.nnz, 256), 256, 0, c.stream>>>(
-          g.offs.get(), g.vw.get(), g.ew.get(), g.n, g.nnz, st.get());
+          g.offs.get(), g.vw.get(), g.ew.get(), g.n, g.nnz, g.tm, st.get());
     });
   }
   LevelStats h;
@@ -110,6 +116,7 @@ void finalize_graph(Ctx& c, DGraph& g) {
   c.sync();
   g.total_vw = (int64_t)h.total_vw;
   g.max_vw = (int64_t)h.max_vw;
+  g.min_vw = g.n > 0 ? (int64_t)h.min_vw : 1;
   g.max_deg = (int64_t)h.max_deg;
   g.max_ew = (int64_t)h.max_ew;
   g.unit_ew = g.nnz == 0 || h.max_ew <= 1;
@@ -136,7 +143,7 @@ void finalize_graph(Ctx& c, DGraph& g) {
     if (!g.bin_cnt[t]) continue;
     int32_t* out = g.bin_store.get() + base;
     cub::CountingInputIterator<int32_t> it(0);
-    TierIs op{g.offs.get(), t};
+    TierIs op{g.offs.get(), t, g.tm};
     size_t tmp = 0;
     CK(cub::DeviceSelect::If(nullptr, tmp, it, out, nsel.get(), (int)g.n, op, c.stream));
     void* p = c.cub_scratch(tmp);

@@ -218,23 +218,45 @@ __global__ void __launch_bounds__(256)
         const int rown = __shfl_sync(0xffffffffu, own, st * RPS + grp);
         const int p = pp[q];
         const unsigned peers = __match_any_sync(gm, p);
-        const long long sm = UNIT ? (long long)__popc(peers) : peer_sum(peers, ww[q], wide);
-        const bool lead = p >= 0 && (__ffs(peers) - 1) == lane;
-        long long sc = (lead && p == rown) ? sm : 0;
-        unsigned long long key =
-            (lead && p != rown && Op::competes(a, p, rown)) ? pack_best(sm, p) : 0ull;
-        long long ex = p >= 0 ? Op::extra(a, p, ww[q]) : 0;
-        sc = gsum<G>(sc, gm);
-        key = gmax<G>(key, gm);
-        ex = gsum<G>(ex, gm);
+        const bool comp = p >= 0 && p != rown && Op::competes(a, p, rown);
         const int src = ((lane - st * RPS) & (RPS - 1)) * G;
-        sc = __shfl_sync(0xffffffffu, sc, src);
-        key = __shfl_sync(0xffffffffu, key, src);
-        ex = __shfl_sync(0xffffffffu, ex, src);
-        if (lane / RPS == st) {
-          my_self = sc;
-          my_key = key;
-          my_ex = ex;
+        if (!wide) {
+          // 32-bit sums (weighted degree < 2^31): single-instruction REDUX
+          // reductions; best part = max conn, then lowest part id
+          const unsigned sm =
+              UNIT ? (unsigned)__popc(peers) : __reduce_add_sync(peers, (unsigned)ww[q]);
+          const unsigned sc =
+              UNIT ? (unsigned)__popc(__ballot_sync(gm, p >= 0 && p == rown))
+                   : __reduce_add_sync(gm, (p >= 0 && p == rown) ? (unsigned)ww[q] : 0u);
+          const unsigned mx = __reduce_max_sync(gm, comp ? sm : 0u);
+          const unsigned pm = __reduce_min_sync(gm, (comp && sm == mx) ? (unsigned)p : 0xffffffffu);
+          const unsigned ex = __reduce_add_sync(gm, p >= 0 ? (unsigned)Op::extra(a, p, ww[q]) : 0u);
+          const unsigned dsc = __shfl_sync(0xffffffffu, sc, src);
+          const unsigned dmx = __shfl_sync(0xffffffffu, mx, src);
+          const unsigned dpm = __shfl_sync(0xffffffffu, pm, src);
+          const unsigned dex = __shfl_sync(0xffffffffu, ex, src);
+          if (lane / RPS == st) {
+            my_self = dsc;
+            my_key = dmx ? pack_best((long long)dmx, (int)dpm) : 0ull;
+            my_ex = dex;
+          }
+        } else {
+          const long long sm = UNIT ? (long long)__popc(peers) : peer_sum(peers, ww[q], wide);
+          const bool lead = p >= 0 && (__ffs(peers) - 1) == lane;
+          long long sc = (lead && p == rown) ? sm : 0;
+          unsigned long long key = (lead && comp) ? pack_best(sm, p) : 0ull;
+          long long ex = p >= 0 ? Op::extra(a, p, ww[q]) : 0;
+          sc = gsum<G>(sc, gm);
+          key = gmax<G>(key, gm);
+          ex = gsum<G>(ex, gm);
+          sc = __shfl_sync(0xffffffffu, sc, src);
+          key = __shfl_sync(0xffffffffu, key, src);
+          ex = __shfl_sync(0xffffffffu, ex, src);
+          if (lane / RPS == st) {
+            my_self = sc;
+            my_key = key;
+            my_ex = ex;
+          }
         }
       }
     }
@@ -243,16 +265,22 @@ __global__ void __launch_bounds__(256)
   Op::block_done(a, acc);
 }
 
-// Tier 4: one warp per row with a per-warp part table in shared memory.
-// Shared layout per warp: tab[k] (u64), tl[tl_cap] (i32), tcnt (i32).
+// Tier 4 (33..2048 entries). A warp owns 32 rows; per-vertex data is loaded
+// once, coalesced. Rows are aggregated one after another into a per-warp
+// shared-memory part table, but the adjacency of the next chunk batch (of
+// this row, or of the next row) is loaded while the current batch's
+// neighbour parts are gathered and aggregated, so two batches of loads are
+// always in flight. Shared layout per warp: tab[k] (u64), tl[tl_cap] (i32),
+// tcnt (i32).
 template <class Op, bool UNIT>
 __global__ void __launch_bounds__(256)
     k_agg_warp(typename Op::Args a, GView g, const int32_t* __restrict__ parts,
                const int32_t* __restrict__ list, int64_t cnt, bool wide, int k,
                int tl_cap, const unsigned long long* __restrict__ dcnt) {
   if (dcnt) cnt = (int64_t)*dcnt;
+  constexpr int U = 2;  // chunks of 32 entries per batch
   extern __shared__ unsigned long long smem[];
-  const int wib = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t per = (size_t)k + (size_t)(tl_cap + 3) / 2;
   unsigned long long* tab = smem + wib * per;
   int* tl = reinterpret_cast<int*>(tab + k);
@@ -260,50 +288,126 @@ __global__ void __launch_bounds__(256)
   for (int i = lane; i < k; i += 32) tab[i] = 0;
   if (lane == 0) *tcnt = 0;
   __syncwarp();
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   long long acc = 0;
-  for (int64_t i = blockIdx.x * (int64_t)nw + wib; i < cnt; i += (int64_t)gridDim.x * nw) {
-    const int v = list ? list[i] : (int)i;
-    const int own = parts[v];
-    if (Op::skip(a, v, own)) continue;
-    const int64_t b = g.offs[v], e = g.offs[v + 1];
+  for (int64_t base = w0 * 32; base < cnt; base += nw * 32) {
+    const int64_t idx = base + lane;
+    int v = 0, own = -1, deg = 0;
+    int64_t beg = 0;
+    if (idx < cnt) {
+      v = list ? list[idx] : (int)idx;
+      own = parts[v];
+      if (Op::skip(a, v, own)) {
+        own = -1;
+      } else {
+        beg = g.offs[v];
+        deg = (int)(g.offs[v + 1] - beg);
+      }
+    }
+    long long my_self = 0, my_ex = 0;
+    unsigned long long my_key = 0;
+    // pipeline state: (row, first chunk) of the batch whose adjacency is loaded
+    int r = 0, c0 = 0;
+    int64_t rb = __shfl_sync(0xffffffffu, beg, 0);
+    int rd = __shfl_sync(0xffffffffu, deg, 0);
+    int uu[U], ww[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int j = (c0 + q) * 32 + lane;
+      uu[q] = j < rd ? g.adj[rb + j] : -1;
+      ww[q] = (j < rd) ? (UNIT ? 1 : g.ew[rb + j]) : 0;
+    }
     long long ex = 0;
-    for (int64_t j = b; j < e; j += 32) {
-      int p = -1, w = 0;
-      if (j + lane < e) {
-        p = parts[g.adj[j + lane]];
-        w = UNIT ? 1 : g.ew[j + lane];
-        ex += Op::extra(a, p, w);
+    while (r < 32) {
+      int pp[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) pp[q] = uu[q] >= 0 ? parts[uu[q]] : -1;
+      // next batch: same row if it has more chunks, else the next row
+      const int cur_r = r, cur_d = rd;
+      int wv[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) wv[q] = ww[q];
+      if ((c0 + U) * 32 < rd) {
+        c0 += U;
+      } else {
+        ++r;
+        c0 = 0;
+        rb = r < 32 ? __shfl_sync(0xffffffffu, beg, r & 31) : 0;
+        rd = r < 32 ? __shfl_sync(0xffffffffu, deg, r & 31) : 0;
       }
-      const unsigned peers = __match_any_sync(0xffffffffu, p);
-      const long long s = UNIT ? (long long)__popc(peers) : peer_sum(peers, w, wide);
-      if (p >= 0 && (__ffs(peers) - 1) == lane) {
-        unsigned long long old = atomicAdd(&tab[p], (unsigned long long)s);
-        if (old == 0) tl[atomicAdd(tcnt, 1)] = p;
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int j = (c0 + q) * 32 + lane;
+        uu[q] = (r < 32 && j < rd) ? g.adj[rb + j] : -1;
+        ww[q] = (r < 32 && j < rd) ? (UNIT ? 1 : g.ew[rb + j]) : 0;
+      }
+      // aggregate the current batch
+      const int rown = __shfl_sync(0xffffffffu, own, cur_r);
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int p = pp[q];
+        if (p >= 0) ex += Op::extra(a, p, wv[q]);
+        const unsigned peers = __match_any_sync(0xffffffffu, p);
+        const long long sm = UNIT ? (long long)__popc(peers) : peer_sum(peers, wv[q], wide);
+        if (p >= 0 && (__ffs(peers) - 1) == lane) {
+          const unsigned long long old = atomicAdd(&tab[p], (unsigned long long)sm);
+          if (old == 0) tl[atomicAdd(tcnt, 1)] = p;
+        }
+      }
+      if (r != cur_r) {  // row cur_r complete: reduce its table
+        __syncwarp();
+        const int nt = *tcnt;
+        long long sc = 0;
+        unsigned long long key = 0;
+        long long ext;
+        if (!wide) {
+          // 32-bit sums: REDUX reductions (max conn, then lowest part)
+          unsigned usc = 0, bm = 0, bp = 0xffffffffu;
+          for (int t = lane; t < nt; t += 32) {
+            const int p = tl[t];
+            const unsigned cv = (unsigned)tab[p];
+            tab[p] = 0;
+            if (p == rown) usc = cv;
+            else if (Op::competes(a, p, rown) && (cv > bm || (cv == bm && (unsigned)p < bp))) {
+              bm = cv;
+              bp = (unsigned)p;
+            }
+          }
+          usc = __reduce_add_sync(0xffffffffu, usc);
+          const unsigned mx = __reduce_max_sync(0xffffffffu, bm);
+          const unsigned pm = __reduce_min_sync(0xffffffffu, bm == mx ? bp : 0xffffffffu);
+          sc = usc;
+          key = mx ? pack_best((long long)mx, (int)pm) : 0ull;
+          ext = __reduce_add_sync(0xffffffffu, (unsigned)ex);
+        } else {
+          for (int t = lane; t < nt; t += 32) {
+            const int p = tl[t];
+            const long long cv = (long long)tab[p];
+            tab[p] = 0;
+            if (p == rown) sc = cv;
+            else if (Op::competes(a, p, rown)) {
+              const unsigned long long kk = pack_best(cv, p);
+              key = kk > key ? kk : key;
+            }
+          }
+          sc = gsum<32>(sc, 0xffffffffu);
+          key = gmax<32>(key, 0xffffffffu);
+          ext = gsum<32>(ex, 0xffffffffu);
+        }
+        ex = 0;
+        if (lane == cur_r) {
+          my_self = sc;
+          my_key = key;
+          my_ex = ext;
+        }
+        __syncwarp();
+        if (lane == 0) *tcnt = 0;
+        __syncwarp();
+        (void)cur_d;
       }
     }
-    __syncwarp();
-    const int nt = *tcnt;
-    long long self_c = 0;
-    unsigned long long key = 0;
-    for (int t = lane; t < nt; t += 32) {
-      const int p = tl[t];
-      const long long cv = (long long)tab[p];
-      tab[p] = 0;
-      if (p == own) self_c = cv;
-      else if (Op::competes(a, p, own)) {
-        unsigned long long kk = pack_best(cv, p);
-        key = kk > key ? kk : key;
-      }
-    }
-    self_c = gsum<32>(self_c, 0xffffffffu);
-    key = gmax<32>(key, 0xffffffffu);
-    ex = gsum<32>(ex, 0xffffffffu);
-    __syncwarp();
-    if (lane == 0) {
-      *tcnt = 0;
-      Op::finish(a, v, own, self_c, key, ex, acc);
-    }
-    __syncwarp();
+    if (own >= 0) Op::finish(a, v, own, my_self, my_key, my_ex, acc);
   }
   Op::block_done(a, acc);
 }
@@ -404,7 +508,8 @@ static void run_agg(Ctx& c, const DGraph& g, MakeArgs mk, const int32_t* parts,
                     int k, const char* name, double bytes_per_vertex,
                     int32_t* const* dlists = nullptr,
                     const unsigned long long* dcnts = nullptr) {
-  const bool wide = g.max_ew >= (1LL << 26);
+  // 32-bit conn sums are exact when every weighted degree is < 2^31
+  const bool wide = g.max_wdeg >= (1LL << 31);
   const GView gv = view(g);
   const double bpe = g.unit_ew ? 8.0 : 12.0;  // adj + gathered part (+ weight)
   for (int t = 0; t < NBINS; ++t) {
@@ -443,7 +548,7 @@ static void run_agg(Ctx& c, const DGraph& g, MakeArgs mk, const int32_t* parts,
       const int nw = warp_tier_warps(c, k, tl_cap, &smem);
       auto kern = g.unit_ew ? k_agg_warp<Op, true> : k_agg_warp<Op, false>;
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      const unsigned grid = grid_for(c, cnt * 32, nw * 32, 2048 / (nw * 32));
+      const unsigned grid = grid_for(c, cnt, nw * 32, 2048 / (nw * 32));
       launch(c, name, bytes, [&] {
         kern<<<grid, nw * 32, smem, c.stream>>>(a, gv, parts, list, cnt, wide, k, tl_cap, dc);
       });
@@ -720,7 +825,7 @@ void lp_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts, int k,
 // F must already hold dests/gains of candidates (-1 elsewhere); this builds
 // the per-tier candidate lists.
 __global__ void k_distribute(const int32_t* __restrict__ cand, int64_t ncand,
-                             const int64_t* __restrict__ offs, int32_t* lists,
+                             const int64_t* __restrict__ offs, TierMap tm, int32_t* lists,
                              RbSegsDev segs, unsigned long long* cnts) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t lim = (ncand + blockDim.x - 1) / blockDim.x * blockDim.x;
@@ -728,7 +833,7 @@ __global__ void k_distribute(const int32_t* __restrict__ cand, int64_t ncand,
     int v = 0, t = -1;
     if (i < ncand) {
       v = cand[i];
-      t = tier_of_degree(offs[v + 1] - offs[v]);
+      t = tm(offs[v + 1] - offs[v]);
     }
     for (int tt = 0; tt < NBINS; ++tt)
       warp_append(t == tt, v, lists + segs.b[tt], cnts + tt);
@@ -743,7 +848,7 @@ void afterburner_only(Ctx& c, Workspace& w, const DGraph& g, const int32_t* part
   if (ncand > 0) {
     launch(c, "distribute", 8.0 * ncand, [&] {
       k_distribute<<<grid_for(c, ncand, 256), 256, 0, c.stream>>>(
-          cand, ncand, g.offs.get(), w.lists.get(), segs, w.ctr.get() + CTR_CAND);
+          cand, ncand, g.offs.get(), g.tm, w.lists.get(), segs, w.ctr.get() + CTR_CAND);
     });
   }
   AbArgs ab{};
@@ -797,14 +902,14 @@ ApplyResult apply_moves(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts,
 // ===========================================================================
 
 // First bucket whose cumulative eligible weight reaches the deficit.
-__global__ void k_rb_scan(const unsigned long long* __restrict__ H, int nb,
-                          const long long* __restrict__ deficit, int32_t* bstar,
-                          long long* cum_before) {
-  typedef cub::BlockScan<long long, 256> BS;
-  __shared__ typename BS::TempStorage ts;
+template <int BS>
+__device__ void rb_scan_op(int op, const unsigned long long* __restrict__ H, int nb,
+                           const long long* __restrict__ deficit, int32_t* bstar,
+                           long long* cum_before) {
+  typedef cub::BlockScan<long long, BS> Scan;
+  __shared__ typename Scan::TempStorage ts;
   __shared__ int s_found;
   __shared__ long long s_run, s_cb;
-  const int op = blockIdx.x;
   const unsigned long long* h = H + (size_t)op * nb;
   const long long D = deficit[op];
   if (threadIdx.x == 0) {
@@ -813,11 +918,11 @@ __global__ void k_rb_scan(const unsigned long long* __restrict__ H, int nb,
     s_cb = 0;
   }
   __syncthreads();
-  for (int base = 0; base < nb; base += 256) {
+  for (int base = 0; base < nb; base += BS) {
     const int i = base + threadIdx.x;
     const long long x = i < nb ? (long long)h[i] : 0;
     long long incl, total;
-    BS(ts).InclusiveSum(x, incl, total);
+    Scan(ts).InclusiveSum(x, incl, total);
     const long long run = s_run;
     const long long cum = run + incl;
     if (i < nb && cum >= D && cum - x < D) {
@@ -833,6 +938,14 @@ __global__ void k_rb_scan(const unsigned long long* __restrict__ H, int nb,
     bstar[op] = s_found;
     cum_before[op] = s_found < nb ? s_cb : s_run;
   }
+  __syncthreads();
+}
+
+// First bucket whose cumulative eligible weight reaches the deficit.
+__global__ void k_rb_scan(const unsigned long long* __restrict__ H, int nb,
+                          const long long* __restrict__ deficit, int32_t* bstar,
+                          long long* cum_before) {
+  rb_scan_op<256>(blockIdx.x, H, nb, deficit, bstar, cum_before);
 }
 
 struct RbSel {
@@ -847,11 +960,10 @@ struct RbSel {
   unsigned long long* CH;
 };
 
-__global__ void k_rb_chunk(RbSel s, const int32_t* __restrict__ rcand,
-                           const unsigned long long* __restrict__ cnt_ptr) {
-  const int64_t cnt = (int64_t)*cnt_ptr;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += stride) {
+__device__ void rb_chunk(const RbSel& s, const int32_t* __restrict__ rcand,
+                         const unsigned long long* __restrict__ cnt_ptr, int64_t t0, int64_t nt) {
+  const int64_t cnt = (int64_t)*(const volatile unsigned long long*)cnt_ptr;
+  for (int64_t i = t0; i < cnt; i += nt) {
     const int v = rcand[i];
     const int op = s.opidx[s.parts[v]];
     if (s.rkey[v] != s.bstar[op]) continue;
@@ -860,21 +972,26 @@ __global__ void k_rb_chunk(RbSel s, const int32_t* __restrict__ rcand,
   }
 }
 
+__global__ void k_rb_chunk(RbSel s, const int32_t* __restrict__ rcand,
+                           const unsigned long long* __restrict__ cnt_ptr) {
+  rb_chunk(s, rcand, cnt_ptr, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
+           (int64_t)gridDim.x * blockDim.x);
+}
+
 // Locate the crossing element of select_prefix (rebalance.py:74-85) inside
 // the crossing bucket, then decide whether it is taken:
 //   take it iff cum[first] - D <= D - cum[first-1]  or  cum[first-1] < required
 // (the min_weight extension of :81-85 always lands on first+1 because
 //  deficit >= required). thr = first id NOT selected inside the bucket.
-__global__ void k_rb_find(RbSel s, const long long* __restrict__ deficit,
-                          const long long* __restrict__ required,
-                          const long long* __restrict__ cum_before,
-                          const int32_t* __restrict__ opart, int64_t n, int nb,
-                          int32_t* thr) {
-  typedef cub::BlockScan<long long, 256> BS;
+template <int BSZ>
+__device__ void rb_find_op(int op, const RbSel& s, const long long* __restrict__ deficit,
+                           const long long* __restrict__ required,
+                           const long long* __restrict__ cum_before,
+                           const int32_t* __restrict__ opart, int64_t n, int nb, int32_t* thr) {
+  typedef cub::BlockScan<long long, BSZ> BS;
   __shared__ typename BS::TempStorage ts;
   __shared__ int s_ch;
   __shared__ long long s_run, s_cb;
-  const int op = blockIdx.x;
   const int bs = s.bstar[op];
   if (bs >= nb) {  // shortfall: every eligible candidate leaves
     if (threadIdx.x == 0) thr[op] = 0x7fffffff;
@@ -889,7 +1006,7 @@ __global__ void k_rb_find(RbSel s, const long long* __restrict__ deficit,
     s_cb = 0;
   }
   __syncthreads();
-  for (int b0 = 0; b0 < s.nch; b0 += 256) {
+  for (int b0 = 0; b0 < s.nch; b0 += BSZ) {
     const int i = b0 + threadIdx.x;
     const long long x = i < s.nch ? (long long)ch[i] : 0;
     long long incl, total;
@@ -935,20 +1052,26 @@ __global__ void k_rb_find(RbSel s, const long long* __restrict__ deficit,
   }
 }
 
+__global__ void k_rb_find(RbSel s, const long long* __restrict__ deficit,
+                          const long long* __restrict__ required,
+                          const long long* __restrict__ cum_before,
+                          const int32_t* __restrict__ opart, int64_t n, int nb, int32_t* thr) {
+  rb_find_op<256>(blockIdx.x, s, deficit, required, cum_before, opart, n, nb, thr);
+}
+
 // Selected iff (bucket, id) < the part's threshold (select_prefix). Weak
 // passes with direct=1 commit vertices that have a valid destination right
 // away (their order is unobservable); everything else (weak: vertices that
 // need a random destination; strong: all) goes to the evict list.
-__global__ void k_rb_select(RbSel s, const int32_t* __restrict__ rcand,
-                            const unsigned long long* __restrict__ cnt_ptr,
-                            const int32_t* __restrict__ rbest, int strong, int direct,
-                            int32_t* evict, unsigned long long* evict_cnt, int32_t* mv,
-                            const int64_t* __restrict__ offs, int32_t* move_lists,
-                            RbSegsDev mseg, unsigned long long* move_cnt) {
-  const int64_t cnt = (int64_t)*cnt_ptr;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t lim = (cnt + blockDim.x - 1) / blockDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < lim; i += stride) {
+__device__ void rb_select(const RbSel& s, const int32_t* __restrict__ rcand,
+                          const unsigned long long* __restrict__ cnt_ptr,
+                          const int32_t* __restrict__ rbest, int strong, int direct,
+                          int32_t* evict, unsigned long long* evict_cnt, int32_t* mv,
+                          const int64_t* __restrict__ offs, TierMap tm, int32_t* move_lists,
+                          RbSegsDev mseg, unsigned long long* move_cnt, int64_t t0, int64_t nt) {
+  const int64_t cnt = (int64_t)*(const volatile unsigned long long*)cnt_ptr;
+  const int64_t lim = (cnt + 31) / 32 * 32;
+  for (int64_t i = t0; i < lim; i += nt) {
     bool sel = false, now = false;
     int v = 0, t = -1;
     if (i < cnt) {
@@ -962,7 +1085,7 @@ __global__ void k_rb_select(RbSel s, const int32_t* __restrict__ rcand,
         if (bp >= 0) {
           now = true;
           mv[v] = bp;
-          t = tier_of_degree(offs[v + 1] - offs[v]);
+          t = tm(offs[v + 1] - offs[v]);
         }
       }
     }
@@ -972,15 +1095,26 @@ __global__ void k_rb_select(RbSel s, const int32_t* __restrict__ rcand,
   }
 }
 
+__global__ void k_rb_select(RbSel s, const int32_t* __restrict__ rcand,
+                            const unsigned long long* __restrict__ cnt_ptr,
+                            const int32_t* __restrict__ rbest, int strong, int direct,
+                            int32_t* evict, unsigned long long* evict_cnt, int32_t* mv,
+                            const int64_t* __restrict__ offs, TierMap tm, int32_t* move_lists,
+                            RbSegsDev mseg, unsigned long long* move_cnt) {
+  rb_select(s, rcand, cnt_ptr, rbest, strong, direct, evict, evict_cnt, mv, offs, tm, move_lists,
+            mseg, move_cnt, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
+            (int64_t)gridDim.x * blockDim.x);
+}
+
 // Collect the vertices of oversized parts into per-tier candidate lists.
 __global__ void k_rb_collect(const int32_t* __restrict__ parts, const int32_t* __restrict__ opidx,
-                             const int64_t* __restrict__ offs, int64_t n, int32_t* lists,
-                             RbSegsDev seg, unsigned long long* cnts) {
+                             const int64_t* __restrict__ offs, TierMap tm, int64_t n,
+                             int32_t* lists, RbSegsDev seg, unsigned long long* cnts) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t lim = (n + blockDim.x - 1) / blockDim.x * blockDim.x;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < lim; v += stride) {
     int t = -1;
-    if (v < n && opidx[parts[v]] >= 0) t = tier_of_degree(offs[v + 1] - offs[v]);
+    if (v < n && opidx[parts[v]] >= 0) t = tm(offs[v + 1] - offs[v]);
     if (__ballot_sync(0xffffffffu, t >= 0) == 0) continue;
     for (int tt = 0; tt < NBINS; ++tt) warp_append(t == tt, (int32_t)v, lists + seg.b[tt], cnts + tt);
   }
@@ -998,6 +1132,7 @@ struct RbTail {
   const int32_t* rkey;
   const int32_t* vw;
   const int64_t* offs;
+  TierMap tm;
   const int32_t* valid_list;
   const int32_t* draws;
   const long long* spare;
@@ -1010,13 +1145,12 @@ struct RbTail {
   unsigned long long* move_cnt;
 };
 
-__global__ void __launch_bounds__(1024) k_rb_tail(RbTail a) {
-  extern __shared__ unsigned long long sk[];
+__device__ void rb_tail(const RbTail& a, unsigned long long* sk) {
   __shared__ long long s_room;
   __shared__ int s_di, s_done;
   __shared__ long long s_wsum[32];
   const int tid = threadIdx.x;
-  const int L = (int)*a.evict_cnt;
+  const int L = (int)*(const volatile unsigned long long*)a.evict_cnt;
   int P2 = 1;
   while (P2 < L) P2 <<= 1;
   for (int i = tid; i < P2; i += blockDim.x) {
@@ -1050,7 +1184,7 @@ __global__ void __launch_bounds__(1024) k_rb_tail(RbTail a) {
     for (int i = tid; i < L; i += blockDim.x) {
       const int v = (int)(sk[i] & 0xffffffffu);
       a.mv[v] = a.valid_list[a.draws[i]];
-      const int t = tier_of_degree(a.offs[v + 1] - a.offs[v]);
+      const int t = a.tm(a.offs[v + 1] - a.offs[v]);
       const unsigned long long q = atomicAdd(a.move_cnt + t, 1ull);
       a.move_lists[a.mseg.b[t] + q] = v;
     }
@@ -1107,7 +1241,7 @@ __global__ void __launch_bounds__(1024) k_rb_tail(RbTail a) {
       if (fits) {
         const int v = (int)(sk[i] & 0xffffffffu);
         a.mv[v] = a.valid_list[s_di];
-        const int t = tier_of_degree(a.offs[v + 1] - a.offs[v]);
+        const int t = a.tm(a.offs[v + 1] - a.offs[v]);
         const unsigned long long q = atomicAdd(a.move_cnt + t, 1ull);
         a.move_lists[a.mseg.b[t] + q] = v;
       }
@@ -1137,6 +1271,60 @@ __global__ void __launch_bounds__(1024) k_rb_tail(RbTail a) {
     __syncthreads();
     if (s_done) break;
   }
+}
+
+__global__ void __launch_bounds__(1024) k_rb_tail(RbTail a) {
+  extern __shared__ unsigned long long sk_dyn[];
+  rb_tail(a, sk_dyn);
+}
+
+// The whole selection chain of a rebalancing pass in one cooperative launch:
+// bucket scan -> crossing-chunk histogram -> crossing element -> select ->
+// (block 0) ordered tail. Replaces five dependent launches.
+struct RbCoop {
+  RbSel s;
+  const unsigned long long* H;
+  int nb;
+  int nover;
+  const long long* deficit;
+  const long long* required;
+  long long* cum_before;
+  const int32_t* opart;
+  int64_t n;
+  const int32_t* rcand;
+  const unsigned long long* rcand_cnt;
+  const int32_t* rbest;
+  int strong;
+  int32_t* evict;
+  unsigned long long* evict_cnt;
+  const int64_t* offs;
+  TierMap tm;
+  int32_t* move_lists;
+  RbSegsDev mseg;
+  unsigned long long* move_cnt;
+  RbTail tail;
+};
+
+__global__ void __launch_bounds__(1024) k_rb_coop(RbCoop a) {
+  extern __shared__ unsigned long long sk_dyn[];
+  cg::grid_group grid = cg::this_grid();
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  for (int op = blockIdx.x; op < a.nover; op += gridDim.x)
+    rb_scan_op<1024>(op, a.H, a.nb, a.deficit, const_cast<int32_t*>(a.s.bstar), a.cum_before);
+  grid.sync();
+  rb_chunk(a.s, a.rcand, a.rcand_cnt, t0, nt);
+  grid.sync();
+  for (int op = blockIdx.x; op < a.nover; op += gridDim.x) {
+    rb_find_op<1024>(op, a.s, a.deficit, a.required, a.cum_before, a.opart, a.n, a.nb,
+                     const_cast<int32_t*>(a.s.thr));
+    __syncthreads();
+  }
+  grid.sync();
+  rb_select(a.s, a.rcand, a.rcand_cnt, a.rbest, a.strong, 1, a.evict, a.evict_cnt, a.tail.mv,
+            a.offs, a.tm, a.move_lists, a.mseg, a.move_cnt, t0, nt);
+  grid.sync();
+  if (blockIdx.x == 0) rb_tail(a.tail, sk_dyn);
 }
 
 __global__ void k_rb_keys(const int32_t* __restrict__ evict, int64_t L,
@@ -1267,6 +1455,7 @@ struct RbCommit {
   const int32_t* dest_sorted;
   int32_t* mv;
   const int64_t* offs;
+  TierMap tm;
   int32_t* lists;  // move lists base
   int64_t seg_base[NBINS];
   unsigned long long* move_cnt;
@@ -1285,7 +1474,7 @@ __global__ void k_rb_commit(RbCommit a, int64_t L) {
       d = a.dest_sorted[i];
       if (d >= 0) {
         a.mv[v] = d;
-        t = tier_of_degree(a.offs[v + 1] - a.offs[v]);
+        t = a.tm(a.offs[v + 1] - a.offs[v]);
       }
       if (a.o_v) {
         a.o_v[i] = v;
@@ -1347,12 +1536,13 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
   const int64_t W = g.total_vw;
   std::vector<double> h_hb(nover);
   std::vector<long long> h_def(nover), h_req(nover), h_spare(nvalid);
-  long long sum_def = 0;
+  long long sum_def = 0, max_evict = 0;
   for (int i = 0; i < nover; ++i) {
     const int64_t pwp = pw[h_opart[i]];
     h_def[i] = pwp - (sigma + 1);
     h_req[i] = pwp - limit;
     sum_def += h_def[i];
+    max_evict += h_def[i] / std::max<int64_t>(g.min_vw, 1) + 1;
     volatile double ideal = (double)W / (double)k;
     volatile double diff = (double)pwp - ideal;
     h_hb[i] = 1.5 * diff;
@@ -1365,8 +1555,8 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
   const int ns = 34 - slot_min;
   const int nb = ns * rho;
   const int nch = (int)(((g.n + rho - 1) / rho + 31) / 32);
-  // at most sum(deficit) vertices leave (every selected weight is >= 1)
-  const bool fast = out == nullptr && sum_def <= TAIL_CAP;
+  // per part at most deficit/min_w + 1 vertices leave (selected prefix < deficit)
+  const bool fast = out == nullptr && max_evict <= TAIL_CAP;
   const bool direct = out == nullptr;
 
   std::vector<uint8_t>& up = w.h_up;
@@ -1380,7 +1570,7 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
   const size_t o_req = pk.put(h_req.data(), nover);
   const size_t o_spare = pk.put(h_spare.data(), nvalid);
   const size_t up_bytes = (pk.off + 15) & ~size_t(15);
-  c.ensure_pinned_up(up_bytes + (size_t)std::max<long long>(sum_def, 1) * 4 + 64);
+  c.ensure_pinned_up(up_bytes + (size_t)std::max<long long>(max_evict, 1) * 4 + 64);
   memcpy(c.pinned_up, up.data(), up_bytes);
   w.up.ensure(up_bytes + 64, c.stream);
   uint8_t* U = w.up.get();
@@ -1405,7 +1595,7 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
     mseg.b[t] = w.seg_base[t];
   }
   launch(c, "rb_collect", 8.0 * g.n, [&] {
-    k_rb_collect<<<grid_for(c, g.n, 256), 256, 0, c.stream>>>(parts, d_opidx, g.offs.get(), g.n,
+    k_rb_collect<<<grid_for(c, g.n, 256), 256, 0, c.stream>>>(parts, d_opidx, g.offs.get(), g.tm, g.n,
                                                              w.lists.get(), cseg,
                                                              w.ctr.get() + CTR_CAND);
   });
@@ -1432,24 +1622,9 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
                 w.ctr.get() + CTR_CAND);
 
   int32_t* bstar = w.bstar.get();
-  launch(c, "rb_scan", 8.0 * nover * nb, [&] {
-    k_rb_scan<<<nover, 256, 0, c.stream>>>(w.H.get(), nb, d_def, bstar, w.cum_before.get());
-  });
   RbSel s{parts, g.vw.get(), d_opidx, w.rkey.get(), bstar, w.thr.get(), rho, nch, w.CH.get()};
   const unsigned long long* rc = w.ctr.get() + CTR_RCAND;
-  launch(c, "rb_chunk", 0.0, [&] {
-    k_rb_chunk<<<grid_for(c, g.n, 256), 256, 0, c.stream>>>(s, w.rcand.get(), rc);
-  });
-  launch(c, "rb_find", 8.0 * nover * nch, [&] {
-    k_rb_find<<<nover, 256, 0, c.stream>>>(s, d_def, d_req, w.cum_before.get(), d_opart, g.n, nb,
-                                           w.thr.get());
-  });
   int32_t* move_base = w.lists.get() + w.cap_n;
-  launch(c, "rb_select", 0.0, [&] {
-    k_rb_select<<<grid_for(c, g.n, 256), 256, 0, c.stream>>>(
-        s, w.rcand.get(), rc, w.rbest.get(), strong, direct ? 1 : 0, w.evict.get(),
-        w.ctr.get() + CTR_EVICT, w.mv.get(), g.offs.get(), move_base, mseg, w.ctr.get() + CTR_MOVE);
-  });
 
   if (fast) {
     RbTail tl{};
@@ -1460,6 +1635,7 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
     tl.rkey = w.rkey.get();
     tl.vw = g.vw.get();
     tl.offs = g.offs.get();
+    tl.tm = g.tm;
     tl.valid_list = d_vlist;
     tl.spare = d_spare;
     tl.nvalid = nvalid;
@@ -1470,20 +1646,70 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
     tl.mseg = mseg;
     tl.move_cnt = w.ctr.get() + CTR_MOVE;
     if (!strong) {
-      // draws for the (at most sum_def) vertices without a valid connection,
-      // generated on the host while the kernels above run
-      const long long D = sum_def;
+      // draws for the (at most max_evict) vertices without a valid
+      // connection, generated on the host while the kernels above run
+      const long long D = max_evict;
       int32_t* hd = reinterpret_cast<int32_t*>(c.pinned_up + up_bytes);
       for (long long i = 0; i < D; ++i) hd[i] = (int32_t)rng.bounded((uint64_t)nvalid);
       w.draws.ensure(D > 0 ? D : 1, c.stream);
       h2d(c, w.draws.get(), hd, D);
       tl.draws = w.draws.get();
     }
+    RbCoop cp{};
+    cp.s = s;
+    cp.H = w.H.get();
+    cp.nb = nb;
+    cp.nover = nover;
+    cp.deficit = d_def;
+    cp.required = d_req;
+    cp.cum_before = w.cum_before.get();
+    cp.opart = d_opart;
+    cp.n = g.n;
+    cp.rcand = w.rcand.get();
+    cp.rcand_cnt = rc;
+    cp.rbest = w.rbest.get();
+    cp.strong = strong;
+    cp.evict = w.evict.get();
+    cp.evict_cnt = w.ctr.get() + CTR_EVICT;
+    cp.offs = g.offs.get();
+    cp.tm = g.tm;
+    cp.move_lists = move_base;
+    cp.mseg = mseg;
+    cp.move_cnt = w.ctr.get() + CTR_MOVE;
+    cp.tail = tl;
     const size_t smem = (size_t)TAIL_CAP * 8 + 1024 * 8;
-    CK(cudaFuncSetAttribute(k_rb_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    launch(c, "rb_tail", 0.0, [&] { k_rb_tail<<<1, 1024, smem, c.stream>>>(tl); });
+    static int coop_grid = 0;
+    if (!coop_grid) {
+      CK(cudaFuncSetAttribute(k_rb_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int per_sm = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rb_coop, 1024, smem));
+      JET_REQUIRE(per_sm >= 1, JET_EINTERNAL, "rebalance kernel does not fit on an SM");
+      coop_grid = per_sm * c.num_sms;
+    }
+    void* args[] = {&cp};
+    launch(c, "rb_select_coop", 0.0, [&] {
+      CK(cudaLaunchCooperativeKernel((const void*)k_rb_coop, dim3(coop_grid), dim3(1024), args,
+                                     smem, c.stream));
+    });
     return true;
   }
+
+  launch(c, "rb_scan", 8.0 * nover * nb, [&] {
+    k_rb_scan<<<nover, 256, 0, c.stream>>>(w.H.get(), nb, d_def, bstar, w.cum_before.get());
+  });
+  launch(c, "rb_chunk", 0.0, [&] {
+    k_rb_chunk<<<grid_for(c, g.n, 256), 256, 0, c.stream>>>(s, w.rcand.get(), rc);
+  });
+  launch(c, "rb_find", 8.0 * nover * nch, [&] {
+    k_rb_find<<<nover, 256, 0, c.stream>>>(s, d_def, d_req, w.cum_before.get(), d_opart, g.n, nb,
+                                           w.thr.get());
+  });
+  launch(c, "rb_select", 0.0, [&] {
+    k_rb_select<<<grid_for(c, g.n, 256), 256, 0, c.stream>>>(
+        s, w.rcand.get(), rc, w.rbest.get(), strong, direct ? 1 : 0, w.evict.get(),
+        w.ctr.get() + CTR_EVICT, w.mv.get(), g.offs.get(), g.tm, move_base, mseg,
+        w.ctr.get() + CTR_MOVE);
+  });
 
   // slow path (large evicted sets, or the parity entry point): order with a
   // device radix sort after reading the evicted count back
@@ -1547,6 +1773,7 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
   rcm.dest_sorted = w.dest_sorted.get();
   rcm.mv = w.mv.get();
   rcm.offs = g.offs.get();
+  rcm.tm = g.tm;
   rcm.lists = move_base;
   for (int t = 0; t < NBINS; ++t) rcm.seg_base[t] = w.seg_base[t];
   rcm.move_cnt = w.ctr.get() + CTR_MOVE;
