@@ -181,6 +181,7 @@ struct Ctx {
   cudaEvent_t timer_a = nullptr, timer_b = nullptr;
   DBuf<uint8_t> flush_buf;
   int32_t lock_epoch = 0;
+  bool host_levels = false;  // force the host-driven per-pass controller
 
   cudaEvent_t take_event();
   int prof_class(const char* name);
@@ -307,6 +308,23 @@ __device__ __forceinline__ void warp_append(bool take, int32_t v, int32_t* list,
   if (lane == leader) base = atomicAdd(cnt, (unsigned long long)__popc(m));
   base = __shfl_sync(am, base, leader);
   if (take) list[base + __popc(m & lanemask_lt())] = v;
+}
+
+// Block-wide int64 sum into *out for any blockDim <= 1024.
+__device__ __forceinline__ void block_sum_atomic_any(long long x, unsigned long long* out) {
+  __shared__ long long red_any[32];
+  x = gsum<32>(x, 0xffffffffu);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (l == 0) red_any[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    long long y = l < nw ? red_any[l] : 0;
+    y = gsum<32>(y, 0xffffffffu);
+    if (l == 0 && y != 0) atomicAdd(out, (unsigned long long)y);
+  }
+  __syncthreads();
 }
 
 // Block-wide int64 sum into *out (one atomic per block).

@@ -1,5 +1,6 @@
 // context.cu — jet_ctx lifetime, error reporting and launch profiling.
 #include "common.cuh"
+#include <cstdlib>
 #include <cstring>
 
 namespace jet {
@@ -103,6 +104,8 @@ int jet_create(int device, jet_ctx** out) {
     uint64_t thr = ~0ULL;
     CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     c->ensure_pinned(1 << 16);
+    const char* hl = getenv("JET_HOST_LEVELS");
+    c->host_levels = hl && hl[0] == '1';
     *out = reinterpret_cast<jet_ctx*>(c);
     return JET_OK;
   } catch (const Error& e) {

@@ -8,6 +8,8 @@
 #include "rng.h"
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 namespace jet {
 
@@ -19,6 +21,8 @@ static double now_s() {
 void refine_level(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, int64_t& cut,
                   const jet_config& cfg, bool finest, int level, jet_level_stats& st,
                   DBuf<int32_t>& keep) {
+  if (!c.host_levels && refine_level_device(c, w, g, parts, cut, cfg, finest, level, st, keep))
+    return;
   const int k = cfg.k;
   const int64_t limit = cfg.limit, sigma = cfg.sigma;
   w.ensure(c, g.n, k);
@@ -111,6 +115,11 @@ void refine_level(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, int64_t
         keep_pw = w.h_pw;
       }
     }
+    static const bool trace_on = getenv("JET_TRACE") && getenv("JET_TRACE")[0] == '1';
+    if (trace_on)
+      fprintf(stderr, "TRACE L%d it%d kind=%d nm=%lld cut=%lld worst=%lld noimp=%d best=%d\n", level,
+              st.iterations - 1, is_lp ? 1 : (rebal_streak <= 2 ? 2 : 3), (long long)ar.n_moves,
+              (long long)cut, (long long)worst(), no_improve, has_best ? 1 : 0);
     if (fixed_point) break;
   }
   d2d(c, parts, keep.get(), g.n);

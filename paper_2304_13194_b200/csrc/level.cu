@@ -1,0 +1,792 @@
+// level.cu — one cooperative kernel per refinement level: the whole
+// jet_refine loop (refine.py:190-294) runs on the device.
+//
+// Every iteration is a fixed sequence of grid-wide phases separated by grid
+// barriers; block 0 takes the controller decisions between them:
+//   decide  : balanced?  -> Jetlp pass | weak | strong | stop  (refine.py:229-263)
+//             rebalance scalars (oversized/valid parts, deficits, heavy
+//             bounds, spare, the pass's numpy PCG64 stream)      (rebalance.py)
+//   pass    : Jetlp: gains+filter sweep, afterburner           (refine.py:78-183)
+//             rebalance: collect, stats, bucket scan, crossing chunk,
+//             crossing element, select, ordered tail           (rebalance.py:91-240)
+//   apply   : exact cut delta + part weights, then commit      (conn.py:215-254)
+//   keep    : best / fallback tracking, phi rule               (refine.py:272-286)
+// The host launches once per level and reads the counters back once.
+#include "refine_dev.cuh"
+#include "controller.cuh"
+#include "rng_dev.cuh"
+#include <cub/block/block_reduce.cuh>
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <map>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+namespace jet {
+
+constexpr int LV_BLOCK = 512;
+constexpr int LV_TAIL_SMEM = 8192;  // evicted keys sorted in shared memory
+constexpr int LV_DRAW_SLACK = 64;
+constexpr int64_t LV_ROWS_PER_BLOCK = 512;
+
+struct LevelCtl {
+  long long cut, best_cut, keep_cut, keep_worst;
+  long long locked, moves, max_evict;
+  int has_best, no_improve, rebal_streak, pass_index;
+  int epoch, new_epoch;
+  int iterations, lp, weak, strong, stuck;
+  int kind;  // 0 stop, 1 Jetlp, 2 weak, 3 strong
+  int locks_all_clear, stop, copy_keep, abort;
+  int nover, nvalid, nb, nch, slot_min, rho;
+  unsigned long long rejects;
+  unsigned long long pcg_state_hi, pcg_state_lo, pcg_inc_hi, pcg_inc_lo;
+};
+
+struct LevelArgs {
+  GView g;
+  int64_t n;
+  int k;
+  TierMap tm;
+  int wide;
+  const int32_t* tlist[NBINS];
+  int64_t tcnt[NBINS];
+  RbSegsDev seg;
+  int tl_cap;
+  int32_t* parts;
+  int32_t* keep;
+  int32_t* cdest;
+  long long* F;
+  int32_t* mv;
+  int32_t* lock;
+  int32_t* cand_lists;
+  int32_t* move_lists;
+  unsigned long long* ctr;
+  long long* keep_pw;
+  int32_t* rkey;
+  int32_t* rbest;
+  double* rloss;
+  int32_t* rcand;
+  int32_t* evict;
+  unsigned long long* H;
+  unsigned long long* Hs;
+  unsigned long long* CH;
+  int32_t* opidx;
+  uint8_t* valid;
+  int32_t* valid_list;
+  int32_t* opart;
+  double* hb;
+  long long* deficit;
+  long long* required;
+  long long* spare;
+  long long* cum_before;
+  int32_t* bstar;
+  int32_t* thr;
+  int32_t* draws;
+  unsigned long long* gscratch;
+  long long limit, sigma, W, min_vw;
+  long long c_num, c_den;
+  double c_f;
+  int c_float;
+  int afterburner, locking;
+  double phi;
+  int no_improve_limit;
+  int sub_buckets;
+  unsigned long long seed;
+  int level;
+  int64_t H_cap, CH_cap, draws_cap;
+  LevelCtl* C;
+  long long* trace;  // optional: 6 values per iteration (JET_TRACE)
+  int trace_cap;
+  unsigned long long* phase_clk;  // optional: clock64 per phase (JET_PHASES)
+};
+
+// phase timer for block 0 / thread 0 (diagnostics only)
+__device__ __forceinline__ long long dev_clock() {
+#ifdef __CUDA_ARCH__
+  return clock64();
+#else
+  return 0;
+#endif
+}
+struct PhaseClock {
+  unsigned long long* acc;
+  long long t;
+  __device__ PhaseClock(unsigned long long* a) : acc(a), t(dev_clock()) {}
+  __device__ __forceinline__ void mark(int ph) {
+    if (acc && blockIdx.x == 0 && threadIdx.x == 0) {
+      const long long now = dev_clock();
+      atomicAdd(acc + ph, (unsigned long long)(now - t));
+      t = now;
+    }
+  }
+};
+
+__device__ __forceinline__ long long ldcg64(const long long* p) {
+  return (long long)__ldcg(reinterpret_cast<const unsigned long long*>(p));
+}
+__device__ __forceinline__ int ldv(const int* p) { return *(const volatile int*)p; }
+
+__device__ __forceinline__ int dev_ceil_log2(long long x) {
+  int r = 0;
+  while ((1LL << r) < x) ++r;
+  return r;
+}
+
+// ---------------------------------------------------------------- decide
+__device__ void lv_decide(const LevelArgs& A) {
+  typedef cub::BlockScan<int, LV_BLOCK> BScan;
+  typedef cub::BlockReduce<long long, LV_BLOCK> BRed;
+  __shared__ typename BScan::TempStorage ts;
+  __shared__ typename BRed::TempStorage tr;
+  __shared__ int s_unbal, s_kind, s_no, s_nv;
+  LevelCtl* C = A.C;
+  const long long* pw = reinterpret_cast<const long long*>(A.ctr + CTR_PW);
+  const int tid = threadIdx.x, k = A.k;
+  if (tid == 0) s_unbal = 0;
+  __syncthreads();
+  for (int p = tid; p < k; p += LV_BLOCK)
+    if (ldcg64(pw + p) > A.limit) s_unbal = 1;
+  __syncthreads();
+  if (tid == 0) {
+    int kind;
+    if (C->stop || C->no_improve >= A.no_improve_limit) {
+      kind = 0;
+    } else if (!s_unbal) {
+      kind = 1;
+      C->rebal_streak = 0;
+      C->locks_all_clear = !A.locking || C->locked == 0;
+      C->new_epoch = A.locking ? C->epoch + 1 : C->epoch;
+    } else if (C->rebal_streak >= 2 + k) {
+      C->stuck = 1;
+      kind = 0;
+    } else {
+      C->epoch = C->epoch + 1;  // table.reset_locks()
+      C->new_epoch = C->epoch;
+      C->locked = 0;
+      kind = C->rebal_streak < 2 ? 2 : 3;
+    }
+    s_kind = kind;
+    C->kind = kind;
+  }
+  for (int i = tid; i < CTR_PW; i += LV_BLOCK) A.ctr[i] = 0;
+  __syncthreads();
+  if (s_kind < 2) return;
+
+  // ---- rebalance scalars (rebalance.py:148-156, :127-131, :224)
+  const bool strong = s_kind == 3;
+  if (tid == 0) {
+    s_no = 0;
+    s_nv = 0;
+  }
+  __syncthreads();
+  long long my_evict = 0;
+  const double ideal = __ddiv_rn((double)A.W, (double)k);
+  for (int base = 0; base < k; base += LV_BLOCK) {
+    const int p = base + tid;
+    long long w = 0;
+    int fo = 0, fv = 0;
+    if (p < k) {
+      w = ldcg64(pw + p);
+      fo = w > A.limit;
+      fv = w < A.sigma;
+    }
+    int ro, rv, to, tv;
+    BScan(ts).ExclusiveSum(fo, ro, to);
+    __syncthreads();
+    BScan(ts).ExclusiveSum(fv, rv, tv);
+    const int bo = s_no, bv = s_nv;
+    if (p < k) {
+      A.opidx[p] = fo ? bo + ro : -1;
+      A.valid[p] = (uint8_t)fv;
+      if (fo) {
+        const int i = bo + ro;
+        A.opart[i] = p;
+        A.deficit[i] = w - (A.sigma + 1);
+        A.required[i] = w - A.limit;
+        A.hb[i] = __dmul_rn(1.5, __dsub_rn((double)w, ideal));
+        my_evict += (w - (A.sigma + 1)) / (A.min_vw > 0 ? A.min_vw : 1) + 1;
+      }
+      if (fv) {
+        A.valid_list[bv + rv] = p;
+        A.spare[bv + rv] = A.sigma - w;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      s_no = bo + to;
+      s_nv = bv + tv;
+    }
+    __syncthreads();
+  }
+  const long long tot_evict = BRed(tr).Sum(my_evict);
+  if (tid == 0) {
+    C->nover = s_no;
+    C->nvalid = s_nv;
+    // every evicted vertex is a candidate, so at most n leave
+    C->max_evict = tot_evict < A.n ? tot_evict : A.n;
+    C->rejects = 0;
+    if (s_nv == 0) {  // RebalanceInfeasibleError -> rebalance_stuck
+      C->stuck = 1;
+      C->kind = 0;
+    } else {
+      const int rho = (int64_t)A.sub_buckets >= A.n ? 1 : A.sub_buckets;
+      const int slot_min = strong ? 1 - dev_ceil_log2(k) : 0;
+      const int nb = (34 - slot_min) * rho;
+      const int nch = (int)(((A.n + rho - 1) / rho + 31) / 32);
+      C->rho = rho;
+      C->slot_min = slot_min;
+      C->nb = nb;
+      C->nch = nch;
+      if ((int64_t)s_no * nb > A.H_cap || (int64_t)s_no * nch > A.CH_cap ||
+          C->max_evict + LV_DRAW_SLACK > A.draws_cap) {
+        C->abort = 1;
+        C->kind = 0;
+      }
+      uint64_t sd[3] = {A.seed, (uint64_t)A.level, (uint64_t)C->pass_index};
+      DevPcg g;
+      if (A.level >= 0) {
+        g = dev_seed(sd, 3);
+      } else {
+        sd[1] = (uint64_t)C->pass_index;
+        g = dev_seed(sd, 2);
+      }
+      C->pcg_state_hi = (unsigned long long)(g.state >> 64);
+      C->pcg_state_lo = (unsigned long long)g.state;
+      C->pcg_inc_hi = (unsigned long long)(g.inc >> 64);
+      C->pcg_inc_lo = (unsigned long long)g.inc;
+    }
+  }
+}
+
+// -------------------------------------------------------------- bookkeep
+__device__ void lv_bookkeep(const LevelArgs& A) {
+  typedef cub::BlockReduce<long long, LV_BLOCK> BRed;
+  __shared__ typename BRed::TempStorage tr;
+  __shared__ int s_copy;
+  LevelCtl* C = A.C;
+  const long long* pw = reinterpret_cast<const long long*>(A.ctr + CTR_PW);
+  const int tid = threadIdx.x, k = A.k;
+  long long worst = LLONG_MIN;
+  for (int p = tid; p < k; p += LV_BLOCK) worst = max(worst, ldcg64(pw + p));
+  worst = BRed(tr).Reduce(worst, cub::Max());
+  if (tid == 0) {
+    const int kind = C->kind;
+    long long nm = 0;
+    for (int t = 0; t < NBINS; ++t) nm += (long long)__ldcg(A.ctr + CTR_MOVE + t);
+    const long long d2 = (long long)__ldcg(A.ctr + CTR_CUT2D);
+    C->cut += d2 / 2;
+    if (kind == 1) {
+      C->lp++;
+      if (A.locking) {
+        C->epoch = C->new_epoch;
+        C->locked = nm;
+      }
+    } else {
+      if (kind == 3) C->strong++;
+      else C->weak++;
+      C->rebal_streak++;
+    }
+    const bool fixed_point = kind == 1 && nm == 0 && C->locks_all_clear;
+    C->pass_index++;
+    C->iterations++;
+    C->moves += nm;
+    C->no_improve++;
+    int copy = 0;
+    const long long cut = C->cut;
+    if (worst <= A.limit) {
+      if (!C->has_best || cut < C->best_cut) {
+        if (!C->has_best || (double)cut < __dmul_rn(A.phi, (double)C->best_cut)) C->no_improve = 0;
+        copy = 1;
+        C->best_cut = cut;
+        C->keep_cut = cut;
+        C->has_best = 1;
+      }
+    } else if (!C->has_best && worst < C->keep_worst) {
+      copy = 1;
+      C->keep_worst = worst;
+      C->keep_cut = cut;
+    }
+    if (fixed_point) C->stop = 1;
+    C->copy_keep = copy;
+    s_copy = copy;
+    if (A.trace && C->iterations <= A.trace_cap) {
+      long long* t = A.trace + 6 * (C->iterations - 1);
+      t[0] = kind;
+      t[1] = nm;
+      t[2] = cut;
+      t[3] = worst;
+      t[4] = C->no_improve;
+      t[5] = C->has_best;
+    }
+  }
+  __syncthreads();
+  if (s_copy)
+    for (int p = tid; p < k; p += LV_BLOCK) A.keep_pw[p] = ldcg64(pw + p);
+}
+
+// ---------------------------------------------------------- rebalancing
+__device__ void lv_draws(const LevelArgs& A, int64_t t0, int64_t nt) {
+  LevelCtl* C = A.C;
+  const int nvalid = ldv(&C->nvalid);
+  const int64_t D = (int64_t)*(const volatile long long*)&C->max_evict;
+  if (nvalid <= 1) {  // integers(0, 1) returns 0 without drawing
+    for (int64_t j = t0; j < D; j += nt) A.draws[j] = 0;
+    return;
+  }
+  DevPcg g;
+  g.state = ((du128)*(const volatile unsigned long long*)&C->pcg_state_hi << 64) |
+            *(const volatile unsigned long long*)&C->pcg_state_lo;
+  g.inc = ((du128)*(const volatile unsigned long long*)&C->pcg_inc_hi << 64) |
+          *(const volatile unsigned long long*)&C->pcg_inc_lo;
+  const uint32_t excl = (uint32_t)nvalid, thr = (0xffffffffu - (uint32_t)(nvalid - 1)) % excl;
+  for (int64_t j = t0; j < D; j += nt) {
+    const uint64_t m = (uint64_t)pcg_word(g, (uint64_t)j) * excl;
+    if ((uint32_t)m < excl && (uint32_t)m < thr) atomicAdd(&C->rejects, 1ull);
+    A.draws[j] = (int32_t)(m >> 32);
+  }
+}
+
+__device__ void lv_draws_fixup(const LevelArgs& A) {
+  // a Lemire rejection shifted the stream: redo the draws sequentially
+  LevelCtl* C = A.C;
+  DevPcgSeq s;
+  s.g.state = ((du128)C->pcg_state_hi << 64) | C->pcg_state_lo;
+  s.g.inc = ((du128)C->pcg_inc_hi << 64) | C->pcg_inc_lo;
+  const int64_t D = C->max_evict;
+  for (int64_t j = 0; j < D; ++j) A.draws[j] = (int32_t)s.below((uint32_t)C->nvalid);
+}
+
+__device__ RbSel lv_sel(const LevelArgs& A) {
+  const LevelCtl* C = A.C;
+  return RbSel{A.parts, A.g.vw, A.opidx, A.rkey, A.bstar, A.thr, ldv(&C->rho), ldv(&C->nch), A.CH};
+}
+
+// --------------------------------------------------------- tier sweeps
+template <class Op, bool UNIT, class MakeArgs>
+__device__ void lv_sweep(const LevelArgs& A, MakeArgs mk, const int32_t* const* lists,
+                         const unsigned long long* dcnts, unsigned long long* smem, int64_t w0,
+                         int64_t nw, long long& acc) {
+  const bool wide = A.wide != 0;
+#pragma unroll 1
+  for (int t = 0; t < NBINS; ++t) {
+    if (A.tcnt[t] == 0) continue;
+    const typename Op::Args a = mk(t);
+    const int32_t* list = lists ? lists[t] : A.tlist[t];
+    const unsigned long long* dc = dcnts ? dcnts + t : nullptr;
+    const int64_t cnt = A.tcnt[t];
+    switch (t) {
+      case 0: agg_small<Op, 4, UNIT>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc); break;
+      case 1: agg_small<Op, 8, UNIT>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc); break;
+      case 2: agg_small<Op, 16, UNIT>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc); break;
+      case 3: agg_small<Op, 32, UNIT>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc); break;
+      case 4: {
+        const size_t per = (size_t)A.k + (size_t)(A.tl_cap + 3) / 2;
+        agg_warp<Op, UNIT>(a, A.g, A.parts, list, cnt, wide, A.k, A.tl_cap, dc,
+                           smem + 0 * per, w0, nw, acc);
+        __syncwarp();
+        break;
+      }
+      default:
+        __syncthreads();
+        agg_block<Op, UNIT>(a, A.g, A.parts, list, cnt, wide, A.k, dc, smem, acc);
+        __syncthreads();
+        break;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- kernel
+template <bool UNIT>
+__global__ void __launch_bounds__(LV_BLOCK, 2) k_level(LevelArgs A) {
+  extern __shared__ unsigned long long lv_smem[];
+  cg::grid_group grid = cg::this_grid();
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  const int64_t w0 = t0 >> 5, nw = nt >> 5;
+  LevelCtl* C = A.C;
+  // warp-tier tables: one per warp of the block
+  const size_t per = (size_t)A.k + (size_t)(A.tl_cap + 3) / 2;
+  unsigned long long* wtab = lv_smem + (threadIdx.x >> 5) * per;
+  SegLists cands, moves;
+  for (int t = 0; t < NBINS; ++t) {
+    cands.list[t] = A.cand_lists + A.seg.b[t];
+    moves.list[t] = A.move_lists + A.seg.b[t];
+  }
+  cands.cnt = A.ctr + CTR_CAND;
+  moves.cnt = A.ctr + CTR_MOVE;
+  int32_t* clists[NBINS];
+  for (int t = 0; t < NBINS; ++t) clists[t] = A.cand_lists + A.seg.b[t];
+
+  PhaseClock pc(A.phase_clk);
+  while (true) {
+    pc.mark(15);
+    if (blockIdx.x == 0) lv_decide(A);
+    grid.sync();
+    pc.mark(0);
+    const int kind = ldv(&C->kind);
+    if (kind == 0) break;
+    long long acc = 0;
+    if (kind == 1) {
+      // ---- Jetlp (refine.py:159-183)
+      LpParams lp;
+      lp.c_num = A.c_num;
+      lp.c_den = A.c_den;
+      lp.c_f = A.c_f;
+      lp.c_use_float = A.c_float;
+      lp.afterburner = A.afterburner;
+      lp.locking = A.locking;
+      lp.lock_epoch = ldv(&C->epoch);
+      auto mk = [&](int t) {
+        LpOp::Args a{};
+        a.parts = A.parts;
+        a.cdest = A.cdest;
+        a.F = A.F;
+        a.mv = A.mv;
+        a.lock = A.lock;
+        a.p = lp;
+        a.out_list = (A.afterburner ? A.cand_lists : A.move_lists) + A.seg.b[t];
+        a.out_cnt = A.ctr + (A.afterburner ? CTR_CAND : CTR_MOVE) + t;
+        a.cut2 = A.ctr + CTR_CUT2;
+        return a;
+      };
+      // per-warp tables start at lv_smem + warp * per inside agg_warp
+      lv_sweep<LpOp, UNIT>(A, mk, nullptr, nullptr, lv_smem, w0, nw, acc);
+      grid.sync();
+      pc.mark(1);
+      if (A.afterburner) {
+        AbArgs ab{};
+        ab.parts = A.parts;
+        ab.cdest = A.cdest;
+        ab.F = A.F;
+        ab.mv = A.mv;
+        ab.move_list = A.move_lists;
+        ab.move_cnt = A.ctr + CTR_MOVE;
+        afterburner_rows<UNIT>(ab, A.g, cands, A.seg, w0, nw);
+        grid.sync();
+        pc.mark(2);
+      }
+    } else {
+      // ---- weak / strong rebalancing (rebalance.py:139-240)
+      const int strong = kind == 3;
+      const int nover = ldv(&C->nover), nb = ldv(&C->nb), nch = ldv(&C->nch);
+      for (int64_t i = t0; i < (int64_t)nover * nb; i += nt) A.H[i] = 0;
+      for (int64_t i = t0; i < (int64_t)nover * (nb / ldv(&C->rho)); i += nt) A.Hs[i] = 0;
+      for (int64_t i = t0; i < (int64_t)nover * nch; i += nt) A.CH[i] = 0;
+      if (!strong) lv_draws(A, t0, nt);
+      rb_collect(A.parts, A.opidx, A.g.offs, A.tm, A.n, A.cand_lists, A.seg, A.ctr + CTR_CAND, t0, nt);
+      grid.sync();
+      pc.mark(3);
+      RbOp::Args ra{};
+      ra.parts = A.parts;
+      ra.vw = A.g.vw;
+      ra.opidx = A.opidx;
+      ra.valid = A.valid;
+      ra.hb = A.hb;
+      ra.nvalid = ldv(&C->nvalid);
+      ra.strong = strong;
+      ra.rho = ldv(&C->rho);
+      ra.slot_min = ldv(&C->slot_min);
+      ra.nb = nb;
+      ra.rkey = A.rkey;
+      ra.rbest = A.rbest;
+      ra.rloss = A.rloss;
+      ra.rcand = A.rcand;
+      ra.rcand_cnt = A.ctr + CTR_RCAND;
+      ra.H = A.H;
+      ra.Hs = A.Hs;
+      lv_sweep<RbOp, UNIT>(A, [&](int) { return ra; }, clists, A.ctr + CTR_CAND, lv_smem, w0, nw,
+                           acc);
+      grid.sync();
+      pc.mark(4);
+      const RbSel s = lv_sel(A);
+      for (int64_t op = w0; op < nover; op += nw)
+        rb_scan_warp((int)op, A.H, A.Hs, nb, ldv(&C->rho), A.deficit, A.bstar, A.cum_before);
+      grid.sync();
+      pc.mark(5);
+      rb_chunk(s, A.rcand, A.ctr + CTR_RCAND, t0, nt);
+      grid.sync();
+      pc.mark(6);
+      for (int64_t op = w0; op < nover; op += nw)
+        rb_find_warp((int)op, s, A.deficit, A.required, A.cum_before, A.opart, A.n, nb, A.thr);
+      grid.sync();
+      pc.mark(7);
+      rb_select(s, A.rcand, A.ctr + CTR_RCAND, A.rbest, strong, 1, A.evict, A.ctr + CTR_EVICT,
+                A.mv, A.g.offs, A.tm, A.move_lists, A.seg, A.ctr + CTR_MOVE, t0, nt);
+      grid.sync();
+      pc.mark(8);
+      if (blockIdx.x == 0) {
+        if (!strong && *(const volatile unsigned long long*)&C->rejects) {
+          if (threadIdx.x == 0) lv_draws_fixup(A);
+          __syncthreads();
+        }
+        RbTail tl{};
+        tl.evict = A.evict;
+        tl.evict_cnt = A.ctr + CTR_EVICT;
+        tl.parts = A.parts;
+        tl.opidx = A.opidx;
+        tl.rkey = A.rkey;
+        tl.vw = A.g.vw;
+        tl.offs = A.g.offs;
+        tl.tm = A.tm;
+        tl.valid_list = A.valid_list;
+        tl.draws = A.draws;
+        tl.spare = A.spare;
+        tl.nvalid = ldv(&C->nvalid);
+        tl.nb = nb;
+        tl.strong = strong;
+        tl.mv = A.mv;
+        tl.move_lists = A.move_lists;
+        tl.mseg = A.seg;
+        tl.move_cnt = A.ctr + CTR_MOVE;
+        tl.smem_cap = LV_TAIL_SMEM;
+        tl.gscratch = A.gscratch;
+        rb_tail(tl, lv_smem);
+      }
+      grid.sync();
+      pc.mark(9);
+    }
+    // ---- apply (conn.py:215-254)
+    {
+      ApArgs ap{A.parts, A.mv, A.ctr + CTR_PW, A.ctr + CTR_CUT2D, A.k};
+      long long d = 0;
+      apply_delta_rows<UNIT>(ap, A.g, moves, w0, nw, d);
+      block_sum_atomic_any(d, A.ctr + CTR_CUT2D);
+    }
+    grid.sync();
+    pc.mark(10);
+    {
+      CommitArgs ca{};
+      ca.parts = A.parts;
+      ca.mv = A.mv;
+      ca.lock = A.lock;
+      ca.epoch = ldv(&C->new_epoch);
+      ca.set_lock = kind == 1 && A.locking;
+      for (int t = 0; t < NBINS; ++t) ca.lists[t] = moves.list[t];
+      ca.cnts = A.ctr + CTR_MOVE;
+      apply_commit_rows(ca, t0, nt);
+    }
+    if (blockIdx.x == 0) lv_bookkeep(A);
+    grid.sync();
+    pc.mark(11);
+    if (ldv(&C->copy_keep))
+      for (int64_t v = t0; v < A.n; v += nt) A.keep[v] = A.parts[v];
+    (void)wtab;
+  }
+  // the returned state is the best balanced one, or the fallback
+  for (int64_t v = t0; v < A.n; v += nt) A.parts[v] = A.keep[v];
+}
+
+// ------------------------------------------------------------------ host
+static int ceil_log2_host(int64_t x) {
+  int r = 0;
+  while ((1LL << r) < x) ++r;
+  return r;
+}
+
+struct LevelScratch {
+  DBuf<LevelCtl> ctl;
+  DBuf<long long> keep_pw;
+  DBuf<int32_t> backup;
+  DBuf<unsigned long long> gscratch;
+};
+
+static LevelScratch& level_scratch(Ctx& c) {
+  static thread_local std::map<Ctx*, LevelScratch> m;
+  return m[&c];
+}
+
+bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, int64_t& cut,
+                         const jet_config& cfg, bool finest, int level, jet_level_stats& st,
+                         DBuf<int32_t>& keep) {
+  const int k = cfg.k;
+  const int rho = (int64_t)cfg.sub_buckets >= g.n ? 1 : cfg.sub_buckets;
+  if (rho > 4096) return false;
+  const int tl_cap = (int)std::min<int64_t>(k, WARP_TIER_MAX_DEG);
+  const size_t per = ((size_t)k + (size_t)(tl_cap + 3) / 2) * 8;
+  size_t smem = (size_t)LV_TAIL_SMEM * 8 + LV_BLOCK * 8;
+  if (g.bin_cnt[BIN_WARP]) smem = std::max(smem, per * (LV_BLOCK / 32));
+  if (g.bin_cnt[BIN_BLOCK]) smem = std::max(smem, (size_t)k * 12);
+  if (smem > (size_t)c.max_smem_optin) return false;
+
+  w.ensure(c, g.n, k);
+  w.bind_level(g);
+  LevelScratch& S = level_scratch(c);
+  S.ctl.ensure(1, c.stream);
+  S.keep_pw.ensure(k, c.stream);
+  S.backup.ensure(g.n, c.stream);
+  S.gscratch.ensure(2 * (size_t)g.n + 2 * LV_BLOCK + 64, c.stream);
+  keep.ensure(g.n, c.stream);
+  const int slot_span = 34 + std::max(0, ceil_log2_host(k) - 1);
+  const int64_t nb_max = (int64_t)slot_span * rho;
+  const int64_t nch = ((g.n + rho - 1) / rho + 31) / 32;
+  w.H.ensure((size_t)k * nb_max, c.stream);
+  w.Hs.ensure((size_t)k * slot_span, c.stream);
+  w.CH.ensure((size_t)k * nch, c.stream);
+  w.draws.ensure(g.n + LV_DRAW_SLACK + 64, c.stream);
+  w.hb.ensure(k, c.stream);
+
+  const std::vector<int64_t> pw_in = w.h_pw;
+  h2d(c, w.d_pw(), w.h_pw.data(), k);
+  h2d(c, S.keep_pw.get(), (const long long*)w.h_pw.data(), k);
+  d2d(c, keep.get(), parts, g.n);
+  d2d(c, S.backup.get(), parts, g.n);
+
+  LevelCtl h{};
+  bool bal = true;
+  int64_t worst = 0;
+  for (int p = 0; p < k; ++p) {
+    bal &= w.h_pw[p] <= cfg.limit;
+    worst = std::max<int64_t>(worst, w.h_pw[p]);
+  }
+  if (getenv("JET_TRACE") && getenv("JET_TRACE")[0] == '1') {
+    fprintf(stderr, "LEVEL %d start cut=%lld bal=%d worst=%lld pw=", level, (long long)cut, (int)bal,
+            (long long)worst);
+    for (int p = 0; p < k && p < 16; ++p) fprintf(stderr, "%lld ", (long long)w.h_pw[p]);
+    fprintf(stderr, "\n");
+  }
+  h.cut = cut;
+  h.best_cut = cut;
+  h.keep_cut = cut;
+  h.keep_worst = worst;
+  h.has_best = bal;
+  h.epoch = ++c.lock_epoch;
+  h.new_epoch = h.epoch;
+  h2d(c, S.ctl.get(), &h, 1);
+
+  LevelArgs A{};
+  A.g = view(g);
+  A.n = g.n;
+  A.k = k;
+  A.tm = g.tm;
+  A.wide = g.max_wdeg >= (1LL << 31);
+  for (int t = 0; t < NBINS; ++t) {
+    A.tlist[t] = tier_list(g, t);
+    A.tcnt[t] = g.bin_cnt[t];
+    A.seg.b[t] = w.seg_base[t];
+  }
+  A.tl_cap = tl_cap;
+  A.parts = parts;
+  A.keep = keep.get();
+  A.cdest = w.cdest.get();
+  A.F = w.F.get();
+  A.mv = w.mv.get();
+  A.lock = w.lock.get();
+  A.cand_lists = w.lists.get();
+  A.move_lists = w.lists.get() + w.cap_n;
+  A.ctr = w.ctr.get();
+  A.keep_pw = S.keep_pw.get();
+  A.rkey = w.rkey.get();
+  A.rbest = w.rbest.get();
+  A.rloss = w.rloss.get();
+  A.rcand = w.rcand.get();
+  A.evict = w.evict.get();
+  A.H = w.H.get();
+  A.Hs = w.Hs.get();
+  A.CH = w.CH.get();
+  A.opidx = w.opidx.get();
+  A.valid = w.valid.get();
+  A.valid_list = w.valid_list.get();
+  A.opart = w.opart.get();
+  A.hb = w.hb.get();
+  A.deficit = w.deficit.get();
+  A.required = w.required.get();
+  A.spare = w.spare.get();
+  A.cum_before = w.cum_before.get();
+  A.bstar = w.bstar.get();
+  A.thr = w.thr.get();
+  A.draws = w.draws.get();
+  A.gscratch = S.gscratch.get();
+  A.limit = cfg.limit;
+  A.sigma = cfg.sigma;
+  A.W = g.total_vw;
+  A.min_vw = g.min_vw;
+  A.c_num = finest ? cfg.c_finest_num : cfg.c_other_num;
+  A.c_den = finest ? cfg.c_finest_den : cfg.c_other_den;
+  A.c_f = finest ? cfg.c_finest : cfg.c_other;
+  A.c_float = finest ? cfg.c_finest_float : cfg.c_other_float;
+  A.afterburner = cfg.afterburner;
+  A.locking = cfg.locking;
+  A.phi = cfg.phi;
+  A.no_improve_limit = cfg.no_improve_limit;
+  A.sub_buckets = cfg.sub_buckets;
+  A.seed = cfg.seed;
+  A.level = level;
+  A.H_cap = (int64_t)w.H.n;
+  A.CH_cap = (int64_t)w.CH.n;
+  A.draws_cap = (int64_t)w.draws.n;
+  A.C = S.ctl.get();
+
+  static const bool trace_on = getenv("JET_TRACE") && getenv("JET_TRACE")[0] == '1';
+  DBuf<long long> trace;
+  if (trace_on) {
+    trace.alloc(6 * 4096, c.stream);
+    A.trace = trace.get();
+    A.trace_cap = 4096;
+  }
+  static const bool phases_on = getenv("JET_PHASES") && getenv("JET_PHASES")[0] == '1';
+  DBuf<unsigned long long> pclk;
+  if (phases_on) {
+    pclk.alloc(16, c.stream);
+    dzero(c, pclk.get(), 16);
+    A.phase_clk = pclk.get();
+  }
+  const void* kern = g.unit_ew ? (const void*)k_level<true> : (const void*)k_level<false>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, LV_BLOCK, smem));
+  if (per_sm < 1) return false;
+  // grid barriers dominate small levels: size the cooperative grid to the
+  // level (about LV_ROWS_PER_BLOCK vertices per block), capped at residency
+  const int64_t want = (g.n + LV_ROWS_PER_BLOCK - 1) / LV_ROWS_PER_BLOCK;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * c.num_sms));
+  void* args[] = {&A};
+  launch(c, "refine_level", 0.0, [&] {
+    CK(cudaLaunchCooperativeKernel(kern, dim3(blocks), dim3(LV_BLOCK), args, smem, c.stream));
+  });
+  d2h(c, &h, S.ctl.get(), 1);
+  w.h_pw.resize(k);
+  d2h(c, w.h_pw.data(), (int64_t*)S.keep_pw.get(), k);
+  c.sync();
+  if (phases_on) {
+    unsigned long long pc[16];
+    d2h(c, pc, pclk.get(), 16);
+    c.sync();
+    static const char* names[16] = {"decide", "lp_sweep", "afterburner", "rb_collect", "rb_stats",
+                                    "rb_scan", "rb_chunk", "rb_find", "rb_select", "rb_tail",
+                                    "apply_delta", "commit+keep", "", "", "", "keep_copy"};
+    fprintf(stderr, "PHASES L%d blocks=%d iters=%d:", level, blocks, h.iterations);
+    for (int i = 0; i < 16; ++i)
+      if (pc[i]) fprintf(stderr, " %s=%.1fus", names[i], pc[i] / 1965.0 / std::max(1, h.iterations));
+    fprintf(stderr, "\n");
+  }
+  if (h.abort) {  // outside the device path's limits: rerun on the host path
+    d2d(c, parts, S.backup.get(), g.n);
+    w.h_pw = pw_in;
+    h2d(c, w.d_pw(), w.h_pw.data(), k);
+    c.sync();
+    c.lock_epoch = h.epoch + 1;
+    return false;
+  }
+  c.lock_epoch = h.epoch + 1;
+  if (trace_on) {
+    std::vector<long long> t(6 * std::min(h.iterations, 4096));
+    d2h(c, t.data(), trace.get(), t.size());
+    c.sync();
+    for (size_t i = 0; i < t.size(); i += 6)
+      fprintf(stderr, "TRACE L%d it%zu kind=%lld nm=%lld cut=%lld worst=%lld noimp=%lld best=%lld\n",
+              level, i / 6, t[i], t[i + 1], t[i + 2], t[i + 3], t[i + 4], t[i + 5]);
+  }
+  cut = h.keep_cut;
+  st.iterations += h.iterations;
+  st.lp_passes += h.lp;
+  st.weak_passes += h.weak;
+  st.strong_passes += h.strong;
+  st.moves += h.moves;
+  st.rebalance_stuck = h.stuck;
+  st.balanced = h.has_best;
+  return true;
+}
+
+}  // namespace jet

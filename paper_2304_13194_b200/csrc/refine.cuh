@@ -45,8 +45,8 @@ struct Workspace {
   DBuf<int32_t> cdest, mv, lock, lists, rkey, rbest, rcand, evict, dest_sorted, draws;
   DBuf<long long> F;
   DBuf<double> rloss;
-  DBuf<unsigned long long> ctr, H, CH, keys, keys_alt;
-  DBuf<int32_t> opidx, valid_list, bstar, thr;
+  DBuf<unsigned long long> ctr, H, Hs, CH, keys, keys_alt;
+  DBuf<int32_t> opidx, valid_list, bstar, thr, opart;
   DBuf<uint8_t> valid;
   DBuf<double> hb;
   DBuf<long long> deficit, required, spare, cum_before;

@@ -1,0 +1,1065 @@
+// refine_dev.cuh — device-side building blocks of the Jet refinement passes,
+// shared by the multi-kernel path (refine.cu) and the persistent per-level
+// controller kernel (level.cu). Every function takes its work range
+// explicitly (warp or thread start + stride) so it runs unchanged as a
+// standalone kernel body or as one phase of a cooperative kernel.
+#pragma once
+#include "refine.cuh"
+#include <cub/block/block_scan.cuh>
+
+namespace jet {
+
+// ===========================================================================
+// Row aggregation framework. For every vertex v of a tier, conn(v, p) is
+// aggregated over the row; an Op decides which parts compete for the "best"
+// slot, what else is summed, and what to do with the result.
+//   tiers 0-3: one G-lane group per row, __match_any_sync groups equal parts
+//   tier 4   : one warp per row, per-warp shared-memory table of k entries
+//   tier 5   : one block per row, per-block shared-memory table
+// ===========================================================================
+
+static __device__ __forceinline__ unsigned long long pack_best(long long conn, int p) {
+  return ((unsigned long long)conn << KBITS) | (unsigned)(KMASK - p);
+}
+static __device__ __forceinline__ int unpack_part(unsigned long long key) {
+  return KMASK - (int)(key & KMASK);
+}
+static __device__ __forceinline__ long long unpack_conn(unsigned long long key) {
+  return (long long)(key >> KBITS);
+}
+
+// ---- Jetlp gains op --------------------------------------------------------
+struct LpOp {
+  struct Args {
+    const int32_t* parts;
+    int32_t* cdest;
+    long long* F;
+    int32_t* mv;
+    const int32_t* lock;
+    LpParams p;
+    int32_t* out_list;  // candidate list (afterburner on) or move list (off)
+    unsigned long long* out_cnt;
+    unsigned long long* cut2;
+    LpDebug dbg;
+  };
+  static __device__ __forceinline__ bool skip(const Args&, int, int) { return false; }
+  static __device__ __forceinline__ bool competes(const Args&, int p, int own) { return p != own; }
+  static __device__ __forceinline__ int extra(const Args&, int, int w) { return w; }
+  // self_c = conn(v, own); key = best other part; ex = weighted degree
+  static __device__ __forceinline__ void finish(const Args& a, int v, int own,
+                                                long long self_c,
+                                                unsigned long long key,
+                                                long long ex, long long& acc) {
+    acc += ex - self_c;
+    const bool boundary = key != 0;
+    const int dest = boundary ? unpack_part(key) : own;
+    const long long F = boundary ? unpack_conn(key) - self_c : NO_GAIN;
+    bool cand = false;
+    if (boundary && !(a.p.locking && a.lock[v] == a.p.lock_epoch)) {
+      if (a.p.afterburner) {
+        long long bound = a.p.c_use_float
+                              ? (long long)floor(a.p.c_f * (double)self_c)
+                              : self_c * a.p.c_num / a.p.c_den;
+        cand = -F < bound;
+      } else {
+        cand = F >= 0;
+      }
+    }
+    if (a.p.afterburner) {
+      a.cdest[v] = cand ? dest : -1;
+      if (cand) a.F[v] = F;
+    } else if (cand) {
+      a.mv[v] = dest;
+    }
+    if (a.dbg.dest) a.dbg.dest[v] = dest;
+    if (a.dbg.gain) a.dbg.gain[v] = F;
+    if (a.dbg.boundary) a.dbg.boundary[v] = boundary;
+    if (a.dbg.conn_self) a.dbg.conn_self[v] = self_c;
+    warp_append(cand, v, a.out_list, a.out_cnt);
+  }
+  static __device__ __forceinline__ void block_done(const Args& a, long long acc) {
+    block_sum_atomic_any(acc, a.cut2);
+  }
+};
+
+// ---- rebalance candidate stats op (rebalance.py:91-113, 35-51) -------------
+struct RbOp {
+  struct Args {
+    const int32_t* parts;
+    const int32_t* vw;
+    const int32_t* opidx;   // part -> oversized rank or -1
+    const uint8_t* valid;   // part -> valid destination
+    const double* hb;       // heavy bound per oversized rank
+    int nvalid;
+    int strong;
+    int rho;
+    int slot_min;
+    int nb;                 // buckets per oversized part
+    int32_t* rkey;
+    int32_t* rbest;
+    double* rloss;
+    int32_t* rcand;
+    unsigned long long* rcand_cnt;
+    unsigned long long* H;
+    unsigned long long* Hs;  // per-slot totals (ns per oversized part)
+  };
+  static __device__ __forceinline__ bool skip(const Args& a, int, int own) {
+    return a.opidx[own] < 0;
+  }
+  static __device__ __forceinline__ bool competes(const Args& a, int p, int) {
+    return a.valid[p] != 0;
+  }
+  static __device__ __forceinline__ int extra(const Args& a, int p, int w) {
+    return a.valid[p] ? w : 0;
+  }
+  static __device__ __forceinline__ void finish(const Args& a, int v, int own,
+                                                long long conn_src,
+                                                unsigned long long key,
+                                                long long sum_valid, long long&) {
+    const int op = a.opidx[own];
+    const long long best_conn = key ? unpack_conn(key) : 0;
+    const int best_part = key ? unpack_part(key) : -1;
+    int slot;
+    double loss;
+    if (!a.strong) {
+      const long long L = conn_src - best_conn;
+      loss = (double)L;
+      slot = L < 0 ? 0 : L == 0 ? 1 : min(2 + (63 - __clzll(L)), 33);
+    } else {
+      // numpy: int64 - (int64 / int) -> float64 (rebalance.py:213)
+      loss = (double)conn_src - (double)sum_valid / (double)a.nvalid;
+      if (loss < 0) slot = 0;
+      else if (loss == 0) slot = 1;
+      else slot = min(2 + ilogb(loss), 33);
+    }
+    slot = max(slot, a.slot_min);
+    const int w = a.vw[v];
+    const bool eligible = (double)w <= a.hb[op];
+    bool take = false;
+    if (eligible) {
+      const int bucket = (slot - a.slot_min) * a.rho + (v % a.rho);
+      a.rkey[v] = bucket;
+      a.rbest[v] = best_part;
+      a.rloss[v] = loss;
+      atomicAdd(&a.H[(size_t)op * a.nb + bucket], (unsigned long long)w);
+      atomicAdd(&a.Hs[(size_t)op * (a.nb / a.rho) + (slot - a.slot_min)], (unsigned long long)w);
+      take = true;
+    } else {
+      a.rkey[v] = -1;
+    }
+    warp_append(take, v, a.rcand, a.rcand_cnt);
+  }
+  static __device__ __forceinline__ void block_done(const Args&, long long) {}
+};
+
+// Tiers 0-3. A warp owns 32 consecutive list entries: vertex ids, offsets
+// and own parts are loaded once, coalesced. Rows are then swept in G steps
+// of 32/G rows (one G-lane group per row); U steps are batched so their
+// adjacency loads and neighbour-part gathers are all in flight together
+// (the single-row-per-warp form is latency-bound at ~300 GB/s). The result
+// of row r is shuffled to lane r, which finishes vertex r.
+template <class Op, int G, bool UNIT>
+static __device__ __forceinline__ void agg_small(const typename Op::Args& a, const GView& g,
+                                          const int32_t* __restrict__ parts,
+                                          const int32_t* __restrict__ list, int64_t cnt,
+                                          bool wide, const unsigned long long* __restrict__ dcnt,
+                                          int64_t w0, int64_t nw, long long& acc) {
+  if (dcnt) cnt = (int64_t)*(const volatile unsigned long long*)dcnt;
+  constexpr int RPS = 32 / G;         // rows per step
+  constexpr int U = G >= 8 ? 8 : G;   // steps per batch (G steps in total)
+  const unsigned gm = group_mask<G>();
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1), grp = lane / G;
+  // rows per warp batch: 32 when there is plenty of work, fewer for small
+  // lists so every warp gets rows (latency, not bandwidth, rules there)
+  const int64_t per_w = (cnt + nw - 1) / nw;
+  const int R = per_w >= 32 ? 32 : (per_w < 1 ? 1 : (int)per_w);
+  for (int64_t base = w0 * R; base < cnt; base += nw * R) {
+    const int64_t idx = base + lane;
+    int v = 0, own = -1, deg = 0;
+    int64_t beg = 0;
+    if (lane < R && idx < cnt) {
+      v = list ? list[idx] : (int)idx;
+      own = parts[v];
+      if (Op::skip(a, v, own)) {
+        own = -1;
+      } else {
+        beg = g.offs[v];
+        deg = (int)(g.offs[v + 1] - beg);
+      }
+    }
+    long long my_self = 0, my_ex = 0;
+    unsigned long long my_key = 0;
+#pragma unroll
+    for (int s0 = 0; s0 < G; s0 += U) {
+      if (s0 * RPS >= R) break;  // remaining steps hold no rows
+      int uu[U], ww[U], pp[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int r = (s0 + q) * RPS + grp;
+        const int64_t rb = __shfl_sync(0xffffffffu, beg, r);
+        const int rd = __shfl_sync(0xffffffffu, deg, r);
+        uu[q] = -1;
+        ww[q] = 0;
+        if (gl < rd) {
+          uu[q] = g.adj[rb + gl];
+          ww[q] = UNIT ? 1 : g.ew[rb + gl];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) pp[q] = uu[q] >= 0 ? parts[uu[q]] : -1;
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int st = s0 + q;
+        const int rown = __shfl_sync(0xffffffffu, own, st * RPS + grp);
+        const int p = pp[q];
+        const unsigned peers = __match_any_sync(gm, p);
+        const bool comp = p >= 0 && p != rown && Op::competes(a, p, rown);
+        const int src = ((lane - st * RPS) & (RPS - 1)) * G;
+        if (!wide) {
+          // 32-bit sums (weighted degree < 2^31): single-instruction REDUX
+          // reductions; best part = max conn, then lowest part id
+          const unsigned sm =
+              UNIT ? (unsigned)__popc(peers) : __reduce_add_sync(peers, (unsigned)ww[q]);
+          const unsigned sc =
+              UNIT ? (unsigned)__popc(__ballot_sync(gm, p >= 0 && p == rown))
+                   : __reduce_add_sync(gm, (p >= 0 && p == rown) ? (unsigned)ww[q] : 0u);
+          const unsigned mx = __reduce_max_sync(gm, comp ? sm : 0u);
+          const unsigned pm = __reduce_min_sync(gm, (comp && sm == mx) ? (unsigned)p : 0xffffffffu);
+          const unsigned ex = __reduce_add_sync(gm, p >= 0 ? (unsigned)Op::extra(a, p, ww[q]) : 0u);
+          const unsigned dsc = __shfl_sync(0xffffffffu, sc, src);
+          const unsigned dmx = __shfl_sync(0xffffffffu, mx, src);
+          const unsigned dpm = __shfl_sync(0xffffffffu, pm, src);
+          const unsigned dex = __shfl_sync(0xffffffffu, ex, src);
+          if (lane / RPS == st) {
+            my_self = dsc;
+            my_key = dmx ? pack_best((long long)dmx, (int)dpm) : 0ull;
+            my_ex = dex;
+          }
+        } else {
+          const long long sm = UNIT ? (long long)__popc(peers) : peer_sum(peers, ww[q], wide);
+          const bool lead = p >= 0 && (__ffs(peers) - 1) == lane;
+          long long sc = (lead && p == rown) ? sm : 0;
+          unsigned long long key = (lead && comp) ? pack_best(sm, p) : 0ull;
+          long long ex = p >= 0 ? Op::extra(a, p, ww[q]) : 0;
+          sc = gsum<G>(sc, gm);
+          key = gmax<G>(key, gm);
+          ex = gsum<G>(ex, gm);
+          sc = __shfl_sync(0xffffffffu, sc, src);
+          key = __shfl_sync(0xffffffffu, key, src);
+          ex = __shfl_sync(0xffffffffu, ex, src);
+          if (lane / RPS == st) {
+            my_self = sc;
+            my_key = key;
+            my_ex = ex;
+          }
+        }
+      }
+    }
+    if (own >= 0) Op::finish(a, v, own, my_self, my_key, my_ex, acc);
+  }
+}
+
+// Tier 4 (33..2048 entries). A warp owns 32 rows; per-vertex data is loaded
+// once, coalesced. Rows are aggregated one after another into a per-warp
+// shared-memory part table, but the adjacency of the next chunk batch (of
+// this row, or of the next row) is loaded while the current batch's
+// neighbour parts are gathered and aggregated, so two batches of loads are
+// always in flight. Shared layout per warp: tab[k] (u64), tl[tl_cap] (i32),
+// tcnt (i32).
+template <class Op, bool UNIT>
+static __device__ void agg_warp(const typename Op::Args& a, const GView& g,
+                         const int32_t* __restrict__ parts, const int32_t* __restrict__ list,
+                         int64_t cnt, bool wide, int k, int tl_cap,
+                         const unsigned long long* __restrict__ dcnt, unsigned long long* smem,
+                         int64_t w0, int64_t nw, long long& acc) {
+  if (dcnt) cnt = (int64_t)*(const volatile unsigned long long*)dcnt;
+  constexpr int U = 2;  // chunks of 32 entries per batch
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t per = (size_t)k + (size_t)(tl_cap + 3) / 2;
+  unsigned long long* tab = smem + wib * per;
+  int* tl = reinterpret_cast<int*>(tab + k);
+  int* tcnt = tl + tl_cap;
+  for (int i = lane; i < k; i += 32) tab[i] = 0;
+  if (lane == 0) *tcnt = 0;
+  __syncwarp();
+  const int64_t per_w = (cnt + nw - 1) / nw;
+  const int R = per_w >= 32 ? 32 : (per_w < 1 ? 1 : (int)per_w);
+  for (int64_t base = w0 * R; base < cnt; base += nw * R) {
+    const int64_t idx = base + lane;
+    int v = 0, own = -1, deg = 0;
+    int64_t beg = 0;
+    if (lane < R && idx < cnt) {
+      v = list ? list[idx] : (int)idx;
+      own = parts[v];
+      if (Op::skip(a, v, own)) {
+        own = -1;
+      } else {
+        beg = g.offs[v];
+        deg = (int)(g.offs[v + 1] - beg);
+      }
+    }
+    long long my_self = 0, my_ex = 0;
+    unsigned long long my_key = 0;
+    // pipeline state: (row, first chunk) of the batch whose adjacency is loaded
+    int r = 0, c0 = 0;
+    int64_t rb = __shfl_sync(0xffffffffu, beg, 0);
+    int rd = __shfl_sync(0xffffffffu, deg, 0);
+    int uu[U], ww[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int j = (c0 + q) * 32 + lane;
+      uu[q] = j < rd ? g.adj[rb + j] : -1;
+      ww[q] = (j < rd) ? (UNIT ? 1 : g.ew[rb + j]) : 0;
+    }
+    long long ex = 0;
+    while (r < R) {
+      int pp[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) pp[q] = uu[q] >= 0 ? parts[uu[q]] : -1;
+      // next batch: same row if it has more chunks, else the next row
+      const int cur_r = r, cur_d = rd;
+      int wv[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) wv[q] = ww[q];
+      if ((c0 + U) * 32 < rd) {
+        c0 += U;
+      } else {
+        ++r;
+        c0 = 0;
+        rb = __shfl_sync(0xffffffffu, beg, r & 31);
+        rd = r < R ? __shfl_sync(0xffffffffu, deg, r & 31) : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int j = (c0 + q) * 32 + lane;
+        uu[q] = (r < R && j < rd) ? g.adj[rb + j] : -1;
+        ww[q] = (r < R && j < rd) ? (UNIT ? 1 : g.ew[rb + j]) : 0;
+      }
+      // aggregate the current batch
+      const int rown = __shfl_sync(0xffffffffu, own, cur_r);
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int p = pp[q];
+        if (p >= 0) ex += Op::extra(a, p, wv[q]);
+        const unsigned peers = __match_any_sync(0xffffffffu, p);
+        const long long sm = UNIT ? (long long)__popc(peers) : peer_sum(peers, wv[q], wide);
+        if (p >= 0 && (__ffs(peers) - 1) == lane) {
+          const unsigned long long old = atomicAdd(&tab[p], (unsigned long long)sm);
+          if (old == 0) tl[atomicAdd(tcnt, 1)] = p;
+        }
+      }
+      if (r != cur_r) {  // row cur_r complete: reduce its table
+        __syncwarp();
+        const int nt = *tcnt;
+        long long sc = 0;
+        unsigned long long key = 0;
+        long long ext;
+        if (!wide) {
+          // 32-bit sums: REDUX reductions (max conn, then lowest part)
+          unsigned usc = 0, bm = 0, bp = 0xffffffffu;
+          for (int t = lane; t < nt; t += 32) {
+            const int p = tl[t];
+            const unsigned cv = (unsigned)tab[p];
+            tab[p] = 0;
+            if (p == rown) usc = cv;
+            else if (Op::competes(a, p, rown) && (cv > bm || (cv == bm && (unsigned)p < bp))) {
+              bm = cv;
+              bp = (unsigned)p;
+            }
+          }
+          usc = __reduce_add_sync(0xffffffffu, usc);
+          const unsigned mx = __reduce_max_sync(0xffffffffu, bm);
+          const unsigned pm = __reduce_min_sync(0xffffffffu, bm == mx ? bp : 0xffffffffu);
+          sc = usc;
+          key = mx ? pack_best((long long)mx, (int)pm) : 0ull;
+          ext = __reduce_add_sync(0xffffffffu, (unsigned)ex);
+        } else {
+          for (int t = lane; t < nt; t += 32) {
+            const int p = tl[t];
+            const long long cv = (long long)tab[p];
+            tab[p] = 0;
+            if (p == rown) sc = cv;
+            else if (Op::competes(a, p, rown)) {
+              const unsigned long long kk = pack_best(cv, p);
+              key = kk > key ? kk : key;
+            }
+          }
+          sc = gsum<32>(sc, 0xffffffffu);
+          key = gmax<32>(key, 0xffffffffu);
+          ext = gsum<32>(ex, 0xffffffffu);
+        }
+        ex = 0;
+        if (lane == cur_r) {
+          my_self = sc;
+          my_key = key;
+          my_ex = ext;
+        }
+        __syncwarp();
+        if (lane == 0) *tcnt = 0;
+        __syncwarp();
+        (void)cur_d;
+      }
+    }
+    if (own >= 0) Op::finish(a, v, own, my_self, my_key, my_ex, acc);
+  }
+}
+
+// Tier 5: one block (256 threads) per row; block-wide shared part table.
+template <class Op, bool UNIT>
+static __device__ void agg_block(const typename Op::Args& a, const GView& g,
+                          const int32_t* __restrict__ parts, const int32_t* __restrict__ list,
+                          int64_t cnt, bool wide, int k, const unsigned long long* __restrict__ dcnt,
+                          unsigned long long* smem, long long& acc) {
+  if (dcnt) cnt = (int64_t)*(const volatile unsigned long long*)dcnt;
+  unsigned long long* tab = smem;
+  int* tl = reinterpret_cast<int*>(tab + k);
+  __shared__ int tcnt;
+  __shared__ long long r_self[32], r_ex[32];
+  __shared__ unsigned long long r_key[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) tab[i] = 0;
+  if (threadIdx.x == 0) tcnt = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x; i < cnt; i += gridDim.x) {
+    const int v = list ? list[i] : (int)i;
+    const int own = parts[v];
+    if (Op::skip(a, v, own)) continue;  // uniform across the block
+    const int64_t b = g.offs[v], e = g.offs[v + 1];
+    long long ex = 0;
+    for (int64_t j0 = b; j0 < e; j0 += blockDim.x) {
+      const int64_t j = j0 + threadIdx.x;
+      int p = -1, w = 0;
+      if (j < e) {
+        p = parts[g.adj[j]];
+        w = UNIT ? 1 : g.ew[j];
+        ex += Op::extra(a, p, w);
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, p);
+      const long long s = UNIT ? (long long)__popc(peers) : peer_sum(peers, w, wide);
+      if (p >= 0 && (__ffs(peers) - 1) == lane) {
+        unsigned long long old = atomicAdd(&tab[p], (unsigned long long)s);
+        if (old == 0) tl[atomicAdd(&tcnt, 1)] = p;
+      }
+    }
+    __syncthreads();
+    const int nt = tcnt;
+    long long self_c = 0;
+    unsigned long long key = 0;
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+      const int p = tl[t];
+      const long long cv = (long long)tab[p];
+      tab[p] = 0;
+      if (p == own) self_c = cv;
+      else if (Op::competes(a, p, own)) {
+        unsigned long long kk = pack_best(cv, p);
+        key = kk > key ? kk : key;
+      }
+    }
+    self_c = gsum<32>(self_c, 0xffffffffu);
+    key = gmax<32>(key, 0xffffffffu);
+    ex = gsum<32>(ex, 0xffffffffu);
+    if (lane == 0) {
+      r_self[wid] = self_c;
+      r_key[wid] = key;
+      r_ex[wid] = ex;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int q = 1; q < (int)(blockDim.x >> 5); ++q) {
+        self_c += r_self[q];
+        key = r_key[q] > key ? r_key[q] : key;
+        ex += r_ex[q];
+      }
+      tcnt = 0;
+      Op::finish(a, v, own, self_c, key, ex, acc);
+    }
+    __syncthreads();
+  }
+}
+
+
+
+// ===========================================================================
+// Reduction-only row kernels: afterburner and apply (cut delta, weights).
+// Rows of a G-tier list are walked by G-lane groups (G = 32 for tiers 4/5).
+// The list length lives on the device (written by the preceding kernel).
+// ===========================================================================
+
+struct RbSegsDev {
+  int64_t b[NBINS];
+};
+
+struct AbArgs {
+  const int32_t* parts;
+  const int32_t* cdest;
+  const long long* F;
+  int32_t* mv;
+  int32_t* move_list;
+  unsigned long long* move_cnt;
+  long long* f2_out;  // optional (parity entry point)
+};
+
+// Segmented vertex lists (one per tier) with device-side lengths.
+struct SegLists {
+  const int32_t* list[NBINS];
+  const unsigned long long* cnt;  // NBINS consecutive counters
+};
+
+// One warp per candidate over all tiers (candidate sets are small).
+template <bool UNIT>
+static __device__ void afterburner_rows(const AbArgs& a, const GView& g, const SegLists& sl,
+                                 const RbSegsDev& mseg, int64_t w0, int64_t ws) {
+  const int lane = threadIdx.x & 31;
+  for (int t = 0; t < NBINS; ++t) {
+    const int64_t cnt = (int64_t)*(const volatile unsigned long long*)(sl.cnt + t);
+    const int32_t* list = sl.list[t];
+    for (int64_t i = w0; i < cnt; i += ws) {
+      const int v = list[i];
+      const int own = a.parts[v];
+      const int dv = a.cdest[v];
+      const long long Fv = a.F[v];
+      const int64_t b = g.offs[v], e = g.offs[v + 1];
+      long long f2 = 0;
+      for (int64_t j = b + lane; j < e; j += 32) {
+        const int u = g.adj[j];
+        int eff = a.parts[u];
+        const int cu = a.cdest[u];
+        if (cu >= 0) {
+          const long long Fu = a.F[u];
+          if (Fu > Fv || (Fu == Fv && u < v)) eff = cu;
+        }
+        const int w = UNIT ? 1 : g.ew[j];
+        f2 += (eff == dv) ? w : (eff == own) ? -w : 0;
+      }
+      f2 = gsum<32>(f2, 0xffffffffu);
+      if (lane == 0) {
+        if (a.f2_out) a.f2_out[v] = f2;
+        if (a.move_list && f2 >= 0) {
+          a.mv[v] = dv;
+          const unsigned long long q = atomicAdd(a.move_cnt + t, 1ull);
+          a.move_list[mseg.b[t] + q] = v;
+        }
+      }
+    }
+  }
+}
+
+struct ApArgs {
+  const int32_t* parts;
+  const int32_t* mv;
+  unsigned long long* pw;
+  unsigned long long* cut2d;
+  int k;
+};
+
+// Exact cut delta of a move batch (conn.py:231-248): for a moved v and
+// neighbour u, c = w([p'(u) != dest] - [p(u) != old]); edges with both ends
+// moved appear twice and are halved, so we sum 2c / c and halve at the end.
+template <bool UNIT>
+static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const SegLists& sl,
+                                 int64_t w0, int64_t ws, long long& acc) {
+  const int lane = threadIdx.x & 31;
+  for (int t = 0; t < NBINS; ++t) {
+    const int64_t cnt = (int64_t)*(const volatile unsigned long long*)(sl.cnt + t);
+    const int32_t* list = sl.list[t];
+    for (int64_t i = w0; i < cnt; i += ws) {
+      const int v = list[i];
+      const int old = a.parts[v];
+      const int dst = a.mv[v];
+      const int64_t b = g.offs[v], e = g.offs[v + 1];
+      long long d = 0;
+      for (int64_t j = b + lane; j < e; j += 32) {
+        const int u = g.adj[j];
+        const int pu = a.parts[u];
+        const int mu = a.mv[u];
+        const int nu = mu >= 0 ? mu : pu;
+        const long long w = UNIT ? 1 : g.ew[j];
+        const long long cc = w * ((long long)(nu != dst) - (long long)(pu != old));
+        d += mu >= 0 ? cc : 2 * cc;
+      }
+      d = gsum<32>(d, 0xffffffffu);
+      if (lane == 0) {
+        acc += d;
+        const unsigned long long wv = (unsigned long long)g.vw[v];
+        atomicAdd(&a.pw[dst], wv);
+        atomicAdd(&a.pw[old], (unsigned long long)(-(long long)wv));
+      }
+    }
+  }
+}
+
+struct CommitArgs {
+  int32_t* parts;
+  int32_t* mv;
+  int32_t* lock;
+  int32_t epoch;
+  int set_lock;
+  const int32_t* lists[NBINS];
+  const unsigned long long* cnts;
+};
+
+static __device__ void apply_commit_rows(const CommitArgs& a, int64_t t0, int64_t stride) {
+  for (int t = 0; t < NBINS; ++t) {
+    const int64_t cnt = (int64_t)*(const volatile unsigned long long*)(a.cnts + t);
+    const int32_t* list = a.lists[t];
+    for (int64_t i = t0; i < cnt; i += stride) {
+      const int v = list[i];
+      a.parts[v] = a.mv[v];
+      a.mv[v] = -1;
+      if (a.set_lock) a.lock[v] = a.epoch;
+    }
+  }
+}
+
+
+template <int BS>
+static __device__ void rb_scan_op(int op, const unsigned long long* __restrict__ H, int nb,
+                           const long long* __restrict__ deficit, int32_t* bstar,
+                           long long* cum_before) {
+  typedef cub::BlockScan<long long, BS> Scan;
+  __shared__ typename Scan::TempStorage ts;
+  __shared__ int s_found;
+  __shared__ long long s_run, s_cb;
+  const unsigned long long* h = H + (size_t)op * nb;
+  const long long D = deficit[op];
+  if (threadIdx.x == 0) {
+    s_found = nb;
+    s_run = 0;
+    s_cb = 0;
+  }
+  __syncthreads();
+  for (int base = 0; base < nb; base += BS) {
+    const int i = base + threadIdx.x;
+    const long long x = i < nb ? (long long)h[i] : 0;
+    long long incl, total;
+    Scan(ts).InclusiveSum(x, incl, total);
+    const long long run = s_run;
+    const long long cum = run + incl;
+    if (i < nb && cum >= D && cum - x < D) {
+      s_found = i;
+      s_cb = cum - x;
+    }
+    __syncthreads();
+    if (s_found < nb) break;
+    if (threadIdx.x == 0) s_run = run + total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    bstar[op] = s_found;
+    cum_before[op] = s_found < nb ? s_cb : s_run;
+  }
+  __syncthreads();
+}
+
+
+
+struct RbSel {
+  const int32_t* parts;
+  const int32_t* vw;
+  const int32_t* opidx;
+  const int32_t* rkey;
+  const int32_t* bstar;
+  const int32_t* thr;
+  int rho;
+  int nch;
+  unsigned long long* CH;
+};
+
+static __device__ void rb_chunk(const RbSel& s, const int32_t* __restrict__ rcand,
+                         const unsigned long long* __restrict__ cnt_ptr, int64_t t0, int64_t nt) {
+  const int64_t cnt = (int64_t)*(const volatile unsigned long long*)cnt_ptr;
+  for (int64_t i = t0; i < cnt; i += nt) {
+    const int v = rcand[i];
+    const int op = s.opidx[s.parts[v]];
+    if (s.rkey[v] != s.bstar[op]) continue;
+    const int ch = (v / s.rho) >> 5;
+    atomicAdd(&s.CH[(size_t)op * s.nch + ch], (unsigned long long)s.vw[v]);
+  }
+}
+
+
+
+// Locate the crossing element of select_prefix (rebalance.py:74-85) inside
+// the crossing bucket, then decide whether it is taken:
+//   take it iff cum[first] - D <= D - cum[first-1]  or  cum[first-1] < required
+// (the min_weight extension of :81-85 always lands on first+1 because
+//  deficit >= required). thr = first id NOT selected inside the bucket.
+template <int BSZ>
+static __device__ void rb_find_op(int op, const RbSel& s, const long long* __restrict__ deficit,
+                           const long long* __restrict__ required,
+                           const long long* __restrict__ cum_before,
+                           const int32_t* __restrict__ opart, int64_t n, int nb, int32_t* thr) {
+  typedef cub::BlockScan<long long, BSZ> BS;
+  __shared__ typename BS::TempStorage ts;
+  __shared__ int s_ch;
+  __shared__ long long s_run, s_cb;
+  const int bs = s.bstar[op];
+  if (bs >= nb) {  // shortfall: every eligible candidate leaves
+    if (threadIdx.x == 0) thr[op] = 0x7fffffff;
+    return;
+  }
+  const long long D = deficit[op];
+  const long long base_cum = cum_before[op];
+  const unsigned long long* ch = s.CH + (size_t)op * s.nch;
+  if (threadIdx.x == 0) {
+    s_ch = -1;
+    s_run = base_cum;
+    s_cb = 0;
+  }
+  __syncthreads();
+  for (int b0 = 0; b0 < s.nch; b0 += BSZ) {
+    const int i = b0 + threadIdx.x;
+    const long long x = i < s.nch ? (long long)ch[i] : 0;
+    long long incl, total;
+    BS(ts).InclusiveSum(x, incl, total);
+    const long long run = s_run;
+    const long long cum = run + incl;
+    if (i < s.nch && cum >= D && cum - x < D) {
+      s_ch = i;
+      s_cb = cum - x;
+    }
+    __syncthreads();
+    if (s_ch >= 0) break;
+    if (threadIdx.x == 0) s_run = run + total;
+    __syncthreads();
+  }
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const int P = opart[op];
+    const int sub = bs % s.rho;
+    const int64_t j = (int64_t)s_ch * 32 + lane;
+    const int64_t v64 = j * s.rho + sub;
+    long long w = 0;
+    if (s_ch >= 0 && v64 < n) {
+      const int v = (int)v64;
+      if (s.parts[v] == P && s.rkey[v] == bs) w = s.vw[v];
+    }
+    long long incl = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const long long cum = s_cb + incl;
+    const bool hit = w > 0 && cum >= D && cum - w < D;
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (m && lane == __ffs(m) - 1) {
+      const long long prev = cum - w;
+      const long long req = required[op];
+      const bool include = (cum - D <= D - prev) || (prev < req);
+      thr[op] = (int)v64 + (include ? 1 : 0);
+    }
+    if (!m && lane == 0) thr[op] = 0x7fffffff;  // unreachable by construction
+  }
+}
+
+
+
+// Selected iff (bucket, id) < the part's threshold (select_prefix). Weak
+// passes with direct=1 commit vertices that have a valid destination right
+// away (their order is unobservable); everything else (weak: vertices that
+// need a random destination; strong: all) goes to the evict list.
+
+// ---- warp-level selection helpers: one warp per oversized part, so all
+// parts proceed in parallel whatever the grid size (the persistent level
+// kernel runs small levels on a handful of blocks).
+
+// First index i of arr[0, len) where run + prefix_sum(arr)[i] >= D; *before =
+// run + prefix before i. Returns -1 (and *before = run + total) if never.
+static __device__ __forceinline__ int warp_cross(const unsigned long long* __restrict__ arr, int len,
+                                                 long long D, long long run, long long* before) {
+  const int lane = threadIdx.x & 31;
+  for (int b0 = 0; b0 < len; b0 += 32) {
+    const int i = b0 + lane;
+    const long long x = i < len ? (long long)arr[i] : 0;
+    long long incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const long long cum = run + incl;
+    const unsigned m = __ballot_sync(0xffffffffu, i < len && cum >= D && cum - x < D);
+    if (m) {
+      const int l = __ffs(m) - 1;
+      *before = __shfl_sync(0xffffffffu, cum - x, l);
+      return b0 + l;
+    }
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  *before = run;
+  return -1;
+}
+
+// bucket crossing (select_prefix on bucket totals): the crossing slot from
+// the per-slot totals, then the crossing sub-bucket inside that slot
+static __device__ void rb_scan_warp(int op, const unsigned long long* __restrict__ H,
+                                    const unsigned long long* __restrict__ Hs, int nb, int rho,
+                                    const long long* __restrict__ deficit, int32_t* bstar,
+                                    long long* cum_before) {
+  const int ns = nb / rho;
+  const long long D = deficit[op];
+  long long before;
+  int b = nb;
+  const int sl = warp_cross(Hs + (size_t)op * ns, ns, D, 0, &before);
+  if (sl >= 0) {
+    long long b2;
+    const int sb = warp_cross(H + (size_t)op * nb + (size_t)sl * rho, rho, D, before, &b2);
+    b = sl * rho + sb;  // sb >= 0: the slot total crosses, so one of its buckets does
+    before = b2;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    bstar[op] = b;
+    cum_before[op] = before;
+  }
+}
+
+// crossing chunk, then the crossing element inside it (see rb_find_op)
+static __device__ void rb_find_warp(int op, const RbSel& s, const long long* __restrict__ deficit,
+                                    const long long* __restrict__ required,
+                                    const long long* __restrict__ cum_before,
+                                    const int32_t* __restrict__ opart, int64_t n, int nb,
+                                    int32_t* thr) {
+  const int lane = threadIdx.x & 31;
+  const int bs = s.bstar[op];
+  if (bs >= nb) {  // shortfall: every eligible candidate leaves
+    if (lane == 0) thr[op] = 0x7fffffff;
+    return;
+  }
+  const long long D = deficit[op];
+  long long cb;
+  const int ch = warp_cross(s.CH + (size_t)op * s.nch, s.nch, D, cum_before[op], &cb);
+  const int P = opart[op];
+  const int sub = bs % s.rho;
+  const int64_t j = (int64_t)ch * 32 + lane;
+  const int64_t v64 = j * s.rho + sub;
+  long long w = 0;
+  if (ch >= 0 && v64 < n) {
+    const int v = (int)v64;
+    if (s.parts[v] == P && s.rkey[v] == bs) w = s.vw[v];
+  }
+  long long incl = w;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const long long cum = cb + incl;
+  const unsigned m = __ballot_sync(0xffffffffu, w > 0 && cum >= D && cum - w < D);
+  if (m && lane == __ffs(m) - 1) {
+    const long long prev = cum - w;
+    const bool include = (cum - D <= D - prev) || (prev < required[op]);
+    thr[op] = (int)v64 + (include ? 1 : 0);
+  }
+  if (!m && lane == 0) thr[op] = 0x7fffffff;  // unreachable by construction
+}
+
+static __device__ void rb_select(const RbSel& s, const int32_t* __restrict__ rcand,
+                          const unsigned long long* __restrict__ cnt_ptr,
+                          const int32_t* __restrict__ rbest, int strong, int direct,
+                          int32_t* evict, unsigned long long* evict_cnt, int32_t* mv,
+                          const int64_t* __restrict__ offs, TierMap tm, int32_t* move_lists,
+                          RbSegsDev mseg, unsigned long long* move_cnt, int64_t t0, int64_t nt) {
+  const int64_t cnt = (int64_t)*(const volatile unsigned long long*)cnt_ptr;
+  const int64_t lim = (cnt + 31) / 32 * 32;
+  for (int64_t i = t0; i < lim; i += nt) {
+    bool sel = false, now = false;
+    int v = 0, t = -1;
+    if (i < cnt) {
+      v = rcand[i];
+      const int op = s.opidx[s.parts[v]];
+      const int rk = s.rkey[v];
+      const int bs = s.bstar[op];
+      sel = rk < bs || (rk == bs && v < s.thr[op]);
+      if (sel && !strong && direct) {
+        const int bp = rbest[v];
+        if (bp >= 0) {
+          now = true;
+          mv[v] = bp;
+          t = tm(offs[v + 1] - offs[v]);
+        }
+      }
+    }
+    warp_append(sel && !now, v, evict, evict_cnt);
+    for (int tt = 0; tt < NBINS; ++tt)
+      warp_append(t == tt, v, move_lists + mseg.b[tt], move_cnt + tt);
+  }
+}
+
+
+
+// Collect the vertices of oversized parts into per-tier candidate lists.
+
+
+// Single-block tail for small evicted sets (length read on device, bounded
+// on the host by sum(deficit) <= cap): bitonic sort of (part, bucket, id)
+// keys in shared memory, then weak: valid[draw[i]] in order; strong:
+// next-fit (rebalance.py:224-236); then commit the moves.
+struct RbTail {
+  const int32_t* evict;
+  const unsigned long long* evict_cnt;
+  const int32_t* parts;
+  const int32_t* opidx;
+  const int32_t* rkey;
+  const int32_t* vw;
+  const int64_t* offs;
+  TierMap tm;
+  const int32_t* valid_list;
+  const int32_t* draws;
+  const long long* spare;
+  int nvalid;
+  int nb;
+  int strong;
+  int32_t* mv;
+  int32_t* move_lists;
+  RbSegsDev mseg;
+  unsigned long long* move_cnt;
+  int smem_cap;                     // keys that fit the caller's shared buffer
+  unsigned long long* gscratch;     // >= 2 * P2 + blockDim words, for larger sets
+};
+
+static __device__ void rb_tail(const RbTail& a, unsigned long long* sk_smem) {
+  __shared__ long long s_room;
+  __shared__ int s_di, s_done;
+  __shared__ long long s_wsum[32];
+  const int tid = threadIdx.x;
+  const int L = (int)*(const volatile unsigned long long*)a.evict_cnt;
+  int P2 = 1;
+  while (P2 < L) P2 <<= 1;
+  unsigned long long* sk = (P2 <= a.smem_cap || a.gscratch == nullptr) ? sk_smem : a.gscratch;
+  for (int i = tid; i < P2; i += blockDim.x) {
+    unsigned long long key = ~0ull;
+    if (i < L) {
+      const int v = a.evict[i];
+      const unsigned long long grp =
+          (unsigned long long)a.opidx[a.parts[v]] * (unsigned)a.nb + (unsigned)a.rkey[v];
+      key = (grp << 32) | (unsigned)v;
+    }
+    sk[i] = key;
+  }
+  __syncthreads();
+  for (int size = 2; size <= P2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < P2; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool asc = (i & size) == 0;
+          const unsigned long long x = sk[i], y = sk[j];
+          if ((x > y) == asc) {
+            sk[i] = y;
+            sk[j] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (!a.strong) {
+    for (int i = tid; i < L; i += blockDim.x) {
+      const int v = (int)(sk[i] & 0xffffffffu);
+      a.mv[v] = a.valid_list[a.draws[i]];
+      const int t = a.tm(a.offs[v + 1] - a.offs[v]);
+      const unsigned long long q = atomicAdd(a.move_cnt + t, 1ull);
+      a.move_lists[a.mseg.b[t] + q] = v;
+    }
+    return;
+  }
+  // next-fit; sequential over runs but each run is a parallel prefix test
+  if (tid == 0) {
+    s_di = 0;
+    s_room = a.nvalid > 0 ? a.spare[0] : 0;
+    s_done = a.nvalid <= 0;
+  }
+  __syncthreads();
+  for (int base = 0; base < L; base += blockDim.x) {
+    const int i = base + tid;
+    const long long w = i < L ? (long long)a.vw[(int)(sk[i] & 0xffffffffu)] : 0;
+    // block inclusive scan of w
+    long long ps = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, ps, o);
+      if ((tid & 31) >= o) ps += y;
+    }
+    if ((tid & 31) == 31) s_wsum[tid >> 5] = ps;
+    __syncthreads();
+    if (tid < 32) {
+      long long x = s_wsum[tid];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (tid >= o) x += y;
+      }
+      s_wsum[tid] = x;
+    }
+    __syncthreads();
+    if (tid >= 32) ps += s_wsum[(tid >> 5) - 1];
+    const int lim = L - base < (int)blockDim.x ? L - base : (int)blockDim.x;
+    // stash inclusive sums in the (already consumed) key slots' upper half:
+    // keep them in a dedicated region after the keys instead
+    long long* pbuf = reinterpret_cast<long long*>(sk + P2);
+    pbuf[tid] = ps;
+    __syncthreads();
+    int pos = 0;
+    long long before = 0;
+    while (true) {
+      if (s_done) break;
+      const long long room = s_room;
+      const bool fits = tid >= pos && tid < lim && ps - before <= room;
+      __shared__ int s_first;
+      if (tid == 0) s_first = lim;
+      __syncthreads();
+      if (tid >= pos && tid < lim && !fits) atomicMin(&s_first, tid);
+      __syncthreads();
+      const int e = s_first;
+      if (fits) {
+        const int v = (int)(sk[i] & 0xffffffffu);
+        a.mv[v] = a.valid_list[s_di];
+        const int t = a.tm(a.offs[v + 1] - a.offs[v]);
+        const unsigned long long q = atomicAdd(a.move_cnt + t, 1ull);
+        a.move_lists[a.mseg.b[t] + q] = v;
+      }
+      __syncthreads();
+      if (e >= lim) {
+        if (tid == 0) s_room = room - (pbuf[lim - 1] - before);
+        __syncthreads();
+        break;
+      }
+      if (tid == 0) {
+        const long long prev = e > 0 ? pbuf[e - 1] : 0;
+        long long r = room - (prev - before);
+        const long long we = pbuf[e] - prev;
+        int di = s_di;
+        while (di < a.nvalid && r < we) {
+          di++;
+          r = di < a.nvalid ? a.spare[di] : 0;
+        }
+        s_di = di;
+        s_room = r;
+        if (di >= a.nvalid) s_done = 1;
+      }
+      __syncthreads();
+      pos = e;
+      before = e > 0 ? pbuf[e - 1] : 0;
+    }
+    __syncthreads();
+    if (s_done) break;
+  }
+}
+
+
+
+
+static __device__ void rb_collect(const int32_t* __restrict__ parts, const int32_t* __restrict__ opidx,
+                           const int64_t* __restrict__ offs, TierMap tm, int64_t n, int32_t* lists,
+                           RbSegsDev seg, unsigned long long* cnts, int64_t t0, int64_t stride) {
+  const int64_t lim = (n + 31) / 32 * 32;
+  for (int64_t v = t0; v < lim; v += stride) {
+    int t = -1;
+    if (v < n && opidx[parts[v]] >= 0) t = tm(offs[v + 1] - offs[v]);
+    if (__ballot_sync(0xffffffffu, t >= 0) == 0) continue;
+    for (int tt = 0; tt < NBINS; ++tt) warp_append(t == tt, (int32_t)v, lists + seg.b[tt], cnts + tt);
+  }
+}
+
+}  // namespace jet
