@@ -248,9 +248,12 @@ inline void dzero(Ctx& c, T* dst, size_t count) {
 // Warp-group helpers (groups of G lanes, G | 32, aligned).
 template <int G>
 __device__ __forceinline__ unsigned group_mask() {
-  if (G == 32) return 0xffffffffu;
-  const unsigned lane = threadIdx.x & 31u;
-  return ((1u << G) - 1u) << (lane & ~(unsigned)(G - 1));
+  if constexpr (G == 32) {
+    return 0xffffffffu;
+  } else {
+    const unsigned lane = threadIdx.x & 31u;
+    return ((1u << G) - 1u) << (lane & ~(unsigned)(G - 1));
+  }
 }
 template <int G, class T>
 __device__ __forceinline__ T gsum(T x, unsigned m) {

@@ -30,6 +30,7 @@ constexpr int LV_BLOCK = 512;
 constexpr int LV_TAIL_SMEM = 8192;  // evicted keys sorted in shared memory
 constexpr int LV_DRAW_SLACK = 64;
 constexpr int64_t LV_ROWS_PER_BLOCK = 512;
+constexpr int LV_RB = 16;  // rows per warp batch in the staged short-row sweep
 
 struct LevelCtl {
   long long cut, best_cut, keep_cut, keep_worst;
@@ -100,6 +101,7 @@ struct LevelArgs {
   long long* trace;  // optional: 6 values per iteration (JET_TRACE)
   int trace_cap;
   unsigned long long* phase_clk;  // optional: clock64 per phase (JET_PHASES)
+  unsigned long long* work;       // {stats rows, entries, ab rows, entries, apply rows, entries}
 };
 
 // phase timer for block 0 / thread 0 (diagnostics only)
@@ -372,15 +374,19 @@ __device__ void lv_sweep(const LevelArgs& A, MakeArgs mk, const int32_t* const* 
 #pragma unroll 1
   for (int t = 0; t < NBINS; ++t) {
     if (A.tcnt[t] == 0) continue;
+    // tiers share one shared-memory union (stages / warp tables / block table)
+    __syncthreads();
     const typename Op::Args a = mk(t);
     const int32_t* list = lists ? lists[t] : A.tlist[t];
     const unsigned long long* dc = dcnts ? dcnts + t : nullptr;
     const int64_t cnt = A.tcnt[t];
+    uint32_t* stg = reinterpret_cast<uint32_t*>(smem) +
+                    (threadIdx.x >> 5) * stage_words<32, LV_RB, UNIT>();
     switch (t) {
-      case 0: agg_small<Op, 4, UNIT>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc); break;
-      case 1: agg_small<Op, 8, UNIT>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc); break;
-      case 2: agg_small<Op, 16, UNIT>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc); break;
-      case 3: agg_small<Op, 32, UNIT>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc); break;
+      case 0: agg_small<Op, 4, UNIT, LV_RB>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc, stg); break;
+      case 1: agg_small<Op, 8, UNIT, LV_RB>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc, stg); break;
+      case 2: agg_small<Op, 16, UNIT, LV_RB>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc, stg); break;
+      case 3: agg_small<Op, 32, UNIT, LV_RB>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc, stg); break;
       case 4: {
         const size_t per = (size_t)A.k + (size_t)(A.tl_cap + 3) / 2;
         agg_warp<Op, UNIT>(a, A.g, A.parts, list, cnt, wide, A.k, A.tl_cap, dc,
@@ -389,12 +395,11 @@ __device__ void lv_sweep(const LevelArgs& A, MakeArgs mk, const int32_t* const* 
         break;
       }
       default:
-        __syncthreads();
         agg_block<Op, UNIT>(a, A.g, A.parts, list, cnt, wide, A.k, dc, smem, acc);
-        __syncthreads();
         break;
     }
   }
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------- kernel
@@ -463,7 +468,7 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_level(LevelArgs A) {
         ab.mv = A.mv;
         ab.move_list = A.move_lists;
         ab.move_cnt = A.ctr + CTR_MOVE;
-        afterburner_rows<UNIT>(ab, A.g, cands, A.seg, w0, nw);
+        afterburner_rows<UNIT>(ab, A.g, cands, A.seg, w0, nw, A.work + 2);
         grid.sync();
         pc.mark(2);
       }
@@ -475,7 +480,8 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_level(LevelArgs A) {
       for (int64_t i = t0; i < (int64_t)nover * (nb / ldv(&C->rho)); i += nt) A.Hs[i] = 0;
       for (int64_t i = t0; i < (int64_t)nover * nch; i += nt) A.CH[i] = 0;
       if (!strong) lv_draws(A, t0, nt);
-      rb_collect(A.parts, A.opidx, A.g.offs, A.tm, A.n, A.cand_lists, A.seg, A.ctr + CTR_CAND, t0, nt);
+      rb_collect(A.parts, A.opidx, A.g.offs, A.tm, A.n, A.cand_lists, A.seg, A.ctr + CTR_CAND, t0, nt,
+                 A.work);
       grid.sync();
       pc.mark(3);
       RbOp::Args ra{};
@@ -551,7 +557,7 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_level(LevelArgs A) {
     {
       ApArgs ap{A.parts, A.mv, A.ctr + CTR_PW, A.ctr + CTR_CUT2D, A.k};
       long long d = 0;
-      apply_delta_rows<UNIT>(ap, A.g, moves, w0, nw, d);
+      apply_delta_rows<UNIT>(ap, A.g, moves, w0, nw, d, A.work + 4);
       block_sum_atomic_any(d, A.ctr + CTR_CUT2D);
     }
     grid.sync();
@@ -590,6 +596,7 @@ struct LevelScratch {
   DBuf<long long> keep_pw;
   DBuf<int32_t> backup;
   DBuf<unsigned long long> gscratch;
+  DBuf<unsigned long long> work;
 };
 
 static LevelScratch& level_scratch(Ctx& c) {
@@ -606,6 +613,7 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   const int tl_cap = (int)std::min<int64_t>(k, WARP_TIER_MAX_DEG);
   const size_t per = ((size_t)k + (size_t)(tl_cap + 3) / 2) * 8;
   size_t smem = (size_t)LV_TAIL_SMEM * 8 + LV_BLOCK * 8;
+  smem = std::max(smem, (size_t)(LV_BLOCK / 32) * stage_words<32, LV_RB, false>() * 4);
   if (g.bin_cnt[BIN_WARP]) smem = std::max(smem, per * (LV_BLOCK / 32));
   if (g.bin_cnt[BIN_BLOCK]) smem = std::max(smem, (size_t)k * 12);
   if (smem > (size_t)c.max_smem_optin) return false;
@@ -617,6 +625,8 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   S.keep_pw.ensure(k, c.stream);
   S.backup.ensure(g.n, c.stream);
   S.gscratch.ensure(2 * (size_t)g.n + 2 * LV_BLOCK + 64, c.stream);
+  S.work.ensure(8, c.stream);
+  dzero(c, S.work.get(), 8);
   keep.ensure(g.n, c.stream);
   const int slot_span = 34 + std::max(0, ceil_log2_host(k) - 1);
   const int64_t nb_max = (int64_t)slot_span * rho;
@@ -717,6 +727,7 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   A.CH_cap = (int64_t)w.CH.n;
   A.draws_cap = (int64_t)w.draws.n;
   A.C = S.ctl.get();
+  A.work = S.work.get();
 
   static const bool trace_on = getenv("JET_TRACE") && getenv("JET_TRACE")[0] == '1';
   DBuf<long long> trace;
@@ -746,6 +757,8 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
     CK(cudaLaunchCooperativeKernel(kern, dim3(blocks), dim3(LV_BLOCK), args, smem, c.stream));
   });
   d2h(c, &h, S.ctl.get(), 1);
+  unsigned long long wk[8];
+  d2h(c, wk, S.work.get(), 8);
   w.h_pw.resize(k);
   d2h(c, w.h_pw.data(), (int64_t*)S.keep_pw.get(), k);
   c.sync();
@@ -770,6 +783,18 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
     return false;
   }
   c.lock_epoch = h.epoch + 1;
+  if (c.prof && !c.recs.empty() && c.recs.back().cls == c.prof_class("refine_level")) {
+    // algorithmic bytes of the launch (roofline accounting)
+    const double ebytes = g.unit_ew ? 8.0 : 12.0;  // adj + neighbour part (+ weight)
+    const double list = g.identity ? 0.0 : 4.0;
+    const double lp_pass = (double)g.n * (8 + 4 + 4 + 4 + list) + (double)g.nnz * ebytes;
+    const double reb_pass = (double)g.n * (4 + 8);  // collect: parts + offsets
+    double b = h.lp * lp_pass + (h.weak + h.strong) * reb_pass;
+    b += (double)wk[0] * (4 + 8 + 4 + 16) + (double)wk[1] * ebytes;            // rb stats
+    b += (double)wk[2] * (4 + 8 + 4 + 4 + 8) + (double)wk[3] * (ebytes + 12);  // afterburner
+    b += (double)wk[4] * (4 + 8 + 4 + 4 + 4 + 16) + (double)wk[5] * (ebytes + 4);  // apply
+    c.recs.back().bytes = b;
+  }
   if (trace_on) {
     std::vector<long long> t(6 * std::min(h.iterations, 4096));
     d2h(c, t.data(), trace.get(), t.size());

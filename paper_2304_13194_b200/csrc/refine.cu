@@ -25,11 +25,25 @@ __global__ void __launch_bounds__(256)
     k_agg_small(typename Op::Args a, GView g, const int32_t* __restrict__ parts,
                 const int32_t* __restrict__ list, int64_t cnt, bool wide,
                 const unsigned long long* __restrict__ dcnt) {
+  extern __shared__ uint32_t agg_stage[];
   long long acc = 0;
   agg_small<Op, G, UNIT>(a, g, parts, list, cnt, wide, dcnt,
                          (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5,
-                         ((int64_t)gridDim.x * blockDim.x) >> 5, acc);
+                         ((int64_t)gridDim.x * blockDim.x) >> 5, acc,
+                         agg_stage + (threadIdx.x >> 5) * stage_words<G, 32, UNIT>());
   Op::block_done(a, acc);
+}
+
+// dynamic shared memory of k_agg_small<Op, G, UNIT> (8 warps), set once
+template <class Op, int G, bool UNIT>
+static size_t agg_small_smem() {
+  static const size_t bytes = [] {
+    const size_t b = (size_t)8 * stage_words<G, 32, UNIT>() * 4;
+    CK(cudaFuncSetAttribute(k_agg_small<Op, G, UNIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)b));
+    return b;
+  }();
+  return bytes;
 }
 
 template <class Op, bool UNIT>
@@ -95,17 +109,17 @@ static void run_agg(Ctx& c, const DGraph& g, MakeArgs mk, const int32_t* parts,
 #define AGG_K(GG, UU) k_agg_small<Op, GG, UU>
         if (g.unit_ew) {
           switch (G) {
-            case 4: AGG_K(4, true)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
-            case 8: AGG_K(8, true)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
-            case 16: AGG_K(16, true)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
-            default: AGG_K(32, true)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
+            case 4: AGG_K(4, true)<<<grid, 256, agg_small_smem<Op, 4, true>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
+            case 8: AGG_K(8, true)<<<grid, 256, agg_small_smem<Op, 8, true>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
+            case 16: AGG_K(16, true)<<<grid, 256, agg_small_smem<Op, 16, true>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
+            default: AGG_K(32, true)<<<grid, 256, agg_small_smem<Op, 32, true>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
           }
         } else {
           switch (G) {
-            case 4: AGG_K(4, false)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
-            case 8: AGG_K(8, false)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
-            case 16: AGG_K(16, false)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
-            default: AGG_K(32, false)<<<grid, 256, 0, c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
+            case 4: AGG_K(4, false)<<<grid, 256, agg_small_smem<Op, 4, false>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
+            case 8: AGG_K(8, false)<<<grid, 256, agg_small_smem<Op, 8, false>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
+            case 16: AGG_K(16, false)<<<grid, 256, agg_small_smem<Op, 16, false>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
+            default: AGG_K(32, false)<<<grid, 256, agg_small_smem<Op, 32, false>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
           }
         }
 #undef AGG_K

@@ -152,27 +152,48 @@ struct RbOp {
   static __device__ __forceinline__ void block_done(const Args&, long long) {}
 };
 
-// Tiers 0-3. A warp owns 32 consecutive list entries: vertex ids, offsets
-// and own parts are loaded once, coalesced. Rows are then swept in G steps
-// of 32/G rows (one G-lane group per row); U steps are batched so their
-// adjacency loads and neighbour-part gathers are all in flight together
-// (the single-row-per-warp form is latency-bound at ~300 GB/s). The result
-// of row r is shuffled to lane r, which finishes vertex r.
-template <class Op, int G, bool UNIT>
+// ---- asynchronous global->shared copies (LDGSTS) ----------------------------
+static __device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+static __device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;\n" ::: "memory");
+}
+
+// Per-warp staging words of the short-row sweep (adjacency, parts, weights).
+template <int G, int RB, bool UNIT>
+__host__ __device__ constexpr int stage_words() {
+  return RB * G * (UNIT ? 2 : 3);
+}
+
+// Tiers 0-3 (rows of <= G entries). A warp owns R <= RB consecutive list
+// entries; their ids, offsets and own parts are loaded once, coalesced. The
+// rows' adjacency (+weights) is then copied into shared memory with
+// fire-and-forget cp.async (one 4-byte copy per entry, all in flight at
+// once), and the neighbour parts are gathered the same way, addressed from
+// the staged adjacency. Only then are the rows aggregated, G lanes per row,
+// from shared memory: three memory round trips per batch of rows instead of
+// a dependent load chain per row. Row r's result is shuffled to lane r.
+template <class Op, int G, bool UNIT, int RB = 32>
 static __device__ __forceinline__ void agg_small(const typename Op::Args& a, const GView& g,
-                                          const int32_t* __restrict__ parts,
-                                          const int32_t* __restrict__ list, int64_t cnt,
-                                          bool wide, const unsigned long long* __restrict__ dcnt,
-                                          int64_t w0, int64_t nw, long long& acc) {
+                                                 const int32_t* __restrict__ parts,
+                                                 const int32_t* __restrict__ list, int64_t cnt,
+                                                 bool wide,
+                                                 const unsigned long long* __restrict__ dcnt,
+                                                 int64_t w0, int64_t nw, long long& acc,
+                                                 uint32_t* stage) {
   if (dcnt) cnt = (int64_t)*(const volatile unsigned long long*)dcnt;
-  constexpr int RPS = 32 / G;         // rows per step
-  constexpr int U = G >= 8 ? 8 : G;   // steps per batch (G steps in total)
+  constexpr int RPS = 32 / G;  // rows per step
   const unsigned gm = group_mask<G>();
   const int lane = threadIdx.x & 31, gl = lane & (G - 1), grp = lane / G;
-  // rows per warp batch: 32 when there is plenty of work, fewer for small
-  // lists so every warp gets rows (latency, not bandwidth, rules there)
+  int* s_adj = reinterpret_cast<int*>(stage);
+  int* s_p = s_adj + RB * G;
+  int* s_w = s_p + RB * G;
+  // rows per batch: RB when there is plenty of work, fewer for small lists
+  // so every warp gets rows (latency, not bandwidth, rules there)
   const int64_t per_w = (cnt + nw - 1) / nw;
-  const int R = per_w >= 32 ? 32 : (per_w < 1 ? 1 : (int)per_w);
+  const int R = per_w >= RB ? RB : (per_w < 1 ? 1 : (int)per_w);
   for (int64_t base = w0 * R; base < cnt; base += nw * R) {
     const int64_t idx = base + lane;
     int v = 0, own = -1, deg = 0;
@@ -187,74 +208,78 @@ static __device__ __forceinline__ void agg_small(const typename Op::Args& a, con
         deg = (int)(g.offs[v + 1] - beg);
       }
     }
+    // stage adjacency (+ weights)
+    for (int st = 0; st * RPS < R; ++st) {
+      const int r = st * RPS + grp;
+      const int64_t rb = __shfl_sync(0xffffffffu, beg, r & 31);
+      const int rd = __shfl_sync(0xffffffffu, deg, r & 31);
+      if (r < R && gl < rd) {
+        cp_async4(&s_adj[r * G + gl], g.adj + rb + gl);
+        if (!UNIT) cp_async4(&s_w[r * G + gl], g.ew + rb + gl);
+      }
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    // gather neighbour parts
+    for (int st = 0; st * RPS < R; ++st) {
+      const int r = st * RPS + grp;
+      const int rd = __shfl_sync(0xffffffffu, deg, r & 31);
+      if (r < R && gl < rd) cp_async4(&s_p[r * G + gl], parts + s_adj[r * G + gl]);
+    }
+    cp_async_wait_all();
+    __syncwarp();
     long long my_self = 0, my_ex = 0;
     unsigned long long my_key = 0;
-#pragma unroll
-    for (int s0 = 0; s0 < G; s0 += U) {
-      if (s0 * RPS >= R) break;  // remaining steps hold no rows
-      int uu[U], ww[U], pp[U];
-#pragma unroll
-      for (int q = 0; q < U; ++q) {
-        const int r = (s0 + q) * RPS + grp;
-        const int64_t rb = __shfl_sync(0xffffffffu, beg, r);
-        const int rd = __shfl_sync(0xffffffffu, deg, r);
-        uu[q] = -1;
-        ww[q] = 0;
-        if (gl < rd) {
-          uu[q] = g.adj[rb + gl];
-          ww[q] = UNIT ? 1 : g.ew[rb + gl];
-        }
+    for (int st = 0; st * RPS < R; ++st) {
+      const int r = st * RPS + grp;
+      const int rd = __shfl_sync(0xffffffffu, deg, r & 31);
+      const int rown = __shfl_sync(0xffffffffu, own, r & 31);
+      int p = -1, w = 0;
+      if (r < R && gl < rd) {
+        p = s_p[r * G + gl];
+        w = UNIT ? 1 : s_w[r * G + gl];
       }
-#pragma unroll
-      for (int q = 0; q < U; ++q) pp[q] = uu[q] >= 0 ? parts[uu[q]] : -1;
-#pragma unroll
-      for (int q = 0; q < U; ++q) {
-        const int st = s0 + q;
-        const int rown = __shfl_sync(0xffffffffu, own, st * RPS + grp);
-        const int p = pp[q];
-        const unsigned peers = __match_any_sync(gm, p);
-        const bool comp = p >= 0 && p != rown && Op::competes(a, p, rown);
-        const int src = ((lane - st * RPS) & (RPS - 1)) * G;
-        if (!wide) {
-          // 32-bit sums (weighted degree < 2^31): single-instruction REDUX
-          // reductions; best part = max conn, then lowest part id
-          const unsigned sm =
-              UNIT ? (unsigned)__popc(peers) : __reduce_add_sync(peers, (unsigned)ww[q]);
-          const unsigned sc =
-              UNIT ? (unsigned)__popc(__ballot_sync(gm, p >= 0 && p == rown))
-                   : __reduce_add_sync(gm, (p >= 0 && p == rown) ? (unsigned)ww[q] : 0u);
-          const unsigned mx = __reduce_max_sync(gm, comp ? sm : 0u);
-          const unsigned pm = __reduce_min_sync(gm, (comp && sm == mx) ? (unsigned)p : 0xffffffffu);
-          const unsigned ex = __reduce_add_sync(gm, p >= 0 ? (unsigned)Op::extra(a, p, ww[q]) : 0u);
-          const unsigned dsc = __shfl_sync(0xffffffffu, sc, src);
-          const unsigned dmx = __shfl_sync(0xffffffffu, mx, src);
-          const unsigned dpm = __shfl_sync(0xffffffffu, pm, src);
-          const unsigned dex = __shfl_sync(0xffffffffu, ex, src);
-          if (lane / RPS == st) {
-            my_self = dsc;
-            my_key = dmx ? pack_best((long long)dmx, (int)dpm) : 0ull;
-            my_ex = dex;
-          }
-        } else {
-          const long long sm = UNIT ? (long long)__popc(peers) : peer_sum(peers, ww[q], wide);
-          const bool lead = p >= 0 && (__ffs(peers) - 1) == lane;
-          long long sc = (lead && p == rown) ? sm : 0;
-          unsigned long long key = (lead && comp) ? pack_best(sm, p) : 0ull;
-          long long ex = p >= 0 ? Op::extra(a, p, ww[q]) : 0;
-          sc = gsum<G>(sc, gm);
-          key = gmax<G>(key, gm);
-          ex = gsum<G>(ex, gm);
-          sc = __shfl_sync(0xffffffffu, sc, src);
-          key = __shfl_sync(0xffffffffu, key, src);
-          ex = __shfl_sync(0xffffffffu, ex, src);
-          if (lane / RPS == st) {
-            my_self = sc;
-            my_key = key;
-            my_ex = ex;
-          }
+      const unsigned peers = __match_any_sync(gm, p);
+      const bool comp = p >= 0 && p != rown && Op::competes(a, p, rown);
+      const int src = ((lane - st * RPS) & (RPS - 1)) * G;
+      if (!wide) {
+        // 32-bit sums (weighted degree < 2^31): single-instruction REDUX
+        // reductions; best part = max conn, then lowest part id
+        const unsigned sm = UNIT ? (unsigned)__popc(peers) : __reduce_add_sync(peers, (unsigned)w);
+        const unsigned sc = UNIT ? (unsigned)__popc(__ballot_sync(gm, p >= 0 && p == rown))
+                                 : __reduce_add_sync(gm, (p >= 0 && p == rown) ? (unsigned)w : 0u);
+        const unsigned mx = __reduce_max_sync(gm, comp ? sm : 0u);
+        const unsigned pm = __reduce_min_sync(gm, (comp && sm == mx) ? (unsigned)p : 0xffffffffu);
+        const unsigned ex = __reduce_add_sync(gm, p >= 0 ? (unsigned)Op::extra(a, p, w) : 0u);
+        const unsigned dsc = __shfl_sync(0xffffffffu, sc, src);
+        const unsigned dmx = __shfl_sync(0xffffffffu, mx, src);
+        const unsigned dpm = __shfl_sync(0xffffffffu, pm, src);
+        const unsigned dex = __shfl_sync(0xffffffffu, ex, src);
+        if (lane / RPS == st) {
+          my_self = dsc;
+          my_key = dmx ? pack_best((long long)dmx, (int)dpm) : 0ull;
+          my_ex = dex;
+        }
+      } else {
+        const long long sm = UNIT ? (long long)__popc(peers) : peer_sum(peers, w, wide);
+        const bool lead = p >= 0 && (__ffs(peers) - 1) == lane;
+        long long sc = (lead && p == rown) ? sm : 0;
+        unsigned long long key = (lead && comp) ? pack_best(sm, p) : 0ull;
+        long long ex = p >= 0 ? Op::extra(a, p, w) : 0;
+        sc = gsum<G>(sc, gm);
+        key = gmax<G>(key, gm);
+        ex = gsum<G>(ex, gm);
+        sc = __shfl_sync(0xffffffffu, sc, src);
+        key = __shfl_sync(0xffffffffu, key, src);
+        ex = __shfl_sync(0xffffffffu, ex, src);
+        if (lane / RPS == st) {
+          my_self = sc;
+          my_key = key;
+          my_ex = ex;
         }
       }
     }
+    __syncwarp();  // the next batch reuses the stage
     if (own >= 0) Op::finish(a, v, own, my_self, my_key, my_ex, acc);
   }
 }
@@ -507,9 +532,12 @@ struct SegLists {
 
 // One warp per candidate over all tiers (candidate sets are small).
 template <bool UNIT>
+// work (optional): += {rows, entries} visited, for the roofline accounting
 static __device__ void afterburner_rows(const AbArgs& a, const GView& g, const SegLists& sl,
-                                 const RbSegsDev& mseg, int64_t w0, int64_t ws) {
+                                 const RbSegsDev& mseg, int64_t w0, int64_t ws,
+                                 unsigned long long* work = nullptr) {
   const int lane = threadIdx.x & 31;
+  unsigned long long wr = 0, we = 0;
   for (int t = 0; t < NBINS; ++t) {
     const int64_t cnt = (int64_t)*(const volatile unsigned long long*)(sl.cnt + t);
     const int32_t* list = sl.list[t];
@@ -519,6 +547,8 @@ static __device__ void afterburner_rows(const AbArgs& a, const GView& g, const S
       const int dv = a.cdest[v];
       const long long Fv = a.F[v];
       const int64_t b = g.offs[v], e = g.offs[v + 1];
+      wr += 1;
+      we += (unsigned long long)(e - b);
       long long f2 = 0;
       for (int64_t j = b + lane; j < e; j += 32) {
         const int u = g.adj[j];
@@ -542,6 +572,10 @@ static __device__ void afterburner_rows(const AbArgs& a, const GView& g, const S
       }
     }
   }
+  if (work && lane == 0 && wr) {
+    atomicAdd(work, wr);
+    atomicAdd(work + 1, we);
+  }
 }
 
 struct ApArgs {
@@ -557,8 +591,10 @@ struct ApArgs {
 // moved appear twice and are halved, so we sum 2c / c and halve at the end.
 template <bool UNIT>
 static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const SegLists& sl,
-                                 int64_t w0, int64_t ws, long long& acc) {
+                                 int64_t w0, int64_t ws, long long& acc,
+                                 unsigned long long* work = nullptr) {
   const int lane = threadIdx.x & 31;
+  unsigned long long wr = 0, we = 0;
   for (int t = 0; t < NBINS; ++t) {
     const int64_t cnt = (int64_t)*(const volatile unsigned long long*)(sl.cnt + t);
     const int32_t* list = sl.list[t];
@@ -567,6 +603,8 @@ static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const S
       const int old = a.parts[v];
       const int dst = a.mv[v];
       const int64_t b = g.offs[v], e = g.offs[v + 1];
+      wr += 1;
+      we += (unsigned long long)(e - b);
       long long d = 0;
       for (int64_t j = b + lane; j < e; j += 32) {
         const int u = g.adj[j];
@@ -585,6 +623,10 @@ static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const S
         atomicAdd(&a.pw[old], (unsigned long long)(-(long long)wv));
       }
     }
+  }
+  if (work && lane == 0 && wr) {
+    atomicAdd(work, wr);
+    atomicAdd(work + 1, we);
   }
 }
 
@@ -1052,13 +1094,24 @@ static __device__ void rb_tail(const RbTail& a, unsigned long long* sk_smem) {
 
 static __device__ void rb_collect(const int32_t* __restrict__ parts, const int32_t* __restrict__ opidx,
                            const int64_t* __restrict__ offs, TierMap tm, int64_t n, int32_t* lists,
-                           RbSegsDev seg, unsigned long long* cnts, int64_t t0, int64_t stride) {
+                           RbSegsDev seg, unsigned long long* cnts, int64_t t0, int64_t stride,
+                           unsigned long long* work = nullptr) {
   const int64_t lim = (n + 31) / 32 * 32;
+  unsigned long long wr = 0, we = 0;
   for (int64_t v = t0; v < lim; v += stride) {
     int t = -1;
-    if (v < n && opidx[parts[v]] >= 0) t = tm(offs[v + 1] - offs[v]);
+    if (v < n && opidx[parts[v]] >= 0) {
+      const int64_t d = offs[v + 1] - offs[v];
+      t = tm(d);
+      wr += 1;
+      we += (unsigned long long)d;
+    }
     if (__ballot_sync(0xffffffffu, t >= 0) == 0) continue;
     for (int tt = 0; tt < NBINS; ++tt) warp_append(t == tt, (int32_t)v, lists + seg.b[tt], cnts + tt);
+  }
+  if (work && wr) {  // candidate rows / entries: the stats sweep visits exactly these
+    atomicAdd(work, wr);
+    atomicAdd(work + 1, we);
   }
 }
 
