@@ -23,6 +23,9 @@
 #include <cub/block/block_scan.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 namespace jet {
 
@@ -385,16 +388,16 @@ static int bits_for(int64_t x) {
 
 static void two_hop(Ctx& c, const DGraph& g, int32_t* partner) {
   const int64_t n = g.n;
-  DBuf<int32_t> left(n, c.stream);
+  int32_t* left_p = c.scratch<int32_t>(13, n);
   DBuf<int64_t> nsel(1, c.stream);
   {
     cub::CountingInputIterator<int32_t> it(0);
     IsFree op{partner};
     size_t tmp = 0;
-    CK(cub::DeviceSelect::If(nullptr, tmp, it, left.get(), nsel.get(), (int)n, op, c.stream));
+    CK(cub::DeviceSelect::If(nullptr, tmp, it, left_p, nsel.get(), (int)n, op, c.stream));
     void* p = c.cub_scratch(tmp);
     launch(c, "th_leftovers", 8.0 * n, [&] {
-      CK(cub::DeviceSelect::If(p, tmp, it, left.get(), nsel.get(), (int)n, op, c.stream));
+      CK(cub::DeviceSelect::If(p, tmp, it, left_p, nsel.get(), (int)n, op, c.stream));
     });
   }
   int64_t nl = 0;
@@ -404,7 +407,7 @@ static void two_hop(Ctx& c, const DGraph& g, int32_t* partner) {
   DBuf<int64_t> deg(nl + 1, c.stream), poff(nl + 1, c.stream);
   dzero(c, deg.get() + nl, 1);
   launch(c, "th_deg", 20.0 * nl, [&] {
-    k_leftover_deg<<<grid_for(c, nl, 256), 256, 0, c.stream>>>(left.get(), nl, g.offs.get(), deg.get());
+    k_leftover_deg<<<grid_for(c, nl, 256), 256, 0, c.stream>>>(left_p, nl, g.offs.get(), deg.get());
   });
   {
     size_t tmp = 0;
@@ -419,19 +422,22 @@ static void two_hop(Ctx& c, const DGraph& g, int32_t* partner) {
   c.sync();
   if (np == 0) return;
   const GView gv = view(g);
-  DBuf<int32_t> k0(np, c.stream), v0(np, c.stream), k1(np, c.stream), v1(np, c.stream);
+  int32_t* k0_p = c.scratch<int32_t>(14, np);
+  int32_t* v0_p = c.scratch<int32_t>(15, np);
+  int32_t* k1_p = c.scratch<int32_t>(16, np);
+  int32_t* v1_p = c.scratch<int32_t>(17, np);
   launch(c, "th_pairs", 16.0 * np, [&] {
-    k_leftover_pairs<<<grid_for(c, nl * 32, 256), 256, 0, c.stream>>>(left.get(), nl, gv, poff.get(),
-                                                                     k0.get(), v0.get());
+    k_leftover_pairs<<<grid_for(c, nl * 32, 256), 256, 0, c.stream>>>(left_p, nl, gv, poff.get(),
+                                                                     k0_p, v0_p);
   });
   {
     size_t tmp = 0;
     const int eb = bits_for(n);
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k0.get(), k1.get(), v0.get(), v1.get(), (int)np, 0,
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k0_p, k1_p, v0_p, v1_p, (int)np, 0,
                                        eb, c.stream));
     void* p = c.cub_scratch(tmp);
     launch(c, "th_sort", 32.0 * np, [&] {
-      CK(cub::DeviceRadixSort::SortPairs(p, tmp, k0.get(), k1.get(), v0.get(), v1.get(), (int)np, 0, eb,
+      CK(cub::DeviceRadixSort::SortPairs(p, tmp, k0_p, k1_p, v0_p, v1_p, (int)np, 0, eb,
                                          c.stream));
     });
   }
@@ -441,11 +447,11 @@ static void two_hop(Ctx& c, const DGraph& g, int32_t* partner) {
   DBuf<int64_t> nruns(1, c.stream);
   {
     size_t tmp = 0;
-    CK(cub::DeviceRunLengthEncode::Encode(nullptr, tmp, k1.get(), centres.get(), ccnt.get(), nruns.get(),
+    CK(cub::DeviceRunLengthEncode::Encode(nullptr, tmp, k1_p, centres.get(), ccnt.get(), nruns.get(),
                                           (int)np, c.stream));
     void* p = c.cub_scratch(tmp);
     launch(c, "th_rle", 12.0 * np, [&] {
-      CK(cub::DeviceRunLengthEncode::Encode(p, tmp, k1.get(), centres.get(), ccnt.get(), nruns.get(),
+      CK(cub::DeviceRunLengthEncode::Encode(p, tmp, k1_p, centres.get(), ccnt.get(), nruns.get(),
                                             (int)np, c.stream));
     });
   }
@@ -461,17 +467,18 @@ static void two_hop(Ctx& c, const DGraph& g, int32_t* partner) {
       CK(cub::DeviceScan::ExclusiveSum(p, tmp, ccnt.get(), coff.get(), (int)(nc + 1), c.stream));
     });
   }
-  DBuf<uint8_t> cact(n, c.stream), ready(nc, c.stream);
-  DBuf<int32_t> minc(n, c.stream);
-  dzero(c, cact.get(), n);
-  th_mark(c, centres.get(), nc, cact.get());
-  TwoHop t{partner, centres.get(), coff.get(), v1.get(), cact.get(), ready.get(), minc.get(), nc};
+  uint8_t* cact_p = c.scratch<uint8_t>(18, n);
+  uint8_t* ready_p = c.scratch<uint8_t>(19, nc);
+  int32_t* minc_p = c.scratch<int32_t>(20, n);
+  dzero(c, cact_p, n);
+  th_mark(c, centres.get(), nc, cact_p);
+  TwoHop t{partner, centres.get(), coff.get(), v1_p, cact_p, ready_p, minc_p, nc};
   DBuf<unsigned long long> act(1, c.stream);
   dzero(c, act.get(), 1);
   const int64_t want = std::max<int64_t>(nc, nl);
   const int blocks = std::min<int64_t>(coop_blocks(c, (const void*)k_two_hop, 1024),
                                        std::max<int64_t>(1, (want * 32 + 1023) / 1024));
-  const int32_t* lp = left.get();
+  const int32_t* lp = left_p;
   unsigned long long* ap = act.get();
   void* args[] = {&t, (void*)&gv, (void*)&lp, (void*)&nl, (void*)&ap};
   launch(c, "two_hop", 0.0, [&] {
@@ -666,9 +673,11 @@ void device_match(Ctx& c, const DGraph& g, int32_t* partner) {
     k_fill<<<grid_for(c, n, 256), 256, 0, c.stream>>>(partner, n, -1);
   });
   if (g.nnz > 0) {
-    DBuf<int32_t> prop(n, c.stream), lists(2 * n, c.stream), mn(2 * n, c.stream);
+    int32_t* prop_p = c.scratch<int32_t>(10, n);
+    int32_t* lists_p = c.scratch<int32_t>(11, 2 * n);
+    int32_t* mn_p = c.scratch<int32_t>(12, 2 * n);
     DBuf<unsigned long long> cnt(2, c.stream);
-    CK(cudaMemsetAsync(mn.get(), 0x7f, 2 * n * sizeof(int32_t), c.stream));
+    CK(cudaMemsetAsync(mn_p, 0x7f, 2 * n * sizeof(int32_t), c.stream));
     const GView gv = view(g);
     while (true) {
       dzero(c, cnt.get(), 2);
@@ -681,13 +690,13 @@ void device_match(Ctx& c, const DGraph& g, int32_t* partner) {
         launch(c, "propose", (g.unit_ew ? 8.0 : 12.0) * g.bin_nnz[t] + 12.0 * bc, [&] {
           if (t < 4)
             JET_TIER_LAUNCH(k_propose, G, g.unit_ew, grid, 256, 0, c.stream, gv, list, bc, partner,
-                            prop.get(), lists.get(), cnt.get());
+                            prop_p, lists_p, cnt.get());
           else if (g.unit_ew)
-            k_propose_long<true><<<grid, 256, 0, c.stream>>>(gv, list, bc, partner, prop.get(),
-                                                            lists.get(), cnt.get());
+            k_propose_long<true><<<grid, 256, 0, c.stream>>>(gv, list, bc, partner, prop_p,
+                                                            lists_p, cnt.get());
           else
-            k_propose_long<false><<<grid, 256, 0, c.stream>>>(gv, list, bc, partner, prop.get(),
-                                                             lists.get(), cnt.get());
+            k_propose_long<false><<<grid, 256, 0, c.stream>>>(gv, list, bc, partner, prop_p,
+                                                             lists_p, cnt.get());
         });
       }
       unsigned long long ne = 0;
@@ -695,7 +704,7 @@ void device_match(Ctx& c, const DGraph& g, int32_t* partner) {
       c.sync();
       if (ne == 0) break;
       // all resolution rounds in one cooperative launch (k_resolve)
-      Resolve R{prop.get(), partner, lists.get(), cnt.get(), mn.get(), n,
+      Resolve R{prop_p, partner, lists_p, cnt.get(), mn_p, n,
                 (unsigned long long)RES_TAIL};
       const size_t smem = sizeof(ResTailSmem);
       static int res_grid = 0;
@@ -968,68 +977,89 @@ __global__ void k_copy_rows(const int64_t* __restrict__ toff, const int64_t* __r
   }
 }
 
+static double wall_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* partner,
                                         int32_t* vmap) {
+  static const bool dbg = getenv("JET_COARSEN_TIMES") && getenv("JET_COARSEN_TIMES")[0] == '2';
+  double tm = dbg ? wall_s() : 0;
+  auto mark = [&](const char* what) {
+    if (!dbg) return;
+    c.sync();
+    const double t = wall_s();
+    fprintf(stderr, "  contract %s %.2fms\n", what, (t - tm) * 1e3);
+    tm = t;
+  };
   const int64_t n = g.n;
-  DBuf<int32_t> flag(n, c.stream), cid(n, c.stream);
+  int32_t* flag_p = c.scratch<int32_t>(0, n);
+  int32_t* cid_p = c.scratch<int32_t>(1, n);
   launch(c, "is_rep", 8.0 * n, [&] {
-    k_is_rep<<<grid_for(c, n, 256), 256, 0, c.stream>>>(partner, n, flag.get());
+    k_is_rep<<<grid_for(c, n, 256), 256, 0, c.stream>>>(partner, n, flag_p);
   });
   {
     size_t tmp = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag.get(), cid.get(), (int)n, c.stream));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag_p, cid_p, (int)n, c.stream));
     void* p = c.cub_scratch(tmp);
     launch(c, "rep_scan", 8.0 * n, [&] {
-      CK(cub::DeviceScan::ExclusiveSum(p, tmp, flag.get(), cid.get(), (int)n, c.stream));
+      CK(cub::DeviceScan::ExclusiveSum(p, tmp, flag_p, cid_p, (int)n, c.stream));
     });
   }
   int32_t last[2];
-  d2h(c, &last[0], cid.get() + n - 1, 1);
-  d2h(c, &last[1], flag.get() + n - 1, 1);
+  d2h(c, &last[0], cid_p + n - 1, 1);
+  d2h(c, &last[1], flag_p + n - 1, 1);
   c.sync();
   const int64_t nc = (int64_t)last[0] + last[1];
+  mark("ids");
   auto cg_ = std::make_unique<DGraph>();
   cg_->n = nc;
   cg_->vw.alloc(nc, c.stream);
-  DBuf<int32_t> mem_a(nc, c.stream), mem_b(nc, c.stream);
-  DBuf<int64_t> rowlen(nc + 1, c.stream), toff(nc + 1, c.stream), cdeg(nc + 1, c.stream);
+  int32_t* mem_a_p = c.scratch<int32_t>(2, nc);
+  int32_t* mem_b_p = c.scratch<int32_t>(3, nc);
+  int64_t* rowlen_p = c.scratch<int64_t>(4, nc + 1);
+  int64_t* toff_p = c.scratch<int64_t>(5, nc + 1);
+  int64_t* cdeg_p = c.scratch<int64_t>(6, nc + 1);
   DBuf<unsigned> ovf(1, c.stream);
   dzero(c, ovf.get(), 1);
-  CoarseMap cm{partner, cid.get(), g.offs.get(), g.vw.get(), vmap, cg_->vw.get(),
-               mem_a.get(), mem_b.get(), rowlen.get(), ovf.get()};
+  CoarseMap cm{partner, cid_p, g.offs.get(), g.vw.get(), vmap, cg_->vw.get(),
+               mem_a_p, mem_b_p, rowlen_p, ovf.get()};
   launch(c, "coarse_map", 24.0 * n, [&] {
     k_coarse_map<<<grid_for(c, n, 256), 256, 0, c.stream>>>(cm, n);
   });
-  dzero(c, rowlen.get() + nc, 1);
-  dzero(c, cdeg.get() + nc, 1);
+  dzero(c, rowlen_p + nc, 1);
+  dzero(c, cdeg_p + nc, 1);
   {
     size_t tmp = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, rowlen.get(), toff.get(), (int)(nc + 1), c.stream));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, rowlen_p, toff_p, (int)(nc + 1), c.stream));
     void* p = c.cub_scratch(tmp);
     launch(c, "rowlen_scan", 16.0 * nc, [&] {
-      CK(cub::DeviceScan::ExclusiveSum(p, tmp, rowlen.get(), toff.get(), (int)(nc + 1), c.stream));
+      CK(cub::DeviceScan::ExclusiveSum(p, tmp, rowlen_p, toff_p, (int)(nc + 1), c.stream));
     });
   }
   int64_t T = 0;
-  d2h(c, &T, toff.get() + nc, 1);
+  d2h(c, &T, toff_p + nc, 1);
   c.sync();
-  DBuf<int32_t> tadj(T > 0 ? T : 1, c.stream), tew(T > 0 ? T : 1, c.stream), big(nc, c.stream);
+  mark("map+scan");
+  int32_t* tadj_p = c.scratch<int32_t>(7, T);
+  int32_t* tew_p = c.scratch<int32_t>(8, T);
+  int32_t* big_p = c.scratch<int32_t>(9, nc);
   DBuf<unsigned long long> big_cnt(1, c.stream);
   dzero(c, big_cnt.get(), 1);
-  RowMerge rm{g.offs.get(), g.adj.get(), g.ew.get(), vmap, mem_a.get(), mem_b.get(), toff.get(),
-              rowlen.get(), tadj.get(), tew.get(), cdeg.get(), big.get(), big_cnt.get(), ovf.get(), nc};
+  RowMerge rm{g.offs.get(), g.adj.get(), g.ew.get(), vmap, mem_a_p, mem_b_p, toff_p,
+              rowlen_p, tadj_p, tew_p, cdeg_p, big_p, big_cnt.get(), ovf.get(), nc};
   launch(c, "contract_rows", 12.0 * g.nnz + 8.0 * T + 16.0 * nc, [&] {
     k_merge_rows<<<grid_for(c, nc * 32, 256), 256, 0, c.stream>>>(rm);
   });
   unsigned long long nbig = 0;
   d2h(c, &nbig, big_cnt.get(), 1);
   c.sync();
+  mark("alloc+rows");
   if (nbig > 0) {
     const int64_t nb = (int64_t)nbig;
     DBuf<int64_t> blen(nb + 1, c.stream), boff(nb + 1, c.stream);
     dzero(c, blen.get() + nb, 1);
     launch(c, "big_len", 16.0 * nb, [&] {
-      k_big_len<<<grid_for(c, nb, 256), 256, 0, c.stream>>>(big.get(), nb, rowlen.get(), blen.get());
+      k_big_len<<<grid_for(c, nb, 256), 256, 0, c.stream>>>(big_p, nb, rowlen_p, blen.get());
     });
     {
       size_t tmp = 0;
@@ -1044,7 +1074,7 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
     c.sync();
     DBuf<unsigned long long> bk(BT, c.stream), bk2(BT, c.stream);
     launch(c, "big_gather", 20.0 * BT, [&] {
-      k_big_gather<<<grid_for(c, nb * 256, 256), 256, 0, c.stream>>>(rm, big.get(), nb, boff.get(), bk.get());
+      k_big_gather<<<grid_for(c, nb * 256, 256), 256, 0, c.stream>>>(rm, big_p, nb, boff.get(), bk.get());
     });
     {
       size_t tmp = 0;
@@ -1057,17 +1087,17 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
       });
     }
     launch(c, "big_dedup", 16.0 * BT, [&] {
-      k_big_dedup<<<grid_for(c, nb * 256, 256), 256, 0, c.stream>>>(rm, big.get(), nb, boff.get(), bk2.get());
+      k_big_dedup<<<grid_for(c, nb * 256, 256), 256, 0, c.stream>>>(rm, big_p, nb, boff.get(), bk2.get());
     });
   }
   // final offsets
   cg_->offs.alloc(nc + 1, c.stream);
   {
     size_t tmp = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cdeg.get(), cg_->offs.get(), (int)(nc + 1), c.stream));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cdeg_p, cg_->offs.get(), (int)(nc + 1), c.stream));
     void* p = c.cub_scratch(tmp);
     launch(c, "cdeg_scan", 16.0 * nc, [&] {
-      CK(cub::DeviceScan::ExclusiveSum(p, tmp, cdeg.get(), cg_->offs.get(), (int)(nc + 1), c.stream));
+      CK(cub::DeviceScan::ExclusiveSum(p, tmp, cdeg_p, cg_->offs.get(), (int)(nc + 1), c.stream));
     });
   }
   int64_t cnnz = 0;
@@ -1080,16 +1110,20 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
   cg_->nnz = cnnz;
   cg_->adj.alloc(cnnz > 0 ? cnnz : 1, c.stream);
   cg_->ew.alloc(cnnz > 0 ? cnnz : 1, c.stream);
+  mark("big+offs");
   launch(c, "copy_rows", 16.0 * cnnz + 16.0 * nc, [&] {
-    k_copy_rows<<<grid_for(c, nc * 32, 256), 256, 0, c.stream>>>(toff.get(), cg_->offs.get(), tadj.get(),
-                                                                tew.get(), cg_->adj.get(), cg_->ew.get(), nc);
+    k_copy_rows<<<grid_for(c, nc * 32, 256), 256, 0, c.stream>>>(toff_p, cg_->offs.get(), tadj_p,
+                                                                tew_p, cg_->adj.get(), cg_->ew.get(), nc);
   });
+  mark("copy");
   finalize_graph(c, *cg_);
+  mark("finalize");
   return cg_;
 }
 
 // build_hierarchy (coarsen.py:141-161; MAX_LEVELS 64, stagnation 0.95 twice)
 void device_build_hierarchy(Ctx& c, const DGraph& g0, int64_t target, Hierarchy& h) {
+  static const bool dbg = getenv("JET_COARSEN_TIMES") && getenv("JET_COARSEN_TIMES")[0] == '1';
   h.base = &g0;
   h.owned.clear();
   h.maps.clear();
@@ -1098,9 +1132,23 @@ void device_build_hierarchy(Ctx& c, const DGraph& g0, int64_t target, Hierarchy&
   DBuf<int32_t> partner;
   while (fine->n > target && (int)h.owned.size() + 1 < 64) {
     partner.ensure(fine->n, c.stream);
+    double t0 = 0, t1 = 0;
+    if (dbg) {
+      c.sync();
+      t0 = wall_s();
+    }
     device_match(c, *fine, partner.get());
+    if (dbg) {
+      c.sync();
+      t1 = wall_s();
+    }
     DBuf<int32_t> vmap(fine->n, c.stream);
     auto coarse = device_contract(c, *fine, partner.get(), vmap.get());
+    if (dbg) {
+      c.sync();
+      fprintf(stderr, "COARSEN n=%lld match=%.2fms contract=%.2fms\n", (long long)fine->n,
+              (t1 - t0) * 1e3, (wall_s() - t1) * 1e3);
+    }
     if (coarse->n == fine->n) break;
     const bool stag = (double)coarse->n > 0.95 * (double)fine->n;
     h.maps.push_back(std::move(vmap));

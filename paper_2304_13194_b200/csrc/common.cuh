@@ -187,11 +187,31 @@ struct Ctx {
   int prof_class(const char* name);
   void flush_prof();
   void ensure_pinned(size_t elems);
+  // pinned upload ring (graph upload from pageable host arrays)
+  static constexpr int UPLOAD_BUFS = 3;
+  static constexpr size_t UPLOAD_CHUNK = (size_t)32 << 20;
+  void* up_host[UPLOAD_BUFS] = {};
+  cudaEvent_t up_ev[UPLOAD_BUFS] = {};
+  DBuf<uint8_t> up_dev;
+  void ensure_upload_ring();
   void ensure_pinned_up(size_t bytes);
   void sync() { CK(cudaStreamSynchronize(stream)); }
   void* cub_scratch(size_t bytes) {
     cub_tmp.ensure(bytes, stream);
     return cub_tmp.get();
+  }
+  // Grow-only scratch slots for large per-level temporaries (coarsening):
+  // sized once by the finest level, reused by every coarser level and call.
+  // Fresh stream-ordered allocations of hundreds of MB occasionally make the
+  // pool map new physical memory, which stalls the host for 100s of ms.
+  static constexpr int NSCRATCH = 24;
+  DBuf<uint8_t> scratch_slots[NSCRATCH];
+  template <class T>
+  T* scratch(int slot, size_t count) {
+    DBuf<uint8_t>& b = scratch_slots[slot];
+    const size_t bytes = (count > 0 ? count : 1) * sizeof(T);
+    if (bytes > b.n) b.alloc(bytes + bytes / 8, stream);
+    return reinterpret_cast<T*>(b.get());
   }
 };
 

@@ -64,6 +64,16 @@ void Ctx::ensure_pinned(size_t elems) {
   pinned_elems = want;
 }
 
+void Ctx::ensure_upload_ring() {
+  if (up_host[0]) return;
+  for (int b = 0; b < UPLOAD_BUFS; ++b) {
+    CK(cudaMallocHost(&up_host[b], UPLOAD_CHUNK));
+    CK(cudaEventCreateWithFlags(&up_ev[b], cudaEventDisableTiming));
+    CK(cudaEventRecord(up_ev[b], stream));
+  }
+  up_dev.alloc((size_t)UPLOAD_BUFS * UPLOAD_CHUNK, stream);
+}
+
 void Ctx::ensure_pinned_up(size_t bytes) {
   if (bytes <= pinned_up_bytes) return;
   if (pinned_up) cudaFreeHost(pinned_up);
@@ -133,6 +143,11 @@ void jet_destroy(jet_ctx* ctx) {
   for (auto e : c->event_pool) cudaEventDestroy(e);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->pinned_up) cudaFreeHost(c->pinned_up);
+  c->up_dev.release();
+  for (int b = 0; b < Ctx::UPLOAD_BUFS; ++b) {
+    if (c->up_host[b]) cudaFreeHost(c->up_host[b]);
+    if (c->up_ev[b]) cudaEventDestroy(c->up_ev[b]);
+  }
   cudaStreamSynchronize(c->stream);
   cudaStreamDestroy(c->stream);
   delete c;

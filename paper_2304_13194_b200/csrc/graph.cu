@@ -5,8 +5,26 @@
 #include "graph.cuh"
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
+#include <algorithm>
+#include <cstring>
+#include <omp.h>
 
 namespace jet {
+
+// memcpy split over the host cores (pageable -> pinned staging)
+static void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+  const size_t piece = (size_t)1 << 21;
+  const int64_t np = (int64_t)((bytes + piece - 1) / piece);
+  if (np <= 1) {
+    memcpy(dst, src, bytes);
+    return;
+  }
+#pragma omp parallel for schedule(static) num_threads(std::min<int>(8, omp_get_num_procs()))
+  for (int64_t i = 0; i < np; ++i) {
+    const size_t o = (size_t)i * piece;
+    memcpy((char*)dst + o, (const char*)src + o, std::min(piece, bytes - o));
+  }
+}
 
 // ---------------------------------------------------------------------------
 // Upload: host arrays (int32 or int64) -> int32 device arrays, with range
@@ -155,6 +173,25 @@ void finalize_graph(Ctx& c, DGraph& g) {
   }
 }
 
+// Pipelined host->device copy of `bytes` from pageable `src`; `consume(dptr,
+// off, len)` is enqueued on the context stream for every device-side chunk.
+template <class F>
+static void staged_upload(Ctx& c, const void* src, size_t bytes, F&& consume) {
+  c.ensure_upload_ring();
+  const size_t CHB = Ctx::UPLOAD_CHUNK;
+  const char* s = static_cast<const char*>(src);
+  for (size_t off = 0, i = 0; off < bytes; off += CHB, ++i) {
+    const size_t len = std::min(CHB, bytes - off);
+    const int b = (int)(i % Ctx::UPLOAD_BUFS);
+    CK(cudaEventSynchronize(c.up_ev[b]));  // the DMA that last used this buffer
+    parallel_memcpy(c.up_host[b], s + off, len);
+    uint8_t* d = c.up_dev.get() + (size_t)b * CHB;
+    CK(cudaMemcpyAsync(d, c.up_host[b], len, cudaMemcpyHostToDevice, c.stream));
+    consume(d, off, len);
+    CK(cudaEventRecord(c.up_ev[b], c.stream));
+  }
+}
+
 std::unique_ptr<DGraph> upload_graph(Ctx& c, int64_t n, const int64_t* offs,
                                      const void* adj, int adt, const void* ew,
                                      int edt, const void* vw, int vdt) {
@@ -174,33 +211,37 @@ std::unique_ptr<DGraph> upload_graph(Ctx& c, int64_t n, const int64_t* offs,
   g->vw.alloc(n, c.stream);
   DBuf<unsigned> bad(1, c.stream);
   dzero(c, bad.get(), 1);
-  h2d(c, g->offs.get(), offs, n + 1);
+  {
+    int64_t* doffs = g->offs.get();
+    staged_upload(c, offs, (size_t)(n + 1) * 8, [&](const void* dchunk, size_t off, size_t bytes) {
+      CK(cudaMemcpyAsync((char*)doffs + off, dchunk, bytes, cudaMemcpyDeviceToDevice, c.stream));
+    });
+  }
   launch(c, "check_offsets", 8.0 * (n + 1), [&] {
     k_check_offsets<<<grid_for(c, n, 256), 256, 0, c.stream>>>(g->offs.get(), n, nnz, bad.get());
   });
-  // staging for int64 -> int32 narrowing, chunked to bound the footprint
-  const int64_t CH = 1LL << 26;
-  DBuf<int64_t> stage;
+  // Host arrays stream through a ring of pinned buffers: several host
+  // threads copy chunk i+1 into pinned memory while chunk i is DMA'd and
+  // narrowed to int32 on the device (pageable cudaMemcpy tops out far below
+  // the link rate).
   auto put = [&](const void* src, int dt, int32_t* dst, int64_t count, long long lo,
                  long long hi, int flag) {
     if (count == 0) return;
-    if (dt == JET_I32) {
-      h2d(c, dst, (const int32_t*)src, count);
-      launch(c, "validate_i32", 4.0 * count, [&] {
-        k_narrow<int32_t><<<grid_for(c, count, 256), 256, 0, c.stream>>>(
-            dst, dst, count, lo, hi, flag, bad.get());
-      });
-      return;
-    }
-    stage.ensure(count < CH ? count : CH, c.stream);
-    for (int64_t b = 0; b < count; b += CH) {
-      int64_t m = count - b < CH ? count - b : CH;
-      h2d(c, stage.get(), (const int64_t*)src + b, m);
-      launch(c, "narrow_i64", 12.0 * m, [&] {
-        k_narrow<int64_t><<<grid_for(c, m, 256), 256, 0, c.stream>>>(
-            stage.get(), dst + b, m, lo, hi, flag, bad.get());
-      });
-    }
+    const size_t esz = dt == JET_I32 ? 4 : 8;
+    staged_upload(c, src, (size_t)count * esz, [&](const void* dchunk, size_t off, size_t bytes) {
+      const int64_t e0 = (int64_t)(off / esz), m = (int64_t)(bytes / esz);
+      if (dt == JET_I32) {
+        launch(c, "validate_i32", 8.0 * m, [&] {
+          k_narrow<int32_t><<<grid_for(c, m, 256), 256, 0, c.stream>>>(
+              (const int32_t*)dchunk, dst + e0, m, lo, hi, flag, bad.get());
+        });
+      } else {
+        launch(c, "narrow_i64", 12.0 * m, [&] {
+          k_narrow<int64_t><<<grid_for(c, m, 256), 256, 0, c.stream>>>(
+              (const int64_t*)dchunk, dst + e0, m, lo, hi, flag, bad.get());
+        });
+      }
+    });
   };
   const long long I32MAX = 2147483647LL;
   put(adj, adt, g->adj.get(), nnz, 0, n - 1, BAD_ADJ);
