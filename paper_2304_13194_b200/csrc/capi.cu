@@ -13,11 +13,13 @@
 struct jet_graph {
   std::unique_ptr<jet::DGraph> g;
   int device = 0;
+  jet::Ctx* ctx = nullptr;  // owning handles keep their context (stream) alive
 };
 struct jet_hierarchy {
   jet::Hierarchy h;
   std::vector<jet_graph> views;  // non-owning wrappers around h's levels
   int device = 0;
+  jet::Ctx* ctx = nullptr;
 };
 
 using namespace jet;
@@ -82,6 +84,8 @@ int jet_graph_upload(jet_ctx* ctx, int64_t n, const int64_t* row_offsets, const 
   jet_graph* jg = new jet_graph();
   jg->g = std::move(g);
   jg->device = c.device;
+  jg->ctx = &c;
+  ctx_retain(&c);
   *out = jg;
   API_END
 }
@@ -113,7 +117,9 @@ int jet_graph_download(jet_ctx* ctx, const jet_graph* g, int64_t* row_offsets, i
 void jet_graph_free(jet_graph* g) {
   if (!g) return;
   cudaSetDevice(g->device);
+  Ctx* c = g->ctx;
   delete g;
+  ctx_release(c);
 }
 
 int jet_cutsize(jet_ctx* ctx, const jet_graph* g, const int64_t* parts, int64_t* cut_out) {
@@ -161,6 +167,8 @@ int jet_contract(jet_ctx* ctx, const jet_graph* g, const int64_t* partner, jet_g
   jet_graph* jg = new jet_graph();
   jg->g = std::move(cg_);
   jg->device = c.device;
+  jg->ctx = &c;
+  ctx_retain(&c);
   *coarse_out = jg;
   API_END
 }
@@ -178,6 +186,8 @@ int jet_hierarchy_build(jet_ctx* ctx, const jet_graph* g, int64_t target, jet_hi
     delete h;
     throw;
   }
+  h->ctx = &c;
+  ctx_retain(&c);
   *out = h;
   API_END
 }
@@ -208,7 +218,9 @@ void jet_hierarchy_free(jet_hierarchy* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   for (auto& v : h->views) v.g.release();  // non-owning
+  Ctx* c = h->ctx;
   delete h;
+  ctx_release(c);
 }
 
 int jet_project(jet_ctx* ctx, int64_t n_coarse, const int64_t* coarse_parts, int64_t n_fine,

@@ -8,6 +8,8 @@
 // Sums (conn, gains, part weights, cut) are int64, matching the reference's
 // int64 numpy arithmetic (_arrays.py:5).
 #pragma once
+#include <atomic>
+#include <memory>
 #include <cuda_runtime.h>
 #include <cooperative_groups.h>
 #include <cstdint>
@@ -156,8 +158,18 @@ struct ProfAgg {
   double ms = 0, bytes = 0;
 };
 
+// Context-owned extension state (defined by the translation unit that uses
+// it); released by jet_destroy while the context stream is still alive.
+struct CtxExt {
+  virtual ~CtxExt() = default;
+};
+
 struct Ctx {
   int device = 0;
+  // Graphs and hierarchies allocated on this context's stream hold a
+  // reference, so the stream outlives every buffer freed on it whatever
+  // order the caller (e.g. interpreter teardown) releases handles in.
+  std::atomic<int> refs{1};
   cudaStream_t stream = nullptr;
   int num_sms = 148;
   int max_smem_optin = 0;
@@ -204,6 +216,7 @@ struct Ctx {
   // sized once by the finest level, reused by every coarser level and call.
   // Fresh stream-ordered allocations of hundreds of MB occasionally make the
   // pool map new physical memory, which stalls the host for 100s of ms.
+  std::unique_ptr<CtxExt> level_ext;  // level.cu: persistent-controller scratch
   static constexpr int NSCRATCH = 24;
   DBuf<uint8_t> scratch_slots[NSCRATCH];
   template <class T>
@@ -214,6 +227,9 @@ struct Ctx {
     return reinterpret_cast<T*>(b.get());
   }
 };
+
+void ctx_retain(Ctx* c);
+void ctx_release(Ctx* c);  // tears the context down at the last reference
 
 // Launch wrapper: counts the launch, brackets it with events when profiling,
 // and checks the launch status. `bytes` = algorithmic bytes of the launch.

@@ -87,6 +87,39 @@ void Ctx::ensure_pinned_up(size_t bytes) {
 
 using namespace jet;
 
+static void ctx_teardown(Ctx* c) {
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  c->cub_tmp.release();
+  c->flush_buf.release();
+  c->level_ext.reset();
+  for (auto& b : c->scratch_slots) b.release();
+  if (c->timer_a) cudaEventDestroy(c->timer_a);
+  if (c->timer_b) cudaEventDestroy(c->timer_b);
+  for (auto& r : c->recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : c->event_pool) cudaEventDestroy(e);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->pinned_up) cudaFreeHost(c->pinned_up);
+  c->up_dev.release();
+  for (int b = 0; b < Ctx::UPLOAD_BUFS; ++b) {
+    if (c->up_host[b]) cudaFreeHost(c->up_host[b]);
+    if (c->up_ev[b]) cudaEventDestroy(c->up_ev[b]);
+  }
+  cudaStreamSynchronize(c->stream);
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+namespace jet {
+void ctx_retain(Ctx* c) { c->refs.fetch_add(1); }
+void ctx_release(Ctx* c) {
+  if (c && c->refs.fetch_sub(1) == 1) ctx_teardown(c);
+}
+}  // namespace jet
+
 extern "C" {
 
 const char* jet_last_error(void) { return g_last_error.c_str(); }
@@ -129,28 +162,7 @@ int jet_create(int device, jet_ctx** out) {
 
 void jet_destroy(jet_ctx* ctx) {
   if (!ctx) return;
-  Ctx* c = reinterpret_cast<Ctx*>(ctx);
-  cudaSetDevice(c->device);
-  cudaStreamSynchronize(c->stream);
-  c->cub_tmp.release();
-  c->flush_buf.release();
-  if (c->timer_a) cudaEventDestroy(c->timer_a);
-  if (c->timer_b) cudaEventDestroy(c->timer_b);
-  for (auto& r : c->recs) {
-    cudaEventDestroy(r.a);
-    cudaEventDestroy(r.b);
-  }
-  for (auto e : c->event_pool) cudaEventDestroy(e);
-  if (c->pinned) cudaFreeHost(c->pinned);
-  if (c->pinned_up) cudaFreeHost(c->pinned_up);
-  c->up_dev.release();
-  for (int b = 0; b < Ctx::UPLOAD_BUFS; ++b) {
-    if (c->up_host[b]) cudaFreeHost(c->up_host[b]);
-    if (c->up_ev[b]) cudaEventDestroy(c->up_ev[b]);
-  }
-  cudaStreamSynchronize(c->stream);
-  cudaStreamDestroy(c->stream);
-  delete c;
+  jet::ctx_release(reinterpret_cast<Ctx*>(ctx));
 }
 
 int jet_synchronize(jet_ctx* ctx) {

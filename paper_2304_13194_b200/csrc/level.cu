@@ -591,7 +591,7 @@ static int ceil_log2_host(int64_t x) {
   return r;
 }
 
-struct LevelScratch {
+struct LevelScratch : CtxExt {
   DBuf<LevelCtl> ctl;
   DBuf<long long> keep_pw;
   DBuf<int32_t> backup;
@@ -600,8 +600,8 @@ struct LevelScratch {
 };
 
 static LevelScratch& level_scratch(Ctx& c) {
-  static thread_local std::map<Ctx*, LevelScratch> m;
-  return m[&c];
+  if (!c.level_ext) c.level_ext.reset(new LevelScratch());
+  return *static_cast<LevelScratch*>(c.level_ext.get());
 }
 
 bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, int64_t& cut,
