@@ -21,6 +21,8 @@ from .errors import (
 )
 
 LIB_PATH = Path(__file__).resolve().parent / "libjet.so"
+if os.environ.get("JET_LIB"):  # alternative build of the same library (experiments)
+    LIB_PATH = Path(os.environ["JET_LIB"]).resolve()
 
 JET_OK, JET_EINVAL, JET_EBALANCE, JET_ECUDA, JET_ENOMEM, JET_EREBALANCE = 0, 1, 2, 3, 4, 5
 JET_EINTERNAL, JET_EUNSUPPORTED = 6, 7

@@ -57,9 +57,10 @@ constexpr int KMASK = (1 << KBITS) - 1;
 constexpr int NBINS = 6;
 constexpr int BIN_WARP = 4, BIN_BLOCK = 5;
 constexpr int64_t WARP_TIER_MAX_DEG = 2048;
-// Per-level degree -> tier map. Small levels merge every row of <= 32
+// Per-level degree -> tier map. Small levels merge every row of <= 64
 // entries into tier 3 (one launch instead of four; launch latency dominates
-// there); large levels use the G = 4/8/16/32 split.
+// there); large levels use the G = 4/8/16/32 split, where the G = 32 tier
+// holds rows of 17..64 entries, two per lane.
 struct TierMap {
   int lim[4];
   __host__ __device__ __forceinline__ int operator()(int64_t d) const {
@@ -71,7 +72,7 @@ struct TierMap {
 };
 constexpr int64_t MERGED_TIER_MAX_N = 1 << 18;
 inline TierMap tiers_for(int64_t n) {
-  return n <= MERGED_TIER_MAX_N ? TierMap{{-1, -1, -1, 32}} : TierMap{{4, 8, 16, 32}};
+  return n <= MERGED_TIER_MAX_N ? TierMap{{-1, -1, -1, 64}} : TierMap{{4, 8, 16, 64}};
 }
 constexpr int TIER_G[4] = {4, 8, 16, 32};
 
@@ -132,7 +133,7 @@ struct DGraph {
   int64_t n = 0, nnz = 0, total_vw = 0;
   int64_t max_deg = 0, max_wdeg = 0, max_ew = 0, max_vw = 0, min_vw = 1;
   bool unit_ew = true;
-  TierMap tm{{4, 8, 16, 32}};
+  TierMap tm{{4, 8, 16, 64}};
   DBuf<int64_t> offs;
   DBuf<int32_t> adj, ew, vw;
   // degree tiers: ascending vertex lists, or identity when one tier holds all
@@ -331,6 +332,18 @@ __device__ __forceinline__ long long peer_sum(unsigned peers, int w, bool wide) 
     int l = __ffs(m) - 1;
     m &= m - 1;
     s += __shfl_sync(peers, w, l);
+  }
+  return s;
+}
+
+// Sum of x over the lanes of `peers` (a __match_any_sync group the caller is in).
+__device__ __forceinline__ long long gsum_peers(unsigned peers, long long x) {
+  long long s = 0;
+  unsigned m = peers;
+  while (m) {
+    const int l = __ffs(m) - 1;
+    m &= m - 1;
+    s += __shfl_sync(peers, x, l);
   }
   return s;
 }

@@ -26,7 +26,13 @@
 
 namespace jet {
 
-constexpr int LV_BLOCK = 512;
+#ifndef LV_BLOCK_SIZE
+#define LV_BLOCK_SIZE 512
+#endif
+#ifndef LV_MIN_BLOCKS
+#define LV_MIN_BLOCKS 2
+#endif
+constexpr int LV_BLOCK = LV_BLOCK_SIZE;
 constexpr int LV_TAIL_SMEM = 8192;  // evicted keys sorted in shared memory
 constexpr int LV_DRAW_SLACK = 64;
 constexpr int64_t LV_ROWS_PER_BLOCK = 512;
@@ -51,6 +57,7 @@ struct LevelArgs {
   int k;
   TierMap tm;
   int wide;
+  int t3_two;  // tier 3 holds rows of 33..64 entries (two per lane)
   const int32_t* tlist[NBINS];
   int64_t tcnt[NBINS];
   RbSegsDev seg;
@@ -115,11 +122,12 @@ __device__ __forceinline__ long long dev_clock() {
 struct PhaseClock {
   unsigned long long* acc;
   long long t;
+  int kind = 0;  // pass kind: phases are accumulated per kind (16 slots each)
   __device__ PhaseClock(unsigned long long* a) : acc(a), t(dev_clock()) {}
   __device__ __forceinline__ void mark(int ph) {
     if (acc && blockIdx.x == 0 && threadIdx.x == 0) {
       const long long now = dev_clock();
-      atomicAdd(acc + ph, (unsigned long long)(now - t));
+      atomicAdd(acc + 16 * kind + ph, (unsigned long long)(now - t));
       t = now;
     }
   }
@@ -277,6 +285,7 @@ __device__ void lv_bookkeep(const LevelArgs& A) {
     const int kind = C->kind;
     long long nm = 0;
     for (int t = 0; t < NBINS; ++t) nm += (long long)__ldcg(A.ctr + CTR_MOVE + t);
+    nm += (long long)__ldcg(A.ctr + CTR_NMOVE);
     const long long d2 = (long long)__ldcg(A.ctr + CTR_CUT2D);
     C->cut += d2 / 2;
     if (kind == 1) {
@@ -314,7 +323,13 @@ __device__ void lv_bookkeep(const LevelArgs& A) {
     C->copy_keep = copy;
     s_copy = copy;
     if (A.trace && C->iterations <= A.trace_cap) {
-      long long* t = A.trace + 6 * (C->iterations - 1);
+      long long* t = A.trace + 10 * (C->iterations - 1);
+      long long ncand = 0;
+      for (int q = 0; q < NBINS; ++q) ncand += (long long)__ldcg(A.ctr + CTR_CAND + q);
+      t[6] = ncand;
+      t[7] = (long long)__ldcg(A.ctr + CTR_RCAND);
+      t[8] = kind >= 2 ? C->max_evict : 0;
+      t[9] = kind >= 2 ? C->nover : 0;
       t[0] = kind;
       t[1] = nm;
       t[2] = cut;
@@ -381,12 +396,18 @@ __device__ void lv_sweep(const LevelArgs& A, MakeArgs mk, const int32_t* const* 
     const unsigned long long* dc = dcnts ? dcnts + t : nullptr;
     const int64_t cnt = A.tcnt[t];
     uint32_t* stg = reinterpret_cast<uint32_t*>(smem) +
-                    (threadIdx.x >> 5) * stage_words<32, LV_RB, UNIT>();
+                    (threadIdx.x >> 5) * stage_words<32, LV_RB / 2, UNIT>();
     switch (t) {
       case 0: agg_small<Op, 4, UNIT, LV_RB>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc, stg); break;
       case 1: agg_small<Op, 8, UNIT, LV_RB>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc, stg); break;
       case 2: agg_small<Op, 16, UNIT, LV_RB>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc, stg); break;
-      case 3: agg_small<Op, 32, UNIT, LV_RB>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc, stg); break;
+      case 3:
+        // rows of <= 32 entries on this level: one entry per lane, full batches
+        if (A.t3_two)
+          agg_small<Op, 32, UNIT, LV_RB / 2, 2>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc, stg);
+        else
+          agg_small<Op, 32, UNIT, LV_RB, 1>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc, stg);
+        break;
       case 4: {
         const size_t per = (size_t)A.k + (size_t)(A.tl_cap + 3) / 2;
         agg_warp<Op, UNIT>(a, A.g, A.parts, list, cnt, wide, A.k, A.tl_cap, dc,
@@ -404,7 +425,7 @@ __device__ void lv_sweep(const LevelArgs& A, MakeArgs mk, const int32_t* const* 
 
 // ---------------------------------------------------------------- kernel
 template <bool UNIT>
-__global__ void __launch_bounds__(LV_BLOCK, 2) k_level(LevelArgs A) {
+__global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) {
   extern __shared__ unsigned long long lv_smem[];
   cg::grid_group grid = cg::this_grid();
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -425,12 +446,14 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_level(LevelArgs A) {
   for (int t = 0; t < NBINS; ++t) clists[t] = A.cand_lists + A.seg.b[t];
 
   PhaseClock pc(A.phase_clk);
+  WorkAcc wk;
   while (true) {
     pc.mark(15);
     if (blockIdx.x == 0) lv_decide(A);
     grid.sync();
     pc.mark(0);
     const int kind = ldv(&C->kind);
+    pc.kind = kind;
     if (kind == 0) break;
     long long acc = 0;
     if (kind == 1) {
@@ -466,9 +489,11 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_level(LevelArgs A) {
         ab.cdest = A.cdest;
         ab.F = A.F;
         ab.mv = A.mv;
-        ab.move_list = A.move_lists;
-        ab.move_cnt = A.ctr + CTR_MOVE;
-        afterburner_rows<UNIT>(ab, A.g, cands, A.seg, w0, nw, A.work + 2);
+        ab.move_list = nullptr;  // moves flagged in mv[], applied from the candidate lists
+        ab.move_cnt = nullptr;
+        long long nmv = 0;
+        afterburner_rows<UNIT>(ab, A.g, cands, A.seg, w0, nw, &wk.v[2], &wk.v[3], &nmv);
+        block_sum_atomic_any(nmv, A.ctr + CTR_NMOVE);
         grid.sync();
         pc.mark(2);
       }
@@ -481,7 +506,7 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_level(LevelArgs A) {
       for (int64_t i = t0; i < (int64_t)nover * nch; i += nt) A.CH[i] = 0;
       if (!strong) lv_draws(A, t0, nt);
       rb_collect(A.parts, A.opidx, A.g.offs, A.tm, A.n, A.cand_lists, A.seg, A.ctr + CTR_CAND, t0, nt,
-                 A.work);
+                 &wk.v[0], &wk.v[1]);
       grid.sync();
       pc.mark(3);
       RbOp::Args ra{};
@@ -557,7 +582,8 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_level(LevelArgs A) {
     {
       ApArgs ap{A.parts, A.mv, A.ctr + CTR_PW, A.ctr + CTR_CUT2D, A.k};
       long long d = 0;
-      apply_delta_rows<UNIT>(ap, A.g, moves, w0, nw, d, A.work + 4);
+      apply_delta_rows<UNIT>(ap, A.g, (kind == 1 && A.afterburner) ? cands : moves, w0, nw, d,
+                             &wk.v[4], &wk.v[5]);
       block_sum_atomic_any(d, A.ctr + CTR_CUT2D);
     }
     grid.sync();
@@ -569,8 +595,9 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_level(LevelArgs A) {
       ca.lock = A.lock;
       ca.epoch = ldv(&C->new_epoch);
       ca.set_lock = kind == 1 && A.locking;
-      for (int t = 0; t < NBINS; ++t) ca.lists[t] = moves.list[t];
-      ca.cnts = A.ctr + CTR_MOVE;
+      const SegLists& ml = (kind == 1 && A.afterburner) ? cands : moves;
+      for (int t = 0; t < NBINS; ++t) ca.lists[t] = ml.list[t];
+      ca.cnts = ml.cnt;
       apply_commit_rows(ca, t0, nt);
     }
     if (blockIdx.x == 0) lv_bookkeep(A);
@@ -582,6 +609,7 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_level(LevelArgs A) {
   }
   // the returned state is the best balanced one, or the fallback
   for (int64_t v = t0; v < A.n; v += nt) A.parts[v] = A.keep[v];
+  for (int i = 0; i < 6; ++i) block_sum_atomic_any((long long)wk.v[i], A.work + i);
 }
 
 // ------------------------------------------------------------------ host
@@ -613,7 +641,7 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   const int tl_cap = (int)std::min<int64_t>(k, WARP_TIER_MAX_DEG);
   const size_t per = ((size_t)k + (size_t)(tl_cap + 3) / 2) * 8;
   size_t smem = (size_t)LV_TAIL_SMEM * 8 + LV_BLOCK * 8;
-  smem = std::max(smem, (size_t)(LV_BLOCK / 32) * stage_words<32, LV_RB, false>() * 4);
+  smem = std::max(smem, (size_t)(LV_BLOCK / 32) * stage_words<32, LV_RB / 2, false>() * 4);
   if (g.bin_cnt[BIN_WARP]) smem = std::max(smem, per * (LV_BLOCK / 32));
   if (g.bin_cnt[BIN_BLOCK]) smem = std::max(smem, (size_t)k * 12);
   if (smem > (size_t)c.max_smem_optin) return false;
@@ -671,6 +699,7 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   A.k = k;
   A.tm = g.tm;
   A.wide = g.max_wdeg >= (1LL << 31);
+  A.t3_two = g.max_deg > 32;
   for (int t = 0; t < NBINS; ++t) {
     A.tlist[t] = tier_list(g, t);
     A.tcnt[t] = g.bin_cnt[t];
@@ -732,15 +761,15 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   static const bool trace_on = getenv("JET_TRACE") && getenv("JET_TRACE")[0] == '1';
   DBuf<long long> trace;
   if (trace_on) {
-    trace.alloc(6 * 4096, c.stream);
+    trace.alloc(10 * 4096, c.stream);
     A.trace = trace.get();
     A.trace_cap = 4096;
   }
   static const bool phases_on = getenv("JET_PHASES") && getenv("JET_PHASES")[0] == '1';
   DBuf<unsigned long long> pclk;
   if (phases_on) {
-    pclk.alloc(16, c.stream);
-    dzero(c, pclk.get(), 16);
+    pclk.alloc(64, c.stream);
+    dzero(c, pclk.get(), 64);
     A.phase_clk = pclk.get();
   }
   const void* kern = g.unit_ew ? (const void*)k_level<true> : (const void*)k_level<false>;
@@ -763,16 +792,21 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   d2h(c, w.h_pw.data(), (int64_t*)S.keep_pw.get(), k);
   c.sync();
   if (phases_on) {
-    unsigned long long pc[16];
-    d2h(c, pc, pclk.get(), 16);
+    unsigned long long pc[64];
+    d2h(c, pc, pclk.get(), 64);
     c.sync();
     static const char* names[16] = {"decide", "lp_sweep", "afterburner", "rb_collect", "rb_stats",
                                     "rb_scan", "rb_chunk", "rb_find", "rb_select", "rb_tail",
                                     "apply_delta", "commit+keep", "", "", "", "keep_copy"};
-    fprintf(stderr, "PHASES L%d blocks=%d iters=%d:", level, blocks, h.iterations);
-    for (int i = 0; i < 16; ++i)
-      if (pc[i]) fprintf(stderr, " %s=%.1fus", names[i], pc[i] / 1965.0 / std::max(1, h.iterations));
-    fprintf(stderr, "\n");
+    static const char* kinds[4] = {"stop", "lp", "weak", "strong"};
+    const int cnt[4] = {1, h.lp, h.weak, h.strong};
+    for (int kd = 1; kd < 4; ++kd) {
+      if (!cnt[kd]) continue;
+      fprintf(stderr, "PHASES L%d blocks=%d %s x%d (us/pass):", level, blocks, kinds[kd], cnt[kd]);
+      for (int i = 0; i < 16; ++i)
+        if (pc[16 * kd + i]) fprintf(stderr, " %s=%.1f", names[i], pc[16 * kd + i] / 1965.0 / cnt[kd]);
+      fprintf(stderr, "\n");
+    }
   }
   if (h.abort) {  // outside the device path's limits: rerun on the host path
     d2d(c, parts, S.backup.get(), g.n);
@@ -796,12 +830,15 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
     c.recs.back().bytes = b;
   }
   if (trace_on) {
-    std::vector<long long> t(6 * std::min(h.iterations, 4096));
+    std::vector<long long> t(10 * std::min(h.iterations, 4096));
     d2h(c, t.data(), trace.get(), t.size());
     c.sync();
-    for (size_t i = 0; i < t.size(); i += 6)
-      fprintf(stderr, "TRACE L%d it%zu kind=%lld nm=%lld cut=%lld worst=%lld noimp=%lld best=%lld\n",
-              level, i / 6, t[i], t[i + 1], t[i + 2], t[i + 3], t[i + 4], t[i + 5]);
+    for (size_t i = 0; i < t.size(); i += 10)
+      fprintf(stderr,
+              "TRACE L%d it%zu kind=%lld nm=%lld cut=%lld worst=%lld noimp=%lld best=%lld cand=%lld "
+              "rcand=%lld D=%lld nover=%lld\n",
+              level, i / 10, t[i], t[i + 1], t[i + 2], t[i + 3], t[i + 4], t[i + 5], t[i + 6], t[i + 7],
+              t[i + 8], t[i + 9]);
   }
   cut = h.keep_cut;
   st.iterations += h.iterations;

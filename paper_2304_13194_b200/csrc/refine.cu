@@ -27,10 +27,11 @@ __global__ void __launch_bounds__(256)
                 const unsigned long long* __restrict__ dcnt) {
   extern __shared__ uint32_t agg_stage[];
   long long acc = 0;
-  agg_small<Op, G, UNIT>(a, g, parts, list, cnt, wide, dcnt,
-                         (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5,
-                         ((int64_t)gridDim.x * blockDim.x) >> 5, acc,
-                         agg_stage + (threadIdx.x >> 5) * stage_words<G, 32, UNIT>());
+  constexpr int RB = G == 32 ? 16 : 32;
+  agg_small<Op, G, UNIT, RB>(a, g, parts, list, cnt, wide, dcnt,
+                             (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5,
+                             ((int64_t)gridDim.x * blockDim.x) >> 5, acc,
+                             agg_stage + (threadIdx.x >> 5) * stage_words<G, RB, UNIT>());
   Op::block_done(a, acc);
 }
 
@@ -38,7 +39,7 @@ __global__ void __launch_bounds__(256)
 template <class Op, int G, bool UNIT>
 static size_t agg_small_smem() {
   static const size_t bytes = [] {
-    const size_t b = (size_t)8 * stage_words<G, 32, UNIT>() * 4;
+    const size_t b = (size_t)8 * stage_words<G, (G == 32 ? 16 : 32), UNIT>() * 4;
     CK(cudaFuncSetAttribute(k_agg_small<Op, G, UNIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)b));
     return b;

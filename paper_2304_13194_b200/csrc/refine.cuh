@@ -18,6 +18,7 @@ enum {
   CTR_CUT2 = 13,   // 2 x cut measured by the last gains sweep
   CTR_RCAND = 14,  // rebalance candidates
   CTR_EVICT = 15,  // evicted vertices
+  CTR_NMOVE = 16,  // Jetlp moves flagged in place (level kernel)
   CTR_PW = 32
 };
 

@@ -9,6 +9,14 @@
 
 namespace jet {
 
+// Per-thread visit counters for the roofline accounting ({rows, entries} of
+// the stats, afterburner and apply sweeps). Kept in registers for a whole
+// level and reduced once at the end: global atomics per warp on two hot
+// counters cost more than the sweeps they count.
+struct WorkAcc {
+  unsigned long long v[6] = {0, 0, 0, 0, 0, 0};
+};
+
 // ===========================================================================
 // Row aggregation framework. For every vertex v of a tier, conn(v, p) is
 // aggregated over the row; an Op decides which parts compete for the "best"
@@ -135,19 +143,31 @@ struct RbOp {
     slot = max(slot, a.slot_min);
     const int w = a.vw[v];
     const bool eligible = (double)w <= a.hb[op];
-    bool take = false;
+    const unsigned am = __activemask();
+    long long hk = -1, sk = -1;
     if (eligible) {
       const int bucket = (slot - a.slot_min) * a.rho + (v % a.rho);
       a.rkey[v] = bucket;
       a.rbest[v] = best_part;
       a.rloss[v] = loss;
-      atomicAdd(&a.H[(size_t)op * a.nb + bucket], (unsigned long long)w);
-      atomicAdd(&a.Hs[(size_t)op * (a.nb / a.rho) + (slot - a.slot_min)], (unsigned long long)w);
-      take = true;
+      hk = (long long)op * a.nb + bucket;
+      sk = (long long)op * (a.nb / a.rho) + (slot - a.slot_min);
     } else {
       a.rkey[v] = -1;
     }
-    warp_append(take, v, a.rcand, a.rcand_cnt);
+    // histogram updates aggregated over equal keys of the warp (few slots
+    // per oversized part: per-vertex atomics would serialise on them)
+    {
+      const unsigned peers = __match_any_sync(am, hk);
+      const long long s2 = gsum_peers(peers, (long long)w);
+      if (hk >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&a.H[hk], (unsigned long long)s2);
+    }
+    {
+      const unsigned peers = __match_any_sync(am, sk);
+      const long long s2 = gsum_peers(peers, (long long)w);
+      if (sk >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&a.Hs[sk], (unsigned long long)s2);
+    }
+    warp_append(eligible, v, a.rcand, a.rcand_cnt);
   }
   static __device__ __forceinline__ void block_done(const Args&, long long) {}
 };
@@ -161,13 +181,19 @@ static __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;\n" ::: "memory");
 }
 
+// Entries per lane of short-row tier G: the top short tier (G = 32 lanes)
+// holds rows of up to 64 entries, two per lane (TIER_SLOTS in common.cuh).
+template <int G>
+__host__ __device__ constexpr int tier_e() {
+  return G == 32 ? 2 : 1;
+}
 // Per-warp staging words of the short-row sweep (adjacency, parts, weights).
-template <int G, int RB, bool UNIT>
+template <int G, int RB, bool UNIT, int E = tier_e<G>()>
 __host__ __device__ constexpr int stage_words() {
-  return RB * G * (UNIT ? 2 : 3);
+  return RB * G * E * (UNIT ? 2 : 3);
 }
 
-// Tiers 0-3 (rows of <= G entries). A warp owns R <= RB consecutive list
+// Tiers 0-3 (rows of <= G*E entries). A warp owns R <= RB consecutive list
 // entries; their ids, offsets and own parts are loaded once, coalesced. The
 // rows' adjacency (+weights) is then copied into shared memory with
 // fire-and-forget cp.async (one 4-byte copy per entry, all in flight at
@@ -175,7 +201,11 @@ __host__ __device__ constexpr int stage_words() {
 // the staged adjacency. Only then are the rows aggregated, G lanes per row,
 // from shared memory: three memory round trips per batch of rows instead of
 // a dependent load chain per row. Row r's result is shuffled to lane r.
-template <class Op, int G, bool UNIT, int RB = 32>
+// Rows with no neighbour outside their own part (most rows of a refined
+// mesh) take a fast path: conn(v, .) is the own-part sum only. Boundary rows
+// group equal parts with __match_any_sync (E = 1) or, two entries per lane
+// (E = 2), walk their distinct competing parts in ascending order.
+template <class Op, int G, bool UNIT, int RB = 32, int E = tier_e<G>()>
 static __device__ __forceinline__ void agg_small(const typename Op::Args& a, const GView& g,
                                                  const int32_t* __restrict__ parts,
                                                  const int32_t* __restrict__ list, int64_t cnt,
@@ -184,12 +214,14 @@ static __device__ __forceinline__ void agg_small(const typename Op::Args& a, con
                                                  int64_t w0, int64_t nw, long long& acc,
                                                  uint32_t* stage) {
   if (dcnt) cnt = (int64_t)*(const volatile unsigned long long*)dcnt;
+  static_assert(E == 1 || G == 32, "two entries per lane only for one row per step");
+  constexpr int S = G * E;     // slots per row
   constexpr int RPS = 32 / G;  // rows per step
   const unsigned gm = group_mask<G>();
   const int lane = threadIdx.x & 31, gl = lane & (G - 1), grp = lane / G;
   int* s_adj = reinterpret_cast<int*>(stage);
-  int* s_p = s_adj + RB * G;
-  int* s_w = s_p + RB * G;
+  int* s_p = s_adj + RB * S;
+  int* s_w = s_p + RB * S;
   // rows per batch: RB when there is plenty of work, fewer for small lists
   // so every warp gets rows (latency, not bandwidth, rules there)
   const int64_t per_w = (cnt + nw - 1) / nw;
@@ -213,9 +245,13 @@ static __device__ __forceinline__ void agg_small(const typename Op::Args& a, con
       const int r = st * RPS + grp;
       const int64_t rb = __shfl_sync(0xffffffffu, beg, r & 31);
       const int rd = __shfl_sync(0xffffffffu, deg, r & 31);
-      if (r < R && gl < rd) {
-        cp_async4(&s_adj[r * G + gl], g.adj + rb + gl);
-        if (!UNIT) cp_async4(&s_w[r * G + gl], g.ew + rb + gl);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int j = e * G + gl;
+        if (r < R && j < rd) {
+          cp_async4(&s_adj[r * S + j], g.adj + rb + j);
+          if (!UNIT) cp_async4(&s_w[r * S + j], g.ew + rb + j);
+        }
       }
     }
     cp_async_wait_all();
@@ -224,7 +260,11 @@ static __device__ __forceinline__ void agg_small(const typename Op::Args& a, con
     for (int st = 0; st * RPS < R; ++st) {
       const int r = st * RPS + grp;
       const int rd = __shfl_sync(0xffffffffu, deg, r & 31);
-      if (r < R && gl < rd) cp_async4(&s_p[r * G + gl], parts + s_adj[r * G + gl]);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int j = e * G + gl;
+        if (r < R && j < rd) cp_async4(&s_p[r * S + j], parts + s_adj[r * S + j]);
+      }
     }
     cp_async_wait_all();
     __syncwarp();
@@ -234,47 +274,119 @@ static __device__ __forceinline__ void agg_small(const typename Op::Args& a, con
       const int r = st * RPS + grp;
       const int rd = __shfl_sync(0xffffffffu, deg, r & 31);
       const int rown = __shfl_sync(0xffffffffu, own, r & 31);
-      int p = -1, w = 0;
-      if (r < R && gl < rd) {
-        p = s_p[r * G + gl];
-        w = UNIT ? 1 : s_w[r * G + gl];
+      int pe[E], we[E];
+      bool outside = false;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int j = e * G + gl;
+        pe[e] = -1;
+        we[e] = 0;
+        if (r < R && j < rd) {
+          pe[e] = s_p[r * S + j];
+          we[e] = UNIT ? 1 : s_w[r * S + j];
+        }
+        outside |= pe[e] >= 0 && pe[e] != rown;
       }
-      const unsigned peers = __match_any_sync(gm, p);
-      const bool comp = p >= 0 && p != rown && Op::competes(a, p, rown);
       const int src = ((lane - st * RPS) & (RPS - 1)) * G;
-      if (!wide) {
-        // 32-bit sums (weighted degree < 2^31): single-instruction REDUX
-        // reductions; best part = max conn, then lowest part id
-        const unsigned sm = UNIT ? (unsigned)__popc(peers) : __reduce_add_sync(peers, (unsigned)w);
-        const unsigned sc = UNIT ? (unsigned)__popc(__ballot_sync(gm, p >= 0 && p == rown))
-                                 : __reduce_add_sync(gm, (p >= 0 && p == rown) ? (unsigned)w : 0u);
-        const unsigned mx = __reduce_max_sync(gm, comp ? sm : 0u);
-        const unsigned pm = __reduce_min_sync(gm, (comp && sm == mx) ? (unsigned)p : 0xffffffffu);
-        const unsigned ex = __reduce_add_sync(gm, p >= 0 ? (unsigned)Op::extra(a, p, w) : 0u);
+      // interior fast path (warp-uniform): no row of this step has a
+      // neighbour outside its own part
+      if (!wide && __ballot_sync(0xffffffffu, outside) == 0) {
+        unsigned loc = 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) loc += pe[e] >= 0 ? (unsigned)we[e] : 0u;
+        const unsigned sc = __reduce_add_sync(gm, loc);
         const unsigned dsc = __shfl_sync(0xffffffffu, sc, src);
-        const unsigned dmx = __shfl_sync(0xffffffffu, mx, src);
-        const unsigned dpm = __shfl_sync(0xffffffffu, pm, src);
-        const unsigned dex = __shfl_sync(0xffffffffu, ex, src);
         if (lane / RPS == st) {
           my_self = dsc;
-          my_key = dmx ? pack_best((long long)dmx, (int)dpm) : 0ull;
-          my_ex = dex;
+          my_key = 0ull;
+          my_ex = own >= 0 ? (long long)Op::extra(a, own, (int)dsc) : 0;  // extra is linear in w
+        }
+        continue;
+      }
+      if constexpr (E == 1) {
+        const int p = pe[0], w = we[0];
+        const unsigned peers = __match_any_sync(gm, p);
+        const bool comp = p >= 0 && p != rown && Op::competes(a, p, rown);
+        if (!wide) {
+          // 32-bit sums (weighted degree < 2^31): single-instruction REDUX
+          // reductions; best part = max conn, then lowest part id
+          const unsigned sm = UNIT ? (unsigned)__popc(peers) : __reduce_add_sync(peers, (unsigned)w);
+          const unsigned sc = UNIT ? (unsigned)__popc(__ballot_sync(gm, p >= 0 && p == rown))
+                                   : __reduce_add_sync(gm, (p >= 0 && p == rown) ? (unsigned)w : 0u);
+          const unsigned mx = __reduce_max_sync(gm, comp ? sm : 0u);
+          const unsigned pm = __reduce_min_sync(gm, (comp && sm == mx) ? (unsigned)p : 0xffffffffu);
+          const unsigned ex = __reduce_add_sync(gm, p >= 0 ? (unsigned)Op::extra(a, p, w) : 0u);
+          const unsigned dsc = __shfl_sync(0xffffffffu, sc, src);
+          const unsigned dmx = __shfl_sync(0xffffffffu, mx, src);
+          const unsigned dpm = __shfl_sync(0xffffffffu, pm, src);
+          const unsigned dex = __shfl_sync(0xffffffffu, ex, src);
+          if (lane / RPS == st) {
+            my_self = dsc;
+            my_key = dmx ? pack_best((long long)dmx, (int)dpm) : 0ull;
+            my_ex = dex;
+          }
+        } else {
+          const long long sm = UNIT ? (long long)__popc(peers) : peer_sum(peers, w, wide);
+          const bool lead = p >= 0 && (__ffs(peers) - 1) == lane;
+          long long sc = (lead && p == rown) ? sm : 0;
+          unsigned long long key = (lead && comp) ? pack_best(sm, p) : 0ull;
+          long long ex = p >= 0 ? Op::extra(a, p, w) : 0;
+          sc = gsum<G>(sc, gm);
+          key = gmax<G>(key, gm);
+          ex = gsum<G>(ex, gm);
+          sc = __shfl_sync(0xffffffffu, sc, src);
+          key = __shfl_sync(0xffffffffu, key, src);
+          ex = __shfl_sync(0xffffffffu, ex, src);
+          if (lane / RPS == st) {
+            my_self = sc;
+            my_key = key;
+            my_ex = ex;
+          }
         }
       } else {
-        const long long sm = UNIT ? (long long)__popc(peers) : peer_sum(peers, w, wide);
-        const bool lead = p >= 0 && (__ffs(peers) - 1) == lane;
-        long long sc = (lead && p == rown) ? sm : 0;
-        unsigned long long key = (lead && comp) ? pack_best(sm, p) : 0ull;
-        long long ex = p >= 0 ? Op::extra(a, p, w) : 0;
-        sc = gsum<G>(sc, gm);
-        key = gmax<G>(key, gm);
-        ex = gsum<G>(ex, gm);
-        sc = __shfl_sync(0xffffffffu, sc, src);
-        key = __shfl_sync(0xffffffffu, key, src);
-        ex = __shfl_sync(0xffffffffu, ex, src);
-        if (lane / RPS == st) {
+        // G = 32 (one row per step), E entries per lane: sums over the row,
+        // then the distinct competing parts in ascending order (ties on the
+        // max therefore keep the lowest part)
+        long long lsc = 0, lex = 0;
+        bool oth[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int p = pe[e];
+          lsc += (p >= 0 && p == rown) ? we[e] : 0;
+          lex += p >= 0 ? Op::extra(a, p, we[e]) : 0;
+          oth[e] = p >= 0 && p != rown && Op::competes(a, p, rown);
+        }
+        const long long sc = wide ? gsum<32>(lsc, 0xffffffffu)
+                                  : (long long)__reduce_add_sync(0xffffffffu, (unsigned)lsc);
+        const long long ex = wide ? gsum<32>(lex, 0xffffffffu)
+                                  : (long long)__reduce_add_sync(0xffffffffu, (unsigned)lex);
+        long long bm = 0;
+        int bp = -1;
+        while (true) {
+          unsigned c = 0xffffffffu;
+#pragma unroll
+          for (int e = 0; e < E; ++e)
+            if (oth[e]) c = min(c, (unsigned)pe[e]);
+          const unsigned cur = __reduce_min_sync(0xffffffffu, c);
+          if (cur == 0xffffffffu) break;
+          long long lc = 0;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            if (pe[e] == (int)cur) {
+              lc += we[e];
+              oth[e] = false;
+            }
+          }
+          const long long cc = wide ? gsum<32>(lc, 0xffffffffu)
+                                    : (long long)__reduce_add_sync(0xffffffffu, (unsigned)lc);
+          if (cc > bm) {
+            bm = cc;
+            bp = (int)cur;
+          }
+        }
+        if (lane == st) {
           my_self = sc;
-          my_key = key;
+          my_key = bm > 0 ? pack_best(bm, bp) : 0ull;
           my_ex = ex;
         }
       }
@@ -531,13 +643,17 @@ struct SegLists {
 };
 
 // One warp per candidate over all tiers (candidate sets are small).
+// With a move list, moves are appended per row (host-driven path); without
+// one (level kernel) only mv[v] is set and the moves are counted into
+// *nmove, and the apply phase walks the candidate lists skipping unmoved
+// rows -- one atomic per row on a hot counter serialises in L2.
+// wr/we (optional): += rows / entries visited, for the roofline accounting.
 template <bool UNIT>
-// work (optional): += {rows, entries} visited, for the roofline accounting
 static __device__ void afterburner_rows(const AbArgs& a, const GView& g, const SegLists& sl,
                                  const RbSegsDev& mseg, int64_t w0, int64_t ws,
-                                 unsigned long long* work = nullptr) {
+                                 unsigned long long* wr = nullptr, unsigned long long* we = nullptr,
+                                 long long* nmove = nullptr) {
   const int lane = threadIdx.x & 31;
-  unsigned long long wr = 0, we = 0;
   for (int t = 0; t < NBINS; ++t) {
     const int64_t cnt = (int64_t)*(const volatile unsigned long long*)(sl.cnt + t);
     const int32_t* list = sl.list[t];
@@ -547,8 +663,10 @@ static __device__ void afterburner_rows(const AbArgs& a, const GView& g, const S
       const int dv = a.cdest[v];
       const long long Fv = a.F[v];
       const int64_t b = g.offs[v], e = g.offs[v + 1];
-      wr += 1;
-      we += (unsigned long long)(e - b);
+      if (wr && lane == 0) {
+        *wr += 1;
+        *we += (unsigned long long)(e - b);
+      }
       long long f2 = 0;
       for (int64_t j = b + lane; j < e; j += 32) {
         const int u = g.adj[j];
@@ -564,17 +682,18 @@ static __device__ void afterburner_rows(const AbArgs& a, const GView& g, const S
       f2 = gsum<32>(f2, 0xffffffffu);
       if (lane == 0) {
         if (a.f2_out) a.f2_out[v] = f2;
-        if (a.move_list && f2 >= 0) {
-          a.mv[v] = dv;
-          const unsigned long long q = atomicAdd(a.move_cnt + t, 1ull);
-          a.move_list[mseg.b[t] + q] = v;
+        if (f2 >= 0) {
+          if (a.move_list) {
+            a.mv[v] = dv;
+            const unsigned long long q = atomicAdd(a.move_cnt + t, 1ull);
+            a.move_list[mseg.b[t] + q] = v;
+          } else if (nmove) {
+            a.mv[v] = dv;
+            *nmove += 1;
+          }
         }
       }
     }
-  }
-  if (work && lane == 0 && wr) {
-    atomicAdd(work, wr);
-    atomicAdd(work + 1, we);
   }
 }
 
@@ -589,22 +708,26 @@ struct ApArgs {
 // Exact cut delta of a move batch (conn.py:231-248): for a moved v and
 // neighbour u, c = w([p'(u) != dest] - [p(u) != old]); edges with both ends
 // moved appear twice and are halved, so we sum 2c / c and halve at the end.
+// Rows whose mv[v] < 0 are skipped (the level kernel applies Jetlp moves
+// straight from the candidate lists).
 template <bool UNIT>
 static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const SegLists& sl,
                                  int64_t w0, int64_t ws, long long& acc,
-                                 unsigned long long* work = nullptr) {
+                                 unsigned long long* wr = nullptr, unsigned long long* we = nullptr) {
   const int lane = threadIdx.x & 31;
-  unsigned long long wr = 0, we = 0;
   for (int t = 0; t < NBINS; ++t) {
     const int64_t cnt = (int64_t)*(const volatile unsigned long long*)(sl.cnt + t);
     const int32_t* list = sl.list[t];
     for (int64_t i = w0; i < cnt; i += ws) {
       const int v = list[i];
-      const int old = a.parts[v];
       const int dst = a.mv[v];
+      if (dst < 0) continue;
+      const int old = a.parts[v];
       const int64_t b = g.offs[v], e = g.offs[v + 1];
-      wr += 1;
-      we += (unsigned long long)(e - b);
+      if (wr && lane == 0) {
+        *wr += 1;
+        *we += (unsigned long long)(e - b);
+      }
       long long d = 0;
       for (int64_t j = b + lane; j < e; j += 32) {
         const int u = g.adj[j];
@@ -615,18 +738,13 @@ static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const S
         const long long cc = w * ((long long)(nu != dst) - (long long)(pu != old));
         d += mu >= 0 ? cc : 2 * cc;
       }
-      d = gsum<32>(d, 0xffffffffu);
+      acc += d;  // per-lane partial sums: the caller reduces over the block
       if (lane == 0) {
-        acc += d;
         const unsigned long long wv = (unsigned long long)g.vw[v];
         atomicAdd(&a.pw[dst], wv);
         atomicAdd(&a.pw[old], (unsigned long long)(-(long long)wv));
       }
     }
-  }
-  if (work && lane == 0 && wr) {
-    atomicAdd(work, wr);
-    atomicAdd(work + 1, we);
   }
 }
 
@@ -646,7 +764,9 @@ static __device__ void apply_commit_rows(const CommitArgs& a, int64_t t0, int64_
     const int32_t* list = a.lists[t];
     for (int64_t i = t0; i < cnt; i += stride) {
       const int v = list[i];
-      a.parts[v] = a.mv[v];
+      const int dst = a.mv[v];
+      if (dst < 0) continue;  // unmoved candidate (level kernel, Jetlp pass)
+      a.parts[v] = dst;
       a.mv[v] = -1;
       if (a.set_lock) a.lock[v] = a.epoch;
     }
@@ -912,7 +1032,7 @@ static __device__ void rb_select(const RbSel& s, const int32_t* __restrict__ rca
       const int op = s.opidx[s.parts[v]];
       const int rk = s.rkey[v];
       const int bs = s.bstar[op];
-      sel = rk < bs || (rk == bs && v < s.thr[op]);
+      sel = rk >= 0 && (rk < bs || (rk == bs && v < s.thr[op]));
       if (sel && !strong && direct) {
         const int bp = rbest[v];
         if (bp >= 0) {
@@ -1095,7 +1215,7 @@ static __device__ void rb_tail(const RbTail& a, unsigned long long* sk_smem) {
 static __device__ void rb_collect(const int32_t* __restrict__ parts, const int32_t* __restrict__ opidx,
                            const int64_t* __restrict__ offs, TierMap tm, int64_t n, int32_t* lists,
                            RbSegsDev seg, unsigned long long* cnts, int64_t t0, int64_t stride,
-                           unsigned long long* work = nullptr) {
+                           unsigned long long* pwr = nullptr, unsigned long long* pwe = nullptr) {
   const int64_t lim = (n + 31) / 32 * 32;
   unsigned long long wr = 0, we = 0;
   for (int64_t v = t0; v < lim; v += stride) {
@@ -1109,9 +1229,9 @@ static __device__ void rb_collect(const int32_t* __restrict__ parts, const int32
     if (__ballot_sync(0xffffffffu, t >= 0) == 0) continue;
     for (int tt = 0; tt < NBINS; ++tt) warp_append(t == tt, (int32_t)v, lists + seg.b[tt], cnts + tt);
   }
-  if (work && wr) {  // candidate rows / entries: the stats sweep visits exactly these
-    atomicAdd(work, wr);
-    atomicAdd(work + 1, we);
+  if (pwr) {  // candidate rows / entries: the stats sweep visits exactly these
+    *pwr += wr;
+    *pwe += we;
   }
 }
 
