@@ -686,9 +686,12 @@ void device_match(Ctx& c, const DGraph& g, int32_t* partner) {
         if (!bc) continue;
         const int G = t < 4 ? TIER_G[t] : 32;
         const int32_t* list = tier_list(g, t);
-        const unsigned grid = grid_for(c, t < 4 ? bc : bc * 32, 256);
+        // tier 3 holds rows of up to 64 entries: k_propose<32> reads one
+        // entry per lane, so such levels propose tier 3 one warp per row
+        const bool short_rows = t < 3 || (t == 3 && g.max_deg <= 32);
+        const unsigned grid = grid_for(c, short_rows ? bc : bc * 32, 256);
         launch(c, "propose", (g.unit_ew ? 8.0 : 12.0) * g.bin_nnz[t] + 12.0 * bc, [&] {
-          if (t < 4)
+          if (short_rows)
             JET_TIER_LAUNCH(k_propose, G, g.unit_ew, grid, 256, 0, c.stream, gv, list, bc, partner,
                             prop_p, lists_p, cnt.get());
           else if (g.unit_ew)
@@ -724,6 +727,217 @@ void device_match(Ctx& c, const DGraph& g, int32_t* partner) {
       });
     }
     two_hop(c, g, partner);
+  }
+  launch(c, "singletons", 8.0 * n, [&] {
+    k_singletons<<<grid_for(c, n, 256), 256, 0, c.stream>>>(partner, n);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Throughput-mode matching (jet_config.deterministic == 0). The reference's
+// matching is sequential (ascending-id resolution, ordered two-hop walk);
+// reproducing it exactly costs many dependent rounds. This mode keeps the
+// heavy-edge criterion but breaks weight ties with a symmetric hash of the
+// edge, so both endpoints rank their edges alike and every proposal that is
+// returned is a locally dominant edge: a few propose/accept rounds match
+// most vertices, each a coalesced sweep over the free rows. Leftovers are
+// paired under their heaviest neighbour (one centre each, radix-sorted), as
+// in mt-Metis leaf matching. Not bit-exact with the reference: the 2 %
+// cutsize gate applies (north_star, throughput mode).
+__device__ __forceinline__ unsigned edge_hash(int a, int b, unsigned salt) {
+  unsigned x = (unsigned)min(a, b) * 0x9E3779B1u ^ ((unsigned)max(a, b) + salt) * 0x85EBCA77u;
+  x ^= x >> 15;
+  x *= 0x2C1B3C6Du;
+  x ^= x >> 12;
+  x *= 0x297A2D39u;
+  x ^= x >> 15;
+  return x | 1u;
+}
+
+// Heaviest free neighbour, ties -> highest edge hash, then lowest id. One
+// warp per row (rows of any length), 32 rows per warp batch for short rows.
+template <bool UNIT>
+__global__ void __launch_bounds__(256)
+    k_propose_fast(GView g, int64_t n, const int32_t* __restrict__ partner, int32_t* prop,
+                   int32_t* elist, unsigned long long* ecnt, unsigned salt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = w0 * 32; base < n; base += nw * 32) {
+    const int64_t idx = base + lane;
+    int v = (int)idx, deg = 0;
+    int64_t beg = 0;
+    bool live = false;
+    if (idx < n) {
+      live = partner[v] < 0;
+      if (live) {
+        beg = g.offs[v];
+        deg = (int)(g.offs[v + 1] - beg);
+      }
+    }
+    unsigned live_m = __ballot_sync(0xffffffffu, live && deg > 0);
+    int my_u = -1;
+    while (live_m) {
+      const int r = __ffs(live_m) - 1;
+      live_m &= live_m - 1;
+      const int rv = (int)(base + r);
+      const int64_t rb = __shfl_sync(0xffffffffu, beg, r);
+      const int rd = __shfl_sync(0xffffffffu, deg, r);
+      unsigned bw = 0, bh = 0;
+      int bu = -1;
+      for (int j = lane; j < rd; j += 32) {
+        const int u = g.adj[rb + j];
+        if (partner[u] >= 0) continue;
+        const unsigned w = UNIT ? 1u : (unsigned)g.ew[rb + j];
+        const unsigned h = edge_hash(rv, u, salt);
+        if (w > bw || (w == bw && (h > bh || (h == bh && u < bu)))) {
+          bw = w;
+          bh = h;
+          bu = u;
+        }
+      }
+      const unsigned mw = __reduce_max_sync(0xffffffffu, bw);
+      const unsigned mh = __reduce_max_sync(0xffffffffu, bw == mw ? bh : 0u);
+      const unsigned mu = __reduce_min_sync(0xffffffffu, (bw == mw && bh == mh && bu >= 0)
+                                                              ? (unsigned)bu : 0xffffffffu);
+      if (lane == r) my_u = mw ? (int)mu : -1;
+    }
+    if (live) prop[v] = my_u;
+    warp_append(live && my_u >= 0, v, elist, ecnt);
+  }
+}
+
+// Accept mutual proposals (locally dominant edges); count the new pairs.
+__global__ void k_accept_mutual(const int32_t* __restrict__ prop, int32_t* partner,
+                                const int32_t* __restrict__ elist,
+                                const unsigned long long* __restrict__ ecnt,
+                                unsigned long long* npairs) {
+  const int64_t cnt = (int64_t)*ecnt;
+  long long mine = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = elist[i];
+    const int u = prop[v];
+    if (v < u && prop[u] == v) {
+      partner[v] = u;
+      partner[u] = v;
+      ++mine;
+    }
+  }
+  block_sum_atomic<256>(mine, npairs);
+}
+
+// Leftovers: key = (centre, v), centre = heaviest neighbour (ties: lowest id).
+__global__ void k_leaf_keys(GView g, const int32_t* __restrict__ left, int64_t nl,
+                            unsigned long long* keys) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = w0; i < nl; i += nw) {
+    const int v = left[i];
+    const int64_t b = g.offs[v], e = g.offs[v + 1];
+    unsigned long long best = 0;
+    for (int64_t j = b + lane; j < e; j += 32) {
+      const unsigned long long w = (unsigned long long)g.ew[j];
+      const unsigned long long key = (w << 32) | (0xffffffffu - (unsigned)g.adj[j]);
+      best = key > best ? key : best;
+    }
+    best = gmax<32>(best, 0xffffffffu);
+    if (lane == 0) {
+      const unsigned long long c = best ? (0xffffffffu - (best & 0xffffffffu)) : 0xffffffffull;
+      keys[i] = (c << 32) | (unsigned)v;
+    }
+  }
+}
+
+// Pair consecutive leftovers under the same centre: (0,1), (2,3), ... of
+// each run of the sorted keys.
+__global__ void k_leaf_pair(const unsigned long long* __restrict__ keys, int64_t nl,
+                            int32_t* partner) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned c = (unsigned)(keys[i] >> 32);
+    if (c == 0xffffffffu) continue;  // isolated vertex
+    if (i > 0 && (unsigned)(keys[i - 1] >> 32) == c) continue;  // not a run start
+    int64_t j = i;
+    while (j + 1 < nl && (unsigned)(keys[j + 1] >> 32) == c) {
+      const int a = (int)(keys[j] & 0xffffffffu), b = (int)(keys[j + 1] & 0xffffffffu);
+      partner[a] = b;
+      partner[b] = a;
+      j += 2;
+      if (j >= nl || (unsigned)(keys[j] >> 32) != c) break;
+    }
+  }
+}
+
+static void leaf_match(Ctx& c, const DGraph& g, int32_t* partner) {
+  const int64_t n = g.n;
+  int32_t* left_p = c.scratch<int32_t>(13, n);
+  DBuf<int64_t> nsel(1, c.stream);
+  {
+    cub::CountingInputIterator<int32_t> it(0);
+    IsFree op{partner};
+    size_t tmp = 0;
+    CK(cub::DeviceSelect::If(nullptr, tmp, it, left_p, nsel.get(), (int)n, op, c.stream));
+    void* p = c.cub_scratch(tmp);
+    launch(c, "th_leftovers", 8.0 * n, [&] {
+      CK(cub::DeviceSelect::If(p, tmp, it, left_p, nsel.get(), (int)n, op, c.stream));
+    });
+  }
+  int64_t nl = 0;
+  d2h(c, &nl, nsel.get(), 1);
+  c.sync();
+  if (nl < 2) return;
+  unsigned long long* k0 = c.scratch<unsigned long long>(14, nl);
+  unsigned long long* k1 = c.scratch<unsigned long long>(16, nl);
+  const GView gv = view(g);
+  launch(c, "leaf_keys", 16.0 * nl, [&] {
+    k_leaf_keys<<<grid_for(c, nl * 32, 256), 256, 0, c.stream>>>(gv, left_p, nl, k0);
+  });
+  size_t tmp = 0;
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k0, k1, (int)nl, 0, 64, c.stream));
+  void* p = c.cub_scratch(tmp);
+  launch(c, "leaf_sort", 32.0 * nl, [&] {
+    CK(cub::DeviceRadixSort::SortKeys(p, tmp, k0, k1, (int)nl, 0, 64, c.stream));
+  });
+  launch(c, "leaf_pair", 16.0 * nl, [&] {
+    k_leaf_pair<<<grid_for(c, nl, 256), 256, 0, c.stream>>>(k1, nl, partner);
+  });
+}
+
+static void device_match_fast(Ctx& c, const DGraph& g, int32_t* partner) {
+  const int64_t n = g.n;
+  launch(c, "fill", 4.0 * n, [&] {
+    k_fill<<<grid_for(c, n, 256), 256, 0, c.stream>>>(partner, n, -1);
+  });
+  if (g.nnz > 0) {
+    int32_t* prop_p = c.scratch<int32_t>(10, n);
+    int32_t* elist_p = c.scratch<int32_t>(11, n);
+    DBuf<unsigned long long> cnt(2, c.stream);
+    const GView gv = view(g);
+    int64_t matched = 0;
+    for (int round = 0; round < 16; ++round) {
+      dzero(c, cnt.get(), 2);
+      launch(c, "propose", (g.unit_ew ? 8.0 : 12.0) * g.nnz + 12.0 * n, [&] {
+        if (g.unit_ew)
+          k_propose_fast<true><<<grid_for(c, n, 256), 256, 0, c.stream>>>(
+              gv, n, partner, prop_p, elist_p, cnt.get(), 0x5bd1e995u * (unsigned)(round + 1));
+        else
+          k_propose_fast<false><<<grid_for(c, n, 256), 256, 0, c.stream>>>(
+              gv, n, partner, prop_p, elist_p, cnt.get(), 0x5bd1e995u * (unsigned)(round + 1));
+      });
+      launch(c, "accept", 12.0 * n, [&] {
+        k_accept_mutual<<<grid_for(c, n, 256), 256, 0, c.stream>>>(prop_p, partner, elist_p,
+                                                                   cnt.get(), cnt.get() + 1);
+      });
+      unsigned long long h[2];
+      d2h(c, h, cnt.get(), 2);
+      c.sync();
+      matched += 2 * (int64_t)h[1];
+      // stop when the free proposers are exhausted or a round adds < 1 % of n
+      if (h[0] == 0 || (int64_t)h[1] * 100 < n - matched || (int64_t)h[1] * 200 < n) break;
+    }
+    leaf_match(c, g, partner);
   }
   launch(c, "singletons", 8.0 * n, [&] {
     k_singletons<<<grid_for(c, n, 256), 256, 0, c.stream>>>(partner, n);
@@ -1122,7 +1336,8 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
 }
 
 // build_hierarchy (coarsen.py:141-161; MAX_LEVELS 64, stagnation 0.95 twice)
-void device_build_hierarchy(Ctx& c, const DGraph& g0, int64_t target, Hierarchy& h) {
+void device_build_hierarchy(Ctx& c, const DGraph& g0, int64_t target, Hierarchy& h,
+                            bool fast) {
   static const bool dbg = getenv("JET_COARSEN_TIMES") && getenv("JET_COARSEN_TIMES")[0] == '1';
   h.base = &g0;
   h.owned.clear();
@@ -1137,7 +1352,10 @@ void device_build_hierarchy(Ctx& c, const DGraph& g0, int64_t target, Hierarchy&
       c.sync();
       t0 = wall_s();
     }
-    device_match(c, *fine, partner.get());
+    if (fast)
+      device_match_fast(c, *fine, partner.get());
+    else
+      device_match(c, *fine, partner.get());
     if (dbg) {
       c.sync();
       t1 = wall_s();

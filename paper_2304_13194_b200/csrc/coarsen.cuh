@@ -19,6 +19,9 @@ struct Hierarchy {
 void device_match(Ctx& c, const DGraph& g, int32_t* partner);
 std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* partner,
                                         int32_t* vmap);
-void device_build_hierarchy(Ctx& c, const DGraph& g0, int64_t target, Hierarchy& h);
+// fast: throughput-mode matching (device_match_fast), else the reference's
+// exact matching semantics.
+void device_build_hierarchy(Ctx& c, const DGraph& g0, int64_t target, Hierarchy& h,
+                            bool fast = false);
 
 }  // namespace jet

@@ -180,7 +180,7 @@ void run_partition(Ctx& c, const DGraph& g0, const jet_config& cfg, int32_t* par
   const int64_t target = std::max<int64_t>(std::max<int64_t>(cfg.coarse_target, 2LL * k), 32);
   Hierarchy h;
   c.prof_tag = "coarsen:";
-  device_build_hierarchy(c, g0, target, h);
+  device_build_hierarchy(c, g0, target, h, cfg.deterministic == 0);
   c.prof_tag.clear();
   c.sync();
   const double t1 = now_s();

@@ -47,6 +47,7 @@ struct LevelCtl {
   int kind;  // 0 stop, 1 Jetlp, 2 weak, 3 strong
   int locks_all_clear, stop, copy_keep, abort;
   int nover, nvalid, nb, nch, slot_min, rho;
+  int tail_max;  // largest (part, bucket) group of the evicted set
   unsigned long long rejects;
   unsigned long long pcg_state_hi, pcg_state_lo, pcg_inc_hi, pcg_inc_lo;
 };
@@ -93,6 +94,7 @@ struct LevelArgs {
   int32_t* thr;
   int32_t* draws;
   unsigned long long* gscratch;
+  unsigned* tailbuf;  // >= 3 * k * nb_max + 1 + n words (group ranking of the tail)
   long long limit, sigma, W, min_vw;
   long long c_num, c_den;
   double c_f;
@@ -423,11 +425,186 @@ __device__ void lv_sweep(const LevelArgs& A, MakeArgs mk, const int32_t* const* 
   __syncthreads();
 }
 
+// Grid-wide bitonic sort of the evicted keys (part rank, bucket, id) when
+// they outnumber one block's shared memory: chunks of C keys are sorted in
+// shared memory, then for every merge size the strides >= C run as global
+// compare-exchange passes and the strides < C inside each chunk again.
+// A one-block sort of 10^5 keys from global memory took ~0.8 ms per pass.
+template <class GSync>
+__device__ void lv_grid_sort(const LevelArgs& A, int L, int P2, int nb, unsigned long long* sm,
+                             GSync gsync, int64_t t0, int64_t nt) {
+  constexpr int C = LV_TAIL_SMEM;
+  unsigned long long* keys = A.gscratch;
+  for (int64_t i = t0; i < P2; i += nt) {
+    unsigned long long key = ~0ull;
+    if (i < L) {
+      const int v = A.evict[i];
+      const unsigned long long grp =
+          (unsigned long long)A.opidx[A.parts[v]] * (unsigned)nb + (unsigned)A.rkey[v];
+      key = (grp << 32) | (unsigned)v;
+    }
+    keys[i] = key;
+  }
+  gsync();
+  const int nch = P2 / C;
+  auto local = [&](int size_lo, int size_hi, int stride_hi) {
+    // sizes [size_lo, size_hi] (doubling); strides from min(size/2, stride_hi) down to 1
+    for (int ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+      unsigned long long* g = keys + (size_t)ch * C;
+      for (int i = threadIdx.x; i < C; i += blockDim.x) sm[i] = g[i];
+      __syncthreads();
+      for (int size = size_lo; size <= size_hi; size <<= 1) {
+        for (int stride = min(size >> 1, stride_hi); stride > 0; stride >>= 1) {
+          for (int i = threadIdx.x; i < C; i += blockDim.x) {
+            const int j = i ^ stride;
+            if (j > i) {
+              const bool asc = (((int64_t)ch * C + i) & size) == 0;
+              const unsigned long long x = sm[i], y = sm[j];
+              if ((x > y) == asc) {
+                sm[i] = y;
+                sm[j] = x;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (int i = threadIdx.x; i < C; i += blockDim.x) g[i] = sm[i];
+      __syncthreads();
+    }
+  };
+  local(2, C, C);
+  gsync();
+  for (int size = 2 * C; size <= P2; size <<= 1) {
+    for (int stride = size >> 1; stride >= C; stride >>= 1) {
+      for (int64_t i = t0; i < P2; i += nt) {
+        const int64_t j = i ^ stride;
+        if (j > i) {
+          const bool asc = (i & size) == 0;
+          const unsigned long long x = keys[i], y = keys[j];
+          if ((x > y) == asc) {
+            keys[i] = y;
+            keys[j] = x;
+          }
+        }
+      }
+      gsync();
+    }
+    local(size, size, C >> 1);
+    gsync();
+  }
+}
+
+// Order of the evicted set without a sort: key (g, v) with group g = (part
+// rank, bucket). rank(v) = #evicted in groups < g + #evicted in g with a
+// smaller id. Groups are counted, scanned (block 0), the members scattered
+// into their group segment, and each member ranks itself inside its
+// segment (groups are tiny: bucket = (slot, id mod rho)). Writes the keys in
+// sorted order to gscratch. Returns false (uniformly) when a group is too
+// large for the quadratic in-segment ranking; the caller then sorts.
+constexpr int LV_TAIL_GROUP_MAX = 512;
+template <class GSync>
+__device__ bool lv_tail_rank(const LevelArgs& A, int L, int nb, GSync gsync, int64_t t0,
+                             int64_t nt) {
+  LevelCtl* C = A.C;
+  const int G = ldv(&C->nover) * nb;
+  unsigned* hist = A.tailbuf;
+  unsigned* base = hist + G;      // per-block exclusive prefix, G
+  unsigned* fill = base + G;      // G
+  unsigned* bpre = fill + G;      // per-block totals -> exclusive prefix, gridDim.x
+  int32_t* seg = reinterpret_cast<int32_t*>(bpre + gridDim.x + 1);
+  for (int64_t i = t0; i < G; i += nt) {
+    hist[i] = 0;
+    fill[i] = 0;
+  }
+  if (t0 == 0) C->tail_max = 0;
+  gsync();
+  const int64_t lim = ((int64_t)L + 31) & ~31LL;
+  for (int64_t i = t0; i < lim; i += nt) {
+    int g = -1;
+    if (i < L) {
+      const int v = A.evict[i];
+      g = A.opidx[A.parts[v]] * nb + A.rkey[v];
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, g);
+    if (g >= 0 && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[g], __popc(peers));
+  }
+  gsync();
+  // scan of the group counts: every block scans its slice of G
+  typedef cub::BlockScan<unsigned, LV_BLOCK> BScan;
+  typedef cub::BlockReduce<unsigned, LV_BLOCK> BRed;
+  __shared__ typename BScan::TempStorage ts;
+  __shared__ typename BRed::TempStorage tr;
+  __shared__ unsigned s_run;
+  const int per = (G + gridDim.x - 1) / gridDim.x;
+  const int lo = min(G, (int)blockIdx.x * per), hi = min(G, lo + per);
+  if (threadIdx.x == 0) s_run = 0;
+  __syncthreads();
+  unsigned mx = 0;
+  for (int b0 = lo; b0 < hi; b0 += LV_BLOCK) {
+    const int i = b0 + threadIdx.x;
+    const unsigned x = i < hi ? hist[i] : 0u;
+    mx = max(mx, x);
+    unsigned ex, tot;
+    BScan(ts).ExclusiveSum(x, ex, tot);
+    const unsigned run = s_run;
+    if (i < hi) base[i] = run + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) s_run = run + tot;
+    __syncthreads();
+  }
+  mx = BRed(tr).Reduce(mx, cub::Max());
+  if (threadIdx.x == 0) {
+    bpre[blockIdx.x] = s_run;
+    atomicMax(&C->tail_max, (int)mx);
+  }
+  gsync();
+  if (ldv(&C->tail_max) > LV_TAIL_GROUP_MAX) return false;
+  if (blockIdx.x == 0) {  // exclusive scan of the block totals (gridDim.x <= 2 * 148)
+    unsigned run = 0;
+    for (int b0 = 0; b0 < (int)gridDim.x; b0 += LV_BLOCK) {
+      const int i = b0 + threadIdx.x;
+      const unsigned x = i < (int)gridDim.x ? bpre[i] : 0u;
+      unsigned ex, tot;
+      BScan(ts).ExclusiveSum(x, ex, tot);
+      __syncthreads();
+      if (i < (int)gridDim.x) bpre[i] = run + ex;
+      run += tot;
+    }
+  }
+  gsync();
+  auto gbase = [&](int g) { return base[g] + bpre[g / per]; };
+  for (int64_t i = t0; i < L; i += nt) {
+    const int v = A.evict[i];
+    const int g = A.opidx[A.parts[v]] * nb + A.rkey[v];
+    seg[gbase(g) + atomicAdd(&fill[g], 1u)] = v;
+  }
+  gsync();
+  for (int64_t i = t0; i < L; i += nt) {
+    const int v = A.evict[i];
+    const int g = A.opidx[A.parts[v]] * nb + A.rkey[v];
+    const unsigned b = gbase(g), e = b + hist[g];
+    unsigned r = 0;
+    for (unsigned j = b; j < e; ++j) r += (unsigned)(seg[j] < v);
+    A.gscratch[b + r] = ((unsigned long long)g << 32) | (unsigned)v;
+  }
+  gsync();
+  return true;
+}
+
 // ---------------------------------------------------------------- kernel
 template <bool UNIT>
 __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) {
   extern __shared__ unsigned long long lv_smem[];
   cg::grid_group grid = cg::this_grid();
+  // a one-block grid (small levels) synchronises with __syncthreads, which
+  // also orders global memory within the block; the grid barrier protocol
+  // costs ~1.5 us per phase even for one block
+  const bool one_block = gridDim.x == 1;
+  auto gsync = [&]() {
+    if (one_block) __syncthreads();
+    else grid.sync();
+  };
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nt = (int64_t)gridDim.x * blockDim.x;
   const int64_t w0 = t0 >> 5, nw = nt >> 5;
@@ -450,7 +627,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
   while (true) {
     pc.mark(15);
     if (blockIdx.x == 0) lv_decide(A);
-    grid.sync();
+    gsync();
     pc.mark(0);
     const int kind = ldv(&C->kind);
     pc.kind = kind;
@@ -481,7 +658,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       };
       // per-warp tables start at lv_smem + warp * per inside agg_warp
       lv_sweep<LpOp, UNIT>(A, mk, nullptr, nullptr, lv_smem, w0, nw, acc);
-      grid.sync();
+      gsync();
       pc.mark(1);
       if (A.afterburner) {
         AbArgs ab{};
@@ -494,7 +671,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
         long long nmv = 0;
         afterburner_rows<UNIT>(ab, A.g, cands, A.seg, w0, nw, &wk.v[2], &wk.v[3], &nmv);
         block_sum_atomic_any(nmv, A.ctr + CTR_NMOVE);
-        grid.sync();
+        gsync();
         pc.mark(2);
       }
     } else {
@@ -507,7 +684,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       if (!strong) lv_draws(A, t0, nt);
       rb_collect(A.parts, A.opidx, A.g.offs, A.tm, A.n, A.cand_lists, A.seg, A.ctr + CTR_CAND, t0, nt,
                  &wk.v[0], &wk.v[1]);
-      grid.sync();
+      gsync();
       pc.mark(3);
       RbOp::Args ra{};
       ra.parts = A.parts;
@@ -529,29 +706,53 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       ra.Hs = A.Hs;
       lv_sweep<RbOp, UNIT>(A, [&](int) { return ra; }, clists, A.ctr + CTR_CAND, lv_smem, w0, nw,
                            acc);
-      grid.sync();
+      gsync();
       pc.mark(4);
       const RbSel s = lv_sel(A);
       for (int64_t op = w0; op < nover; op += nw)
         rb_scan_warp((int)op, A.H, A.Hs, nb, ldv(&C->rho), A.deficit, A.bstar, A.cum_before);
-      grid.sync();
+      gsync();
       pc.mark(5);
       rb_chunk(s, A.rcand, A.ctr + CTR_RCAND, t0, nt);
-      grid.sync();
+      gsync();
       pc.mark(6);
       for (int64_t op = w0; op < nover; op += nw)
         rb_find_warp((int)op, s, A.deficit, A.required, A.cum_before, A.opart, A.n, nb, A.thr);
-      grid.sync();
+      gsync();
       pc.mark(7);
       rb_select(s, A.rcand, A.ctr + CTR_RCAND, A.rbest, strong, 1, A.evict, A.ctr + CTR_EVICT,
                 A.mv, A.g.offs, A.tm, A.move_lists, A.seg, A.ctr + CTR_MOVE, t0, nt);
-      grid.sync();
+      gsync();
       pc.mark(8);
-      if (blockIdx.x == 0) {
-        if (!strong && *(const volatile unsigned long long*)&C->rejects) {
-          if (threadIdx.x == 0) lv_draws_fixup(A);
-          __syncthreads();
+      const int Lev = (int)*(const volatile unsigned long long*)(A.ctr + CTR_EVICT);
+      int P2ev = 1;
+      while (P2ev < Lev) P2ev <<= 1;
+      if (!strong && *(const volatile unsigned long long*)&C->rejects) {
+        // a Lemire rejection shifted the draw stream: redo it sequentially
+        if (blockIdx.x == 0 && threadIdx.x == 0) lv_draws_fixup(A);
+        gsync();
+      }
+      pc.mark(13);
+      // large evicted sets: order them with the whole grid, and for weak
+      // passes assign the random destinations with the whole grid too
+      const bool big_tail = P2ev > LV_TAIL_SMEM / 4;
+      if (big_tail && !lv_tail_rank(A, Lev, nb, gsync, t0, nt))
+        lv_grid_sort(A, Lev, P2ev, nb, lv_smem, gsync, t0, nt);
+      pc.mark(12);
+      if (big_tail && !strong) {
+        const int nvalid = ldv(&C->nvalid);
+        const int64_t lim = ((int64_t)Lev + 31) & ~31LL;
+        for (int64_t i = t0; i < lim; i += nt) {
+          int v = 0, t = -1;
+          if (i < Lev) {
+            v = (int)(A.gscratch[i] & 0xffffffffu);
+            A.mv[v] = A.valid_list[nvalid > 1 ? A.draws[i] : 0];
+            t = A.tm(A.g.offs[v + 1] - A.g.offs[v]);
+          }
+          for (int tt = 0; tt < NBINS; ++tt)
+            warp_append(t == tt, v, A.move_lists + A.seg.b[tt], A.ctr + CTR_MOVE + tt);
         }
+      } else if (blockIdx.x == 0) {
         RbTail tl{};
         tl.evict = A.evict;
         tl.evict_cnt = A.ctr + CTR_EVICT;
@@ -573,9 +774,10 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
         tl.move_cnt = A.ctr + CTR_MOVE;
         tl.smem_cap = LV_TAIL_SMEM;
         tl.gscratch = A.gscratch;
+        tl.presorted = big_tail;
         rb_tail(tl, lv_smem);
       }
-      grid.sync();
+      gsync();
       pc.mark(9);
     }
     // ---- apply (conn.py:215-254)
@@ -586,7 +788,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
                              &wk.v[4], &wk.v[5]);
       block_sum_atomic_any(d, A.ctr + CTR_CUT2D);
     }
-    grid.sync();
+    gsync();
     pc.mark(10);
     {
       CommitArgs ca{};
@@ -601,7 +803,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       apply_commit_rows(ca, t0, nt);
     }
     if (blockIdx.x == 0) lv_bookkeep(A);
-    grid.sync();
+    gsync();
     pc.mark(11);
     if (ldv(&C->copy_keep))
       for (int64_t v = t0; v < A.n; v += nt) A.keep[v] = A.parts[v];
@@ -624,6 +826,7 @@ struct LevelScratch : CtxExt {
   DBuf<long long> keep_pw;
   DBuf<int32_t> backup;
   DBuf<unsigned long long> gscratch;
+  DBuf<unsigned> tailbuf;
   DBuf<unsigned long long> work;
 };
 
@@ -652,7 +855,7 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   S.ctl.ensure(1, c.stream);
   S.keep_pw.ensure(k, c.stream);
   S.backup.ensure(g.n, c.stream);
-  S.gscratch.ensure(2 * (size_t)g.n + 2 * LV_BLOCK + 64, c.stream);
+  S.gscratch.ensure(4 * (size_t)g.n + 2 * LV_BLOCK + 2 * LV_TAIL_SMEM + 64, c.stream);
   S.work.ensure(8, c.stream);
   dzero(c, S.work.get(), 8);
   keep.ensure(g.n, c.stream);
@@ -660,6 +863,7 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   const int64_t nb_max = (int64_t)slot_span * rho;
   const int64_t nch = ((g.n + rho - 1) / rho + 31) / 32;
   w.H.ensure((size_t)k * nb_max, c.stream);
+  S.tailbuf.ensure(3 * (size_t)k * nb_max + 2048 + (size_t)g.n, c.stream);
   w.Hs.ensure((size_t)k * slot_span, c.stream);
   w.CH.ensure((size_t)k * nch, c.stream);
   w.draws.ensure(g.n + LV_DRAW_SLACK + 64, c.stream);
@@ -737,6 +941,7 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   A.thr = w.thr.get();
   A.draws = w.draws.get();
   A.gscratch = S.gscratch.get();
+  A.tailbuf = S.tailbuf.get();
   A.limit = cfg.limit;
   A.sigma = cfg.sigma;
   A.W = g.total_vw;
@@ -797,7 +1002,7 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
     c.sync();
     static const char* names[16] = {"decide", "lp_sweep", "afterburner", "rb_collect", "rb_stats",
                                     "rb_scan", "rb_chunk", "rb_find", "rb_select", "rb_tail",
-                                    "apply_delta", "commit+keep", "", "", "", "keep_copy"};
+                                    "apply_delta", "commit+keep", "tail_sort", "draw_fixup", "", "keep_copy"};
     static const char* kinds[4] = {"stop", "lp", "weak", "strong"};
     const int cnt[4] = {1, h.lp, h.weak, h.strong};
     for (int kd = 1; kd < 4; ++kd) {

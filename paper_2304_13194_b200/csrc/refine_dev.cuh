@@ -1078,6 +1078,7 @@ struct RbTail {
   unsigned long long* move_cnt;
   int smem_cap;                     // keys that fit the caller's shared buffer
   unsigned long long* gscratch;     // >= 2 * P2 + blockDim words, for larger sets
+  int presorted;                    // keys already sorted in gscratch (grid sort)
 };
 
 static __device__ void rb_tail(const RbTail& a, unsigned long long* sk_smem) {
@@ -1088,8 +1089,9 @@ static __device__ void rb_tail(const RbTail& a, unsigned long long* sk_smem) {
   const int L = (int)*(const volatile unsigned long long*)a.evict_cnt;
   int P2 = 1;
   while (P2 < L) P2 <<= 1;
-  unsigned long long* sk = (P2 <= a.smem_cap || a.gscratch == nullptr) ? sk_smem : a.gscratch;
-  for (int i = tid; i < P2; i += blockDim.x) {
+  unsigned long long* sk =
+      (!a.presorted && (P2 <= a.smem_cap || a.gscratch == nullptr)) ? sk_smem : a.gscratch;
+  for (int i = tid; i < P2 && !a.presorted; i += blockDim.x) {
     unsigned long long key = ~0ull;
     if (i < L) {
       const int v = a.evict[i];
@@ -1100,7 +1102,7 @@ static __device__ void rb_tail(const RbTail& a, unsigned long long* sk_smem) {
     sk[i] = key;
   }
   __syncthreads();
-  for (int size = 2; size <= P2; size <<= 1) {
+  for (int size = 2; size <= P2 && !a.presorted; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       for (int i = tid; i < P2; i += blockDim.x) {
         const int j = i ^ stride;
@@ -1117,12 +1119,17 @@ static __device__ void rb_tail(const RbTail& a, unsigned long long* sk_smem) {
     }
   }
   if (!a.strong) {
-    for (int i = tid; i < L; i += blockDim.x) {
-      const int v = (int)(sk[i] & 0xffffffffu);
-      a.mv[v] = a.valid_list[a.draws[i]];
-      const int t = a.tm(a.offs[v + 1] - a.offs[v]);
-      const unsigned long long q = atomicAdd(a.move_cnt + t, 1ull);
-      a.move_lists[a.mseg.b[t] + q] = v;
+    // warp-aggregated appends: one atomic per warp and tier, not per move
+    const int lim = (L + 31) & ~31;
+    for (int i = tid; i < lim; i += blockDim.x) {
+      int v = 0, t = -1;
+      if (i < L) {
+        v = (int)(sk[i] & 0xffffffffu);
+        a.mv[v] = a.valid_list[a.draws[i]];
+        t = a.tm(a.offs[v + 1] - a.offs[v]);
+      }
+      for (int tt = 0; tt < NBINS; ++tt)
+        warp_append(t == tt, v, a.move_lists + a.mseg.b[tt], a.move_cnt + tt);
     }
     return;
   }
@@ -1174,12 +1181,15 @@ static __device__ void rb_tail(const RbTail& a, unsigned long long* sk_smem) {
       if (tid >= pos && tid < lim && !fits) atomicMin(&s_first, tid);
       __syncthreads();
       const int e = s_first;
-      if (fits) {
-        const int v = (int)(sk[i] & 0xffffffffu);
-        a.mv[v] = a.valid_list[s_di];
-        const int t = a.tm(a.offs[v + 1] - a.offs[v]);
-        const unsigned long long q = atomicAdd(a.move_cnt + t, 1ull);
-        a.move_lists[a.mseg.b[t] + q] = v;
+      {
+        int v = 0, t = -1;
+        if (fits) {
+          v = (int)(sk[i] & 0xffffffffu);
+          a.mv[v] = a.valid_list[s_di];
+          t = a.tm(a.offs[v + 1] - a.offs[v]);
+        }
+        for (int tt = 0; tt < NBINS; ++tt)
+          warp_append(t == tt, v, a.move_lists + a.mseg.b[tt], a.move_cnt + tt);
       }
       __syncthreads();
       if (e >= lim) {

@@ -3,7 +3,9 @@ per-kernel-class CUDA-event profile."""
 import sys, time, json
 sys.path.insert(0, '.')
 import numpy as np
+import os
 import paper_2304_13194_b200 as J
+DET = os.environ.get('JET_MODE', 'det') == 'det'
 from paper_2304_13194_b200 import generators as gen, _lib
 from paper_2304_13194_b200.driver import partition_resident
 
@@ -12,7 +14,7 @@ k = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 t = time.perf_counter(); g = gen.grid27_graph(N); print("gen", time.perf_counter() - t, g.n, g.m, flush=True)
 ctx = _lib.Context.default()
 dg = _lib.DeviceGraph.upload(g, ctx)
-cfg = J.RefinerConfig(k=k, imbalance=0.03, seed=0)
+cfg = J.RefinerConfig(k=k, imbalance=0.03, seed=0, deterministic=DET)
 for rep in range(3):
     ctx.profile(rep == 2)
     ctx.profile_reset()

@@ -1,7 +1,9 @@
 """Per-level x per-kernel event profile of one partition."""
 import sys, collections
 sys.path.insert(0, '.')
+import os
 import paper_2304_13194_b200 as J
+DET = os.environ.get('JET_MODE', 'det') == 'det'
 from paper_2304_13194_b200 import generators as gen, _lib
 from paper_2304_13194_b200.driver import partition_resident
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 128
@@ -9,7 +11,7 @@ k = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 g = gen.grid27_graph(N)
 ctx = _lib.Context.default()
 dg = _lib.DeviceGraph.upload(g, ctx)
-cfg = J.RefinerConfig(k=k, imbalance=0.03, seed=0)
+cfg = J.RefinerConfig(k=k, imbalance=0.03, seed=0, deterministic=DET)
 partition_resident(dg, g, cfg, want_parts=False)
 ctx.profile(True); ctx.profile_only("@levels"); ctx.profile_reset()
 parts, pw, st = partition_resident(dg, g, cfg, want_parts=False)

@@ -9,7 +9,7 @@ from paper_2304_13194_b200 import generators as gen, ops
 
 cu = ctypes.CDLL("libcuda.so.1")
 g = gen.grid27_graph(128)
-cfg = J.RefinerConfig(k=64, imbalance=0.03, seed=0)
+cfg = J.RefinerConfig(k=64, imbalance=0.03, seed=0, deterministic=True)
 res = J.partition(g, cfg)
 p0 = res.state.parts.copy()
 h = J.build_hierarchy(g, 128)

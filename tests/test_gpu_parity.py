@@ -124,7 +124,7 @@ def test_jet_refine(golden):
         g = graph_of(d, f"p{i}_")
         k, seed, ab, lk = (int(x) for x in d[f"p{i}_cfg"])
         cfg = J.RefinerConfig(k=k, imbalance=float(d[f"p{i}_imb"][0]), seed=seed,
-                              afterburner=bool(ab), locking=bool(lk))
+                              afterburner=bool(ab), locking=bool(lk), deterministic=True)
         st = J.PartitionState.from_parts(g, d[f"p{i}_rparts_in"], k)
         out, stats = J.jet_refine(g, st, cfg, finest=True, seed_path=(0,))
         exp = d[f"p{i}_rstats"].tolist()
@@ -140,7 +140,7 @@ def test_partition_pipeline(golden):
         g = graph_of(d, f"p{i}_")
         k, seed, ab, lk = (int(x) for x in d[f"p{i}_cfg"])
         cfg = J.RefinerConfig(k=k, imbalance=float(d[f"p{i}_imb"][0]), seed=seed,
-                              afterburner=bool(ab), locking=bool(lk))
+                              afterburner=bool(ab), locking=bool(lk), deterministic=True)
         res = J.partition(g, cfg)
         assert [lv["iterations"] for lv in res.metrics["levels"]] == d[f"p{i}_iters"].tolist(), i
         assert res.state.cutsize == int(d[f"p{i}_cut"][0]), i
@@ -154,7 +154,7 @@ def test_oracle_config_grid256(golden):
     d = golden("oracle_grid256")
     g = gen.grid_graph(256, 256)
     assert np.array_equal(J.match_vertices(g), d["match"].astype(np.int64))
-    res = J.partition(g, J.RefinerConfig(k=8, imbalance=0.03, seed=0))
+    res = J.partition(g, J.RefinerConfig(k=8, imbalance=0.03, seed=0, deterministic=True))
     assert res.state.cutsize == 1183 == int(d["cut"][0])
     assert res.state.part_weights.tolist() == d["pw"].tolist()
     assert [lv["iterations"] for lv in res.metrics["levels"]] == d["iters"].tolist()
