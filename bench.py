@@ -55,6 +55,8 @@ class ClockSampler:
         self.lines = []
 
     def __enter__(self):
+        if os.environ.get("JET_BENCH_NO_CLOCKS") == "1":  # diagnostics only
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={CLOCK_FIELDS}",
