@@ -139,6 +139,20 @@ int jet_graph_download(jet_ctx* ctx, const jet_graph* g, int64_t* row_offsets,
                        int64_t* vertex_weights);
 void jet_graph_free(jet_graph* g);
 
+/* ---- on-device benchmark inputs (generators.py, graph.py:132-200) ---- */
+/* The reference's rmat_graph(scale, edge_factor, seed, probs)
+ * (generators.py:32-55) and geometric_graph(n, radius, seed)
+ * (generators.py:58-97), each followed by its preprocess (graph.py:132-200:
+ * self loops dropped, symmetrised, duplicates merged, largest connected
+ * component renumbered), generated on the device. The result is identical to
+ * the reference's graph for the same arguments (numpy's PCG64 stream is
+ * replayed by jump-ahead). probs4 may be NULL for (0.57, 0.19, 0.19, 0.05).
+ * Limits: 2 * 2^scale * edge_factor < 2^31; geometric n < 2^31. */
+int jet_generate_rmat(jet_ctx* ctx, int32_t scale, int32_t edge_factor, uint64_t seed,
+                      const double* probs4, jet_graph** out);
+int jet_generate_geometric(jet_ctx* ctx, int64_t n, double radius, uint64_t seed,
+                           jet_graph** out);
+
 /* ---- metrics ---------------------------------------------------------- */
 /* cutsize(graph, parts)  graph.py:215-221 */
 int jet_cutsize(jet_ctx* ctx, const jet_graph* g, const int64_t* parts,

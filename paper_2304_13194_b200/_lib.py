@@ -92,6 +92,8 @@ _SIGS = {
     "jet_graph_info": (C.c_int, [P, P, P, P]),
     "jet_graph_download": (C.c_int, [P, P, P, P, P, P]),
     "jet_graph_free": (None, [P]),
+    "jet_generate_rmat": (C.c_int, [P, i32, i32, C.c_uint64, P, C.POINTER(P)]),
+    "jet_generate_geometric": (C.c_int, [P, i64, C.c_double, C.c_uint64, C.POINTER(P)]),
     "jet_cutsize": (C.c_int, [P, P, P, P]),
     "jet_part_weights": (C.c_int, [P, P, P, i32, P]),
     "jet_match": (C.c_int, [P, P, P]),

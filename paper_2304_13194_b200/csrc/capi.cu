@@ -90,6 +90,37 @@ int jet_graph_upload(jet_ctx* ctx, int64_t n, const int64_t* row_offsets, const 
   API_END
 }
 
+int jet_generate_rmat(jet_ctx* ctx, int32_t scale, int32_t edge_factor, uint64_t seed,
+                      const double* probs4, jet_graph** out) {
+  API_BEGIN
+  Ctx& c = C(ctx);
+  JET_REQUIRE(out, JET_EINVAL, "out is NULL");
+  const double def[4] = {0.57, 0.19, 0.19, 0.05};
+  auto g = device_rmat(c, scale, edge_factor, seed, probs4 ? probs4 : def);
+  jet_graph* jg = new jet_graph();
+  jg->g = std::move(g);
+  jg->device = c.device;
+  jg->ctx = &c;
+  ctx_retain(&c);
+  *out = jg;
+  API_END
+}
+
+int jet_generate_geometric(jet_ctx* ctx, int64_t n, double radius, uint64_t seed,
+                           jet_graph** out) {
+  API_BEGIN
+  Ctx& c = C(ctx);
+  JET_REQUIRE(out, JET_EINVAL, "out is NULL");
+  auto g = device_rgg(c, n, radius, seed);
+  jet_graph* jg = new jet_graph();
+  jg->g = std::move(g);
+  jg->device = c.device;
+  jg->ctx = &c;
+  ctx_retain(&c);
+  *out = jg;
+  API_END
+}
+
 int jet_graph_info(const jet_graph* g, int64_t* n, int64_t* nnz, int64_t* total_vertex_weight) {
   API_BEGIN
   const DGraph& d = G(g);

@@ -54,5 +54,9 @@ void upload_i64_as_i32(Ctx& c, const int64_t* host, int64_t n, int32_t* dst,
                        long long lo, long long hi, const char* what);
 void download_i32_as_i64(Ctx& c, const int32_t* dsrc, int64_t n, int64_t* host);
 void set_last_error(const std::string& s);
+// gen.cu: the reference's generators + preprocess, on the device
+std::unique_ptr<DGraph> device_rmat(Ctx& c, int scale, int edge_factor, uint64_t seed,
+                                    const double probs[4]);
+std::unique_ptr<DGraph> device_rgg(Ctx& c, int64_t n, double radius, uint64_t seed);
 
 }  // namespace jet

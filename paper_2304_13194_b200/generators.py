@@ -1,7 +1,9 @@
-"""Benchmark / test inputs (host numpy). Graph generation is outside the
-partitioner's hot path; these build the same CSR the
-reference's generators produce for lattices, without its preprocess pass
-(a lattice is connected and already clean, so preprocess is the identity).
+"""Benchmark / test inputs. Graph generation is outside the partitioner's
+hot path. Lattices are built on the host (numpy): the
+same CSR the reference's generators produce, without its preprocess pass (a
+lattice is connected and already clean, so preprocess is the identity).
+R-MAT and random geometric graphs are generated on the device (csrc/gen.cu),
+bit-identical to the reference's rmat_graph / geometric_graph + preprocess.
 """
 
 from __future__ import annotations
@@ -52,3 +54,58 @@ def grid27_graph(nx: int, ny: int | None = None, nz: int | None = None, dtype=np
     offs = [(a, b, c) for a in (-1, 0, 1) for b in (-1, 0, 1) for c in (-1, 0, 1)
             if (a, b, c) != (0, 0, 0)]
     return _stencil_graph((nx, ny, nz), offs, dtype)
+
+
+# ---------------------------------------------------------------------------
+# Random inputs, generated on the device (csrc/gen.cu): the same graphs the
+# reference's rmat_graph / geometric_graph + preprocess produce
+# (generators.py:32-97, graph.py:132-200), replayed from numpy's PCG64 stream.
+
+def rmat_device(scale: int, edge_factor: int = 8, seed: int = 0,
+                probs=(0.57, 0.19, 0.19, 0.05), ctx=None):
+    """R-MAT graph (largest component) resident on the device."""
+    import ctypes as C
+    from . import _lib
+    ctx = ctx or _lib.Context.default()
+    pr = np.ascontiguousarray(probs, dtype=np.float64)
+    if pr.shape != (4,):
+        raise ValueError("probs must have four entries")
+    h = C.c_void_p()
+    _lib.check(_lib.lib().jet_generate_rmat(ctx.handle, int(scale), int(edge_factor),
+                                            int(seed), _lib.ptr(pr), C.byref(h)))
+    return _lib.DeviceGraph(ctx, h)
+
+
+def geometric_device(n: int, radius: float, seed: int = 0, ctx=None):
+    """Random geometric graph on the unit square (largest component), on the device."""
+    import ctypes as C
+    from . import _lib
+    ctx = ctx or _lib.Context.default()
+    h = C.c_void_p()
+    _lib.check(_lib.lib().jet_generate_geometric(ctx.handle, int(n), float(radius), int(seed),
+                                                 C.byref(h)))
+    return _lib.DeviceGraph(ctx, h)
+
+
+def _host(dg) -> Graph:
+    offs, adj, ew, vw = dg.download()
+    return Graph(offs, adj, ew, vw)
+
+
+def rmat_graph(scale: int, edge_factor: int = 8, seed: int = 0,
+               probs=(0.57, 0.19, 0.19, 0.05)) -> Graph:
+    """The reference's rmat_graph (generators.py:32-55), generated on the device."""
+    dg = rmat_device(scale, edge_factor, seed, probs)
+    try:
+        return _host(dg)
+    finally:
+        dg.free()
+
+
+def geometric_graph(n: int, radius: float, seed: int = 0) -> Graph:
+    """The reference's geometric_graph (generators.py:58-97), generated on the device."""
+    dg = geometric_device(n, radius, seed)
+    try:
+        return _host(dg)
+    finally:
+        dg.free()
