@@ -36,6 +36,7 @@ constexpr int LV_BLOCK = LV_BLOCK_SIZE;
 constexpr int LV_TAIL_SMEM = 8192;  // evicted keys sorted in shared memory
 constexpr int LV_DRAW_SLACK = 64;
 constexpr int64_t LV_ROWS_PER_BLOCK = 512;
+constexpr int64_t LV_ENTRIES_PER_BLOCK = 16384;  // dense coarse levels (R-MAT)
 constexpr int LV_RB = 16;  // rows per warp batch in the staged short-row sweep
 
 struct LevelCtl {
@@ -49,6 +50,7 @@ struct LevelCtl {
   int nover, nvalid, nb, nch, slot_min, rho;
   int tail_max;  // largest (part, bucket) group of the evicted set
   unsigned long long rejects;
+  long long rej_pos[32];  // word positions of Lemire rejections (first 32)
   unsigned long long pcg_state_hi, pcg_state_lo, pcg_inc_hi, pcg_inc_lo;
 };
 
@@ -360,9 +362,43 @@ __device__ void lv_draws(const LevelArgs& A, int64_t t0, int64_t nt) {
   g.inc = ((du128)*(const volatile unsigned long long*)&C->pcg_inc_hi << 64) |
           *(const volatile unsigned long long*)&C->pcg_inc_lo;
   const uint32_t excl = (uint32_t)nvalid, thr = (0xffffffffu - (uint32_t)(nvalid - 1)) % excl;
-  for (int64_t j = t0; j < D; j += nt) {
+  // words [D, D + slack) are only screened: a rejection before D shifts the
+  // stream onto them
+  for (int64_t j = t0; j < D + LV_DRAW_SLACK; j += nt) {
     const uint64_t m = (uint64_t)pcg_word(g, (uint64_t)j) * excl;
-    if ((uint32_t)m < excl && (uint32_t)m < thr) atomicAdd(&C->rejects, 1ull);
+    if ((uint32_t)m < excl && (uint32_t)m < thr) {
+      const unsigned long long q = atomicAdd(&C->rejects, 1ull);
+      if (q < 32) C->rej_pos[q] = j;
+    }
+    if (j < D) A.draws[j] = (int32_t)(m >> 32);
+  }
+}
+
+// Rejected words are skipped by numpy's Lemire loop, so draw j is the word
+// at the (j+1)-th accepted position: w = j + #{rejected q <= w} (fixed point,
+// at most #rejections + 1 steps). Parallel over the draws.
+__device__ void lv_draws_fix_parallel(const LevelArgs& A, int64_t t0, int64_t nt) {
+  LevelCtl* C = A.C;
+  const int R = (int)*(const volatile unsigned long long*)&C->rejects;
+  const int64_t D = (int64_t)*(const volatile long long*)&C->max_evict;
+  const int nvalid = ldv(&C->nvalid);
+  DevPcg g;
+  g.state = ((du128)*(const volatile unsigned long long*)&C->pcg_state_hi << 64) |
+            *(const volatile unsigned long long*)&C->pcg_state_lo;
+  g.inc = ((du128)*(const volatile unsigned long long*)&C->pcg_inc_hi << 64) |
+          *(const volatile unsigned long long*)&C->pcg_inc_lo;
+  long long qmin = LLONG_MAX;
+  for (int r = 0; r < R; ++r) qmin = min(qmin, *(const volatile long long*)&C->rej_pos[r]);
+  for (int64_t j = t0; j < D; j += nt) {
+    if (j < qmin) continue;  // before the first rejection nothing moved
+    int64_t w = j;
+    while (true) {
+      int64_t cnt = 0;
+      for (int r = 0; r < R; ++r) cnt += *(const volatile long long*)&C->rej_pos[r] <= w;
+      if (j + cnt == w) break;
+      w = j + cnt;
+    }
+    const uint64_t m = (uint64_t)pcg_word(g, (uint64_t)w) * (uint32_t)nvalid;
     A.draws[j] = (int32_t)(m >> 32);
   }
 }
@@ -728,8 +764,12 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       int P2ev = 1;
       while (P2ev < Lev) P2ev <<= 1;
       if (!strong && *(const volatile unsigned long long*)&C->rejects) {
-        // a Lemire rejection shifted the draw stream: redo it sequentially
-        if (blockIdx.x == 0 && threadIdx.x == 0) lv_draws_fixup(A);
+        // a Lemire rejection shifted the draw stream: re-derive the draws
+        // (in parallel; sequentially only past 32 rejections)
+        if (*(const volatile unsigned long long*)&C->rejects <= 32)
+          lv_draws_fix_parallel(A, t0, nt);
+        else if (blockIdx.x == 0 && threadIdx.x == 0)
+          lv_draws_fixup(A);
         gsync();
       }
       pc.mark(13);
@@ -984,7 +1024,8 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   if (per_sm < 1) return false;
   // grid barriers dominate small levels: size the cooperative grid to the
   // level (about LV_ROWS_PER_BLOCK vertices per block), capped at residency
-  const int64_t want = (g.n + LV_ROWS_PER_BLOCK - 1) / LV_ROWS_PER_BLOCK;
+  const int64_t want = std::max((g.n + LV_ROWS_PER_BLOCK - 1) / LV_ROWS_PER_BLOCK,
+                                (g.nnz + LV_ENTRIES_PER_BLOCK - 1) / LV_ENTRIES_PER_BLOCK);
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * c.num_sms));
   void* args[] = {&A};
   launch(c, "refine_level", 0.0, [&] {

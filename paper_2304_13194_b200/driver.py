@@ -138,12 +138,27 @@ def build_metrics(graph, config, state, st, total, W, limit) -> dict:
     }
 
 
+class _DeviceGraphInfo:
+    """What _prepare reads, from a device-resident graph (unit vertex weights
+    are recognised from W == n without a download)."""
+
+    def __init__(self, dgraph):
+        n, _, W = dgraph.info()
+        self.row_offsets = np.empty(n + 1, np.int8)
+        self.total_vertex_weight = W
+        self.vertex_weights = np.ones(1, np.int64) if W == n else dgraph.download()[3]
+
+
 def partition_resident(dgraph: _lib.DeviceGraph, graph, config: RefinerConfig,
                        want_parts: bool = True):
     """Partition a graph already resident in HBM (device-timed benchmark leg).
 
     `graph` supplies the host-side checks (vertex weights); `dgraph` is its
-    uploaded copy. Returns (parts or None, part_weights, RunStats)."""
+    uploaded copy. `graph` may be None for a device-generated graph: the
+    checks then read the device copy. Returns (parts or None, part_weights,
+    RunStats)."""
+    if graph is None:
+        graph = _DeviceGraphInfo(dgraph)
     n, W, limit = _prepare(graph, config)
     cfg = to_c(config, W)
     parts = np.empty(n, np.int64) if want_parts else None
