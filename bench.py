@@ -198,6 +198,52 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+EXTRA_CONFIGS = [  # BASELINE configs 3-4, generated on the device (reference generators)
+    ("rmat22", "R-MAT scale 22 edgefactor 16 (LCC n=2,395,105, m=64,153,772), k=64, lambda=1.03, seed=0", 64),
+    ("rgg16m", "2D random geometric graph 2^24 points, mean degree ~12, k=256, lambda=1.03, seed=0", 256),
+]
+
+
+def measure_extra_configs(ctx, steps=2):
+    """Device-timed partitions of configs 3-4 (inputs generated on the device,
+    identical to the reference's generators); cut vs the reference's
+    (tests/golden/quality.json, C oracle pinned to the reference)."""
+    import math
+    import paper_2304_13194_b200 as J
+    from paper_2304_13194_b200 import generators as gen
+    from paper_2304_13194_b200.driver import partition_resident
+    try:
+        q = json.loads((ROOT / "tests" / "golden" / "quality.json").read_text())
+    except Exception:
+        q = {}
+    out = []
+    for name, workload, k in EXTRA_CONFIGS:
+        if name == "rmat22":
+            dg = gen.rmat_device(22, 16, 0, ctx=ctx)
+        else:
+            n = 1 << 24
+            dg = gen.geometric_device(n, math.sqrt(12 / (math.pi * n)), 0, ctx=ctx)
+        n, nnz, W = dg.info()
+        cfg = J.RefinerConfig(k=k, imbalance=IMB, seed=SEED, deterministic=True)
+        partition_resident(dg, None, cfg, want_parts=False)  # warm
+        ms = []
+        for _ in range(steps):
+            ctx.flush_l2()
+            ctx.timer_start()
+            _, pw, st = partition_resident(dg, None, cfg, want_parts=False)
+            ms.append(ctx.timer_stop())
+        t = sum(ms) / len(ms) * 1e-3
+        ref = q.get(name, {}).get("cuts", {}).get("0")
+        out.append({"workload": workload, "n": n, "m": nnz // 2, "partition_time_s": t,
+                    "edges_per_s": (nnz // 2) / t, "cutsize": int(st.cutsize),
+                    "reference_cutsize": ref,
+                    "cut_ratio_vs_cpu_ref": (int(st.cutsize) / ref) if ref else None,
+                    "balanced": bool(st.balanced), "steps": steps,
+                    "mode": "deterministic (bit-exact reference semantics)"})
+        dg.free()
+    return out
+
+
 def run_ours(args, world, rank, local):
     import paper_2304_13194_b200 as J
     from paper_2304_13194_b200 import _lib
@@ -275,6 +321,7 @@ def run_ours(args, world, rank, local):
                "sample": f"one full partition of the same workload on the host "
                          f"({dt:.1f} s, cut {cut}); C port of the reference algorithm"}
     clocks = clk.summary()
+    extra = measure_extra_configs(ctx) if (rank == 0 and not args.no_extra_configs) else None
     if rank == 0:
         line = {
             "metric": "edges/s", "value": value, "unit": "edges/s", "n_gpus": world,
@@ -299,6 +346,7 @@ def run_ours(args, world, rank, local):
                          "launches": dom["launches"], "share_of_step": dominant_share},
             "cpu_baseline": cpu,
             "clocks": clocks,
+            "configs_measured": extra,
         }
         print(json.dumps(line), flush=True)
 
@@ -310,6 +358,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra-configs", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
     world, rank, local = dist_setup()

@@ -362,6 +362,25 @@ __device__ __forceinline__ void warp_append(bool take, int32_t v, int32_t* list,
   if (take) list[base + __popc(m & lanemask_lt())] = v;
 }
 
+// Block-wide int64 sum returned to every thread (any blockDim <= 1024; all
+// threads of the block must call it).
+__device__ __forceinline__ long long block_sum_all(long long x) {
+  __shared__ long long red_all[33];
+  x = gsum<32>(x, 0xffffffffu);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (l == 0) red_all[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    long long y = l < nw ? red_all[l] : 0;
+    y = gsum<32>(y, 0xffffffffu);
+    if (l == 0) red_all[32] = y;
+  }
+  __syncthreads();
+  return red_all[32];
+}
+
 // Block-wide int64 sum into *out for any blockDim <= 1024.
 __device__ __forceinline__ void block_sum_atomic_any(long long x, unsigned long long* out) {
   __shared__ long long red_any[32];

@@ -657,6 +657,47 @@ static __device__ void afterburner_rows(const AbArgs& a, const GView& g, const S
   for (int t = 0; t < NBINS; ++t) {
     const int64_t cnt = (int64_t)*(const volatile unsigned long long*)(sl.cnt + t);
     const int32_t* list = sl.list[t];
+    if (t == BIN_BLOCK) {
+      // hub rows (> WARP_TIER_MAX_DEG entries): a block per row
+      for (int64_t i = blockIdx.x; i < cnt; i += gridDim.x) {
+        const int v = list[i];
+        const int own = a.parts[v];
+        const int dv = a.cdest[v];
+        const long long Fv = a.F[v];
+        const int64_t b = g.offs[v], e = g.offs[v + 1];
+        if (wr && threadIdx.x == 0) {
+          *wr += 1;
+          *we += (unsigned long long)(e - b);
+        }
+        long long f2 = 0;
+        for (int64_t j = b + threadIdx.x; j < e; j += blockDim.x) {
+          const int u = g.adj[j];
+          int eff = a.parts[u];
+          const int cu = a.cdest[u];
+          if (cu >= 0) {
+            const long long Fu = a.F[u];
+            if (Fu > Fv || (Fu == Fv && u < v)) eff = cu;
+          }
+          const int w = UNIT ? 1 : g.ew[j];
+          f2 += (eff == dv) ? w : (eff == own) ? -w : 0;
+        }
+        f2 = block_sum_all(f2);
+        if (threadIdx.x == 0) {
+          if (a.f2_out) a.f2_out[v] = f2;
+          if (f2 >= 0) {
+            if (a.move_list) {
+              a.mv[v] = dv;
+              const unsigned long long q = atomicAdd(a.move_cnt + t, 1ull);
+              a.move_list[mseg.b[t] + q] = v;
+            } else if (nmove) {
+              a.mv[v] = dv;
+              *nmove += 1;
+            }
+          }
+        }
+      }
+      continue;
+    }
     for (int64_t i = w0; i < cnt; i += ws) {
       const int v = list[i];
       const int own = a.parts[v];
@@ -718,6 +759,35 @@ static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const S
   for (int t = 0; t < NBINS; ++t) {
     const int64_t cnt = (int64_t)*(const volatile unsigned long long*)(sl.cnt + t);
     const int32_t* list = sl.list[t];
+    if (t == BIN_BLOCK) {
+      // hub rows: a block per row (block-uniform skip of unmoved rows)
+      for (int64_t i = blockIdx.x; i < cnt; i += gridDim.x) {
+        const int v = list[i];
+        const int dst = a.mv[v];
+        if (dst < 0) continue;
+        const int old = a.parts[v];
+        const int64_t b = g.offs[v], e = g.offs[v + 1];
+        if (wr && threadIdx.x == 0) {
+          *wr += 1;
+          *we += (unsigned long long)(e - b);
+        }
+        for (int64_t j = b + threadIdx.x; j < e; j += blockDim.x) {
+          const int u = g.adj[j];
+          const int pu = a.parts[u];
+          const int mu = a.mv[u];
+          const int nu = mu >= 0 ? mu : pu;
+          const long long w = UNIT ? 1 : g.ew[j];
+          const long long cc = w * ((long long)(nu != dst) - (long long)(pu != old));
+          acc += mu >= 0 ? cc : 2 * cc;
+        }
+        if (threadIdx.x == 0) {
+          const unsigned long long wv = (unsigned long long)g.vw[v];
+          atomicAdd(&a.pw[dst], wv);
+          atomicAdd(&a.pw[old], (unsigned long long)(-(long long)wv));
+        }
+      }
+      continue;
+    }
     for (int64_t i = w0; i < cnt; i += ws) {
       const int v = list[i];
       const int dst = a.mv[v];
