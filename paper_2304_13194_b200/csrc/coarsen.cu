@@ -500,6 +500,7 @@ struct Resolve {
   int32_t* mn;     // 2 x n
   int64_t n;
   unsigned long long small;
+  unsigned long long* stats;  // optional (JET_MATCH_STATS): rounds, tail edges, tail steps
 };
 
 __device__ void resolve_a(const Resolve& R, int in, int out, int64_t t0, int64_t nt) {
@@ -508,7 +509,8 @@ __device__ void resolve_a(const Resolve& R, int in, int out, int64_t t0, int64_t
   int32_t* lout = R.lists + (size_t)out * R.n;
   int32_t* mcur = R.mn + (size_t)out * R.n;
   int32_t* mprev = R.mn + (size_t)in * R.n;
-  const int64_t lim = (cnt + 31) / 32 * 32;
+  // block-uniform trip count: the surviving edges are appended per block
+  const int64_t lim = (cnt + blockDim.x - 1) / blockDim.x * blockDim.x;
   for (int64_t i = t0; i < lim; i += nt) {
     bool alive = false;
     int v = 0;
@@ -523,7 +525,7 @@ __device__ void resolve_a(const Resolve& R, int in, int out, int64_t t0, int64_t
         atomicMin(&mcur[u], v);
       }
     }
-    warp_append(alive, v, lout, R.cnt + out);
+    block_append(alive, v, lout, R.cnt + out);
   }
 }
 
@@ -565,6 +567,8 @@ __device__ __forceinline__ int res_slot(ResTailSmem& S, int v) {
 }
 
 __device__ void resolve_tail(const Resolve& R, int in, ResTailSmem& S) {
+  const long long c0 = clock64();
+  int tail_rounds = 0;
   const int L = (int)vload(R.cnt + in);
   const int32_t* lin = R.lists + (size_t)in * R.n;
   // the global minima written for these edges in the previous grid round
@@ -627,8 +631,13 @@ __device__ void resolve_tail(const Resolve& R, int in, ResTailSmem& S) {
     }
     __syncthreads();
     cur ^= 1;
+    ++tail_rounds;
   }
   if (threadIdx.x == 0) R.cnt[in] = 0;
+  if (R.stats && threadIdx.x == 0) {
+    R.stats[2] += (unsigned long long)(clock64() - c0);
+    R.stats[3] += (unsigned long long)tail_rounds;
+  }
 }
 
 __global__ void __launch_bounds__(1024) k_resolve(Resolve R) {
@@ -649,6 +658,10 @@ __global__ void __launch_bounds__(1024) k_resolve(Resolve R) {
     ++r;
   }
   if (blockIdx.x != 0) return;
+  if (R.stats && threadIdx.x == 0) {
+    R.stats[0] += (unsigned long long)r;
+    R.stats[1] += vload(R.cnt + ((r - 1) & 1));
+  }
   // live edges of list `in` were last scattered into mn[in]; that buffer was
   // reset by resolve_a of this round only if the round ran, so clear the
   // entries of the list now (they would otherwise leak into a later call)
@@ -665,6 +678,281 @@ __global__ void __launch_bounds__(1024) k_resolve(Resolve R) {
   }
   __syncthreads();
   resolve_tail(R, in, *reinterpret_cast<ResTailSmem*>(res_smem));
+}
+
+// ---------------------------------------------------------------------------
+// Phase-1 resolution by frontier (work-efficient, exact). The ascending-id
+// scan accepts the proposal edge e_v = (v, P(v)) iff both endpoints are free
+// when v's turn comes. An edge is dead once an endpoint is matched; a live
+// edge's turn is decided once every lower-id live edge sharing an endpoint
+// is decided, i.e. when it is the lowest live edge at both endpoints -- and
+// then it is accepted. Each vertex keeps its incident proposal edges sorted
+// by id and a head pointer to its lowest live one. A round (1) accepts the
+// frontier (pairwise non-adjacent: no conflicts), (2) refreshes the heads of
+// the vertices whose head edge died (neighbours of the newly matched ones),
+// (3) queues the refreshed heads that are now lowest at both endpoints.
+// Rounds follow the dependency depth, each touching only the frontier.
+struct Frontier {
+  const int32_t* prop;
+  int32_t* partner;
+  const unsigned long long* inc;  // sorted (endpoint << 32 | edge id)
+  const int32_t* ioff;            // n + 1
+  int32_t* head;                  // n (index into inc)
+  int32_t* qflag;                 // n: round an edge was queued in
+  int32_t* aflag;                 // n: round a vertex was refreshed in
+  int32_t* fr;                    // 2 x cap
+  int32_t* aff;                   // affected vertices of the round, <= n
+  unsigned long long* fcnt;       // [0,1] frontier sizes, [2] affected, [3] rounds
+  const int32_t* props;           // proposers
+  int64_t ne, cap;
+};
+
+__device__ __forceinline__ int fr_other(const Frontier& F, int e, int x) {
+  return e == x ? F.prop[e] : e;
+}
+
+// edge at x's head, or -1
+__device__ __forceinline__ int fr_head_edge(const Frontier& F, int x) {
+  const int h = F.head[x];
+  return h < F.ioff[x + 1] ? (int)(F.inc[h] & 0xffffffffu) : -1;
+}
+
+// lowest live edge at unmatched vertex x, scanning from its (possibly stale,
+// never overtaking) head; warp-cooperative, result in every lane
+__device__ __forceinline__ int fr_first_live(const Frontier& F, int x, int* pos) {
+  const int lane = threadIdx.x & 31;
+  const int end = F.ioff[x + 1];
+  for (int q = F.head[x]; q < end; q += 32) {
+    const int j = q + lane;
+    int e = -1;
+    bool live = false;
+    if (j < end) {
+      e = (int)(F.inc[j] & 0xffffffffu);
+      live = F.partner[fr_other(F, e, x)] < 0;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, live);
+    if (m) {
+      const int l = __ffs(m) - 1;
+      *pos = q + l;
+      return __shfl_sync(0xffffffffu, e, l);
+    }
+  }
+  *pos = end;
+  return -1;
+}
+
+// thread-level scan for the lowest live edge at unmatched x, at most `lim`
+// entries; returns -2 when the limit is hit (the caller defers x to a warp)
+__device__ __forceinline__ int fr_first_live_t(const Frontier& F, int x, int lim, int* pos) {
+  const int end = F.ioff[x + 1];
+  int q = F.head[x];
+  for (int s = 0; q < end; ++q, ++s) {
+    if (s == lim) return -2;
+    const int e = (int)(F.inc[q] & 0xffffffffu);
+    if (F.partner[fr_other(F, e, x)] < 0) {
+      *pos = q;
+      return e;
+    }
+  }
+  *pos = end;
+  return -1;
+}
+
+constexpr int FR_SHORT = 64;     // entries a thread scans before deferring to a warp
+constexpr int FR_DEFER = 2048;   // deferred entries per block and phase
+
+__global__ void __launch_bounds__(1024) k_resolve_frontier(Frontier F) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ int s_def[FR_DEFER];
+  __shared__ int s_ndef;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  // initial frontier: edges that are lowest at both endpoints (all live)
+  for (int64_t i = t0; i < ((F.ne + 31) & ~31LL); i += nt) {
+    bool rd = false;
+    int v = 0;
+    if (i < F.ne) {
+      v = F.props[i];
+      rd = fr_head_edge(F, v) == v && fr_head_edge(F, F.prop[v]) == v;
+    }
+    warp_append(rd, v, F.fr, F.fcnt);
+  }
+  grid.sync();
+  int cur = 0;
+  for (int round = 1;; ++round) {
+    const int64_t L = (int64_t)vload(F.fcnt + cur);
+    if (L == 0) break;
+    const int32_t* fin = F.fr + (size_t)cur * F.cap;
+    int32_t* fout = F.fr + (size_t)(cur ^ 1) * F.cap;
+    // (1) accept the frontier
+    for (int64_t i = t0; i < L; i += nt) {
+      const int v = fin[i], u = F.prop[v];
+      F.partner[v] = u;
+      F.partner[u] = v;
+    }
+    if (t0 == 0) {
+      F.fcnt[cur ^ 1] = 0;
+      F.fcnt[2] = 0;
+    }
+    grid.sync();
+    // (2) unmatched vertices sharing an edge with a newly matched one (their
+    // head edge may have died), deduplicated; long incidence lists (hubs)
+    // are walked by a warp
+    auto touch = [&](int y) {
+      if (F.partner[y] >= 0 || atomicExch(&F.aflag[y], round) == round) return false;
+      return true;
+    };
+    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < 2 * L; b0 += nt) {
+      if (threadIdx.x == 0) s_ndef = 0;
+      __syncthreads();
+      const int64_t i = b0 + threadIdx.x;
+      if (i < 2 * L) {
+        const int v = fin[i >> 1];
+        const int x = (i & 1) ? F.prop[v] : v;
+        const int beg = F.ioff[x], end = F.ioff[x + 1];
+        if (end - beg > FR_SHORT) {
+          const int d = atomicAdd(&s_ndef, 1);
+          s_def[d] = x;  // d < blockDim <= FR_DEFER
+        } else {
+          for (int q = beg; q < end; ++q) {
+            const int y = fr_other(F, (int)(F.inc[q] & 0xffffffffu), x);
+            if (touch(y)) F.aff[atomicAdd(F.fcnt + 2, 1ull)] = y;
+          }
+        }
+      }
+      __syncthreads();
+      for (int d = wib; d < s_ndef; d += nwb) {
+        const int x = s_def[d];
+        const int end = F.ioff[x + 1];
+        for (int q0 = F.ioff[x]; q0 < end; q0 += 32) {
+          const int q = q0 + lane;
+          int y = -1;
+          if (q < end) {
+            y = fr_other(F, (int)(F.inc[q] & 0xffffffffu), x);
+            if (!touch(y)) y = -1;
+          }
+          warp_append(y >= 0, y, F.aff, F.fcnt + 2);
+        }
+      }
+      __syncthreads();
+    }
+    grid.sync();
+    // (3) refresh each affected head; queue it if it is also the lowest live
+    // edge at its other endpoint
+    const int64_t A = (int64_t)vload(F.fcnt + 2);
+    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < A; b0 += nt) {
+      if (threadIdx.x == 0) s_ndef = 0;
+      __syncthreads();
+      const int64_t i = b0 + threadIdx.x;
+      if (i < A) {
+        const int y = F.aff[i];
+        int pos, pz;
+        const int h = fr_first_live_t(F, y, FR_SHORT, &pos);
+        bool defer = h == -2;
+        if (!defer) {
+          F.head[y] = pos;
+          if (h >= 0) {
+            const int hz = fr_first_live_t(F, fr_other(F, h, y), FR_SHORT, &pz);
+            if (hz == -2) defer = true;
+            else if (hz == h && atomicExch(&F.qflag[h], round) != round)
+              fout[atomicAdd(F.fcnt + (cur ^ 1), 1ull)] = h;
+          }
+        }
+        if (defer) s_def[atomicAdd(&s_ndef, 1)] = y;
+      }
+      __syncthreads();
+      for (int d = wib; d < s_ndef; d += nwb) {
+        const int y = s_def[d];
+        int pos, pz;
+        const int h = fr_first_live(F, y, &pos);
+        if (lane == 0) F.head[y] = pos;
+        if (h < 0) continue;
+        const int hz = fr_first_live(F, fr_other(F, h, y), &pz);
+        if (lane == 0 && hz == h && atomicExch(&F.qflag[h], round) != round)
+          fout[atomicAdd(F.fcnt + (cur ^ 1), 1ull)] = h;
+      }
+      __syncthreads();
+    }
+    grid.sync();
+    if (t0 == 0) F.fcnt[3] += 1;
+    cur ^= 1;
+  }
+}
+
+__global__ void k_inc_keys(const int32_t* __restrict__ props, int64_t ne,
+                           const int32_t* __restrict__ prop, unsigned long long* keys) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ne;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned v = (unsigned)props[i], u = (unsigned)prop[v];
+    keys[2 * i] = ((unsigned long long)v << 32) | v;
+    keys[2 * i + 1] = ((unsigned long long)u << 32) | v;
+  }
+}
+
+// ioff[x] = first incidence of endpoint x (lower bound in the sorted keys)
+__global__ void k_inc_offsets(const unsigned long long* __restrict__ keys, int64_t M, int64_t n,
+                              int32_t* ioff, int32_t* head, int32_t* aflag) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x <= n;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long key = (unsigned long long)x << 32;
+    int64_t lo = 0, hi = M;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < key) lo = mid + 1;
+      else hi = mid;
+    }
+    ioff[x] = (int32_t)lo;
+    if (x < n) {
+      head[x] = (int32_t)lo;
+      aflag[x] = 0;
+    }
+  }
+}
+
+static void resolve_frontier(Ctx& c, int64_t n, const int32_t* prop, int32_t* partner,
+                             const int32_t* props, int64_t ne) {
+  const int64_t M = 2 * ne;
+  unsigned long long* keys = c.scratch<unsigned long long>(21, 2 * M);
+  int32_t* ints = c.scratch<int32_t>(22, 5 * n + 1);
+  int32_t* fr = c.scratch<int32_t>(23, 2 * ne);
+  unsigned long long* fcnt = c.scratch<unsigned long long>(24, 4);
+  int32_t *ioff = ints, *head = ints + n + 1, *qflag = ints + 2 * n + 1, *aflag = ints + 3 * n + 1,
+          *aff = ints + 4 * n + 1;
+  dzero(c, fcnt, 4);
+  dzero(c, qflag, n);
+  launch(c, "match_inc", 16.0 * ne, [&] {
+    k_inc_keys<<<grid_for(c, ne, 256), 256, 0, c.stream>>>(props, ne, prop, keys);
+  });
+  int end_bit = 33;
+  while (end_bit < 64 && (1LL << (end_bit - 32)) <= n) ++end_bit;
+  size_t tmp = 0;
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys, keys + M, (int)M, 0, end_bit, c.stream));
+  void* p = c.cub_scratch(tmp);
+  launch(c, "match_inc_sort", 32.0 * M, [&] {
+    CK(cub::DeviceRadixSort::SortKeys(p, tmp, keys, keys + M, (int)M, 0, end_bit, c.stream));
+  });
+  launch(c, "match_inc", 16.0 * n, [&] {
+    k_inc_offsets<<<grid_for(c, n + 1, 256), 256, 0, c.stream>>>(keys + M, M, n, ioff, head,
+                                                                 aflag);
+  });
+  Frontier F{prop, partner, keys + M, ioff, head, qflag, aflag, fr, aff, fcnt, props, ne, ne};
+  static int fgrid = 0;
+  if (!fgrid) fgrid = coop_blocks(c, (const void*)k_resolve_frontier, 1024);
+  const int blocks = (int)std::min<int64_t>(fgrid, std::max<int64_t>(1, (ne + 16383) / 16384));
+  void* args[] = {&F};
+  launch(c, "match_resolve", 0.0, [&] {
+    CK(cudaLaunchCooperativeKernel((const void*)k_resolve_frontier, dim3(blocks), dim3(1024), args,
+                                   0, c.stream));
+  });
+  static const bool mstats = getenv("JET_MATCH_STATS") && getenv("JET_MATCH_STATS")[0] == '1';
+  if (mstats) {
+    unsigned long long hs[4];
+    d2h(c, hs, fcnt, 4);
+    c.sync();
+    fprintf(stderr, "FRONTIER n=%lld edges=%lld blocks=%d rounds=%llu\n", (long long)n,
+            (long long)ne, blocks, hs[3]);
+  }
 }
 
 void device_match(Ctx& c, const DGraph& g, int32_t* partner) {
@@ -706,9 +994,20 @@ void device_match(Ctx& c, const DGraph& g, int32_t* partner) {
       d2h(c, &ne, cnt.get(), 1);
       c.sync();
       if (ne == 0) break;
+      static const bool old_rounds = getenv("JET_MATCH_ROUNDS") && getenv("JET_MATCH_ROUNDS")[0] == '1';
+      if (!old_rounds) {
+        resolve_frontier(c, n, prop_p, partner, lists_p, (int64_t)ne);
+        continue;
+      }
       // all resolution rounds in one cooperative launch (k_resolve)
+      static const bool mstats = getenv("JET_MATCH_STATS") && getenv("JET_MATCH_STATS")[0] == '1';
+      static DBuf<unsigned long long>* sbuf = nullptr;
+      if (mstats && !sbuf) {
+        sbuf = new DBuf<unsigned long long>(4, c.stream);
+        dzero(c, sbuf->get(), 4);
+      }
       Resolve R{prop_p, partner, lists_p, cnt.get(), mn_p, n,
-                (unsigned long long)RES_TAIL};
+                (unsigned long long)RES_TAIL, mstats ? sbuf->get() : nullptr};
       const size_t smem = sizeof(ResTailSmem);
       static int res_grid = 0;
       if (!res_grid) {
@@ -725,6 +1024,14 @@ void device_match(Ctx& c, const DGraph& g, int32_t* partner) {
         CK(cudaLaunchCooperativeKernel((const void*)k_resolve, dim3(blocks), dim3(1024), args, smem,
                                        c.stream));
       });
+      if (mstats) {
+        unsigned long long hs[4];
+        d2h(c, hs, sbuf->get(), 4);
+        c.sync();
+        fprintf(stderr, "MATCH n=%lld live=%llu blocks=%d rounds=%llu tail=%llu tail_us=%.1f tail_rounds=%llu\n",
+                (long long)n, ne, blocks, hs[0], hs[1], hs[2] / 1965.0, hs[3]);
+        dzero(c, sbuf->get(), 4);
+      }
     }
     two_hop(c, g, partner);
   }

@@ -218,7 +218,7 @@ struct Ctx {
   // Fresh stream-ordered allocations of hundreds of MB occasionally make the
   // pool map new physical memory, which stalls the host for 100s of ms.
   std::unique_ptr<CtxExt> level_ext;  // level.cu: persistent-controller scratch
-  static constexpr int NSCRATCH = 24;
+  static constexpr int NSCRATCH = 28;
   DBuf<uint8_t> scratch_slots[NSCRATCH];
   template <class T>
   T* scratch(int slot, size_t count) {
@@ -360,6 +360,35 @@ __device__ __forceinline__ void warp_append(bool take, int32_t v, int32_t* list,
   if (lane == leader) base = atomicAdd(cnt, (unsigned long long)__popc(m));
   base = __shfl_sync(am, base, leader);
   if (take) list[base + __popc(m & lanemask_lt())] = v;
+}
+
+// Block-aggregated append: one global atomic per block and call instead of
+// one per warp (a hot counter serialises in L2). Every thread of the block
+// must call it (block-uniform loop trip counts).
+__device__ __forceinline__ void block_append(bool take, int32_t v, int32_t* list,
+                                             unsigned long long* cnt) {
+  __shared__ unsigned s_wc[32];
+  __shared__ unsigned long long s_base;
+  const unsigned m = __ballot_sync(0xffffffffu, take);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int nw = (blockDim.x + 31) >> 5;
+  if (l == 0) s_wc[w] = __popc(m);
+  __syncthreads();
+  if (w == 0) {
+    const unsigned x = l < nw ? s_wc[l] : 0u;
+    unsigned inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (l >= o) inc += y;
+    }
+    const unsigned tot = __shfl_sync(0xffffffffu, inc, 31);
+    if (l < nw) s_wc[l] = inc - x;
+    if (l == 0) s_base = tot ? atomicAdd(cnt, (unsigned long long)tot) : 0ull;
+  }
+  __syncthreads();
+  if (take) list[s_base + s_wc[w] + __popc(m & lanemask_lt())] = v;
+  __syncthreads();
 }
 
 // Block-wide int64 sum returned to every thread (any blockDim <= 1024; all

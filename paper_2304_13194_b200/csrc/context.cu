@@ -1,5 +1,7 @@
 // context.cu — jet_ctx lifetime, error reporting and launch profiling.
 #include "common.cuh"
+#include <algorithm>
+#include <cstdlib>
 #include <cstdlib>
 #include <cstring>
 
@@ -146,6 +148,24 @@ int jet_create(int device, jet_ctx** out) {
     CK(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = ~0ULL;
     CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    // Reserve physical memory in the pool up front: growing the pool inside
+    // a partition (cudaMallocAsync mapping new memory) stalled the host for
+    // 100s of ms on dense coarse levels. JET_POOL_RESERVE_MB overrides.
+    {
+      size_t fr = 0, tot = 0;
+      CK(cudaMemGetInfo(&fr, &tot));
+      size_t want = std::min<size_t>(fr / 4, (size_t)24 << 30);
+      if (const char* e = getenv("JET_POOL_RESERVE_MB")) want = (size_t)atoll(e) << 20;
+      if (want) {
+        void* p = nullptr;
+        if (cudaMallocAsync(&p, want, c->stream) == cudaSuccess) {
+          cudaFreeAsync(p, c->stream);
+          cudaStreamSynchronize(c->stream);
+        } else {
+          cudaGetLastError();
+        }
+      }
+    }
     c->ensure_pinned(1 << 16);
     const char* hl = getenv("JET_HOST_LEVELS");
     c->host_levels = hl && hl[0] == '1';

@@ -24,7 +24,9 @@ for name in which:
     tg = time.perf_counter() - t
     n, nnz, W = dg.info()
     cfg = J.RefinerConfig(k=k, imbalance=0.03, seed=0, deterministic=mode)
-    for rep in range(2):
+    for rep in range(3):
+        ctx.profile(rep == 2)
+        ctx.profile_reset()
         t = time.perf_counter()
         parts, pw, st = partition_resident(dg, None, cfg, want_parts=False)
         tp = time.perf_counter() - t
@@ -32,6 +34,11 @@ for name in which:
               f"(coarsen {st.t_coarsen:.3f} init {st.t_initial:.3f} unc {st.t_uncoarsen:.3f}) "
               f"cut={st.cutsize} balanced={st.balanced} levels={st.n_levels} "
               f"launches={st.kernel_launches}", flush=True)
+    rp = ctx.profile_report()
+    tot = sum(v['ms'] for k_, v in rp.items() if k_ != '__total__')
+    for nm, v in sorted(rp.items(), key=lambda x: -x[1]['ms'])[:14]:
+        if nm != '__total__':
+            print(f"   {nm:20s} launches={v['launches']:6d} ms={v['ms']:9.3f} ({100*v['ms']/tot:5.1f}%)")
     for i in range(st.n_levels):
         L = st.levels[i]
         print(f"   L{L.level}: n={L.n} m={L.m} iters={L.iterations} lp={L.lp_passes} w={L.weak_passes} "
