@@ -26,6 +26,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 namespace jet {
 
@@ -225,6 +226,7 @@ struct TwoHop {
   uint8_t* ready;           // per centre index
   int32_t* minc;            // per vertex id (leftovers only)
   int64_t nc;
+  unsigned long long* stats;  // optional: rounds
 };
 
 // Retire centres with <= 1 unmatched member; count the remaining active.
@@ -341,6 +343,7 @@ __global__ void __launch_bounds__(1024)
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
   while (true) {
+    if (t.stats && blockIdx.x == 0 && threadIdx.x == 0) t.stats[0] += 1;
     th_retire(t, active, w0, ws);
     grid.sync();
     if (vload(active) == 0) return;
@@ -350,6 +353,174 @@ __global__ void __launch_bounds__(1024)
     grid.sync();
     if (w0 == 0 && (threadIdx.x & 31) == 0) *active = 0;
     th_pair(t, w0, ws);
+    grid.sync();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Two-hop by frontier (same rule, work-efficient). Counters per centre:
+// ucnt = unmatched members, good = unmatched members whose smallest active
+// centre (minc) is this centre. A centre retires when ucnt <= 1 and is
+// processed (pairs its unmatched members consecutively) when good == ucnt.
+// Each leftover keeps a cursor into its (sorted) adjacency at its minc. A
+// round decides the candidate centres, then updates the counters touched by
+// the newly matched members and advances the leftovers whose minc retired;
+// only centres whose counters changed are candidates next round.
+struct TwoHopF {
+  int32_t* partner;
+  const int32_t* centres;
+  const int64_t* coff;
+  const int32_t* members;
+  uint8_t* cact;        // per vertex id
+  int32_t* cidx;        // vertex id -> centre index
+  int32_t* ucnt;        // per centre
+  int32_t* good;        // per centre
+  int32_t* cflag;       // per centre: round it was queued in
+  int32_t* lcur;        // per vertex id (leftovers): offset of minc in its row, or -1
+  int32_t* cand;        // 2 x nc
+  int32_t* dlist;       // deactivated centres of the round, <= nc
+  int32_t* mlist;       // members matched in the round, <= nl
+  unsigned long long* cnt;  // [0,1] candidates, [2,3] deactivated, [4,5] matched (by round
+                            // parity), [6] rounds
+  int64_t nc;
+};
+
+__device__ __forceinline__ void thf_queue(const TwoHopF& t, int ci, int round, int32_t* out,
+                                          unsigned long long* ocnt) {
+  if (atomicExch(&t.cflag[ci], round) != round) out[atomicAdd(ocnt, 1ull)] = ci;
+}
+
+__global__ void __launch_bounds__(1024)
+    k_two_hop_frontier(TwoHopF t, GView g, const int32_t* __restrict__ left, int64_t nl) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = t0 >> 5, nw = nt >> 5;
+  for (int64_t ci = t0; ci < t.nc; ci += nt) {
+    t.ucnt[ci] = (int32_t)(t.coff[ci + 1] - t.coff[ci]);
+    t.good[ci] = 0;
+    t.cidx[t.centres[ci]] = (int32_t)ci;
+  }
+  grid.sync();
+  // every neighbour of a leftover is a centre, all active: minc = first entry
+  for (int64_t i = t0; i < nl; i += nt) {
+    const int v = left[i];
+    const int64_t b = g.offs[v];
+    if (g.offs[v + 1] > b) {
+      t.lcur[v] = 0;
+      atomicAdd(&t.good[t.cidx[g.adj[b]]], 1);
+    } else {
+      t.lcur[v] = -1;
+    }
+  }
+  grid.sync();
+  int cur = 0;
+  for (int round = 1;; ++round) {
+    const bool all = round == 1;
+    const int64_t C = all ? t.nc : (int64_t)vload(t.cnt + cur);
+    if (C == 0) break;
+    const int32_t* cin = t.cand + (size_t)cur * t.nc;
+    int32_t* cout = t.cand + (size_t)(cur ^ 1) * t.nc;
+    const int par = round & 1;
+    // (1) decide the candidates: retire, or pair (a warp per centre)
+    for (int64_t k = w0; k < C; k += nw) {
+      const int ci = all ? (int)k : cin[k];
+      const int c = t.centres[ci];
+      if (!t.cact[c]) continue;
+      const int u = t.ucnt[ci];
+      if (u <= 1 || t.good[ci] == u) {
+        if (u > 1) {
+          // pair consecutive unmatched members (coarsen.py:95-103)
+          const int64_t b = t.coff[ci], e = t.coff[ci + 1];
+          int pending = -1;
+          for (int64_t j0 = b; j0 < e; j0 += 32) {
+            const int64_t j = j0 + lane;
+            int v = -1;
+            bool un = false;
+            if (j < e) {
+              v = t.members[j];
+              un = t.partner[v] < 0;
+            }
+            const unsigned um = __ballot_sync(0xffffffffu, un);
+            const int off = pending >= 0 ? 1 : 0;
+            const unsigned below = um & lanemask_lt();
+            const int pos = __popc(below) + off;
+            int mate = -1;
+            const int src = below ? 31 - __clz(below) : lane;
+            const int vprev = __shfl_sync(0xffffffffu, v, src);
+            if (un && (pos & 1)) mate = below ? vprev : pending;
+            __syncwarp();
+            if (mate >= 0) {
+              t.partner[v] = mate;
+              t.partner[mate] = v;
+            }
+            warp_append(mate >= 0, v, t.mlist, t.cnt + 4 + par);
+            warp_append(mate >= 0, mate, t.mlist, t.cnt + 4 + par);
+            const int total = __popc(um) + off;
+            if (total & 1) {
+              const int last = um ? 31 - __clz(um) : -1;
+              const int lv = __shfl_sync(0xffffffffu, v, last >= 0 ? last : 0);
+              pending = last >= 0 ? lv : pending;
+            } else {
+              pending = -1;
+            }
+            __syncwarp();
+          }
+        }
+        if (lane == 0) {
+          t.cact[c] = 0;
+          t.dlist[atomicAdd(t.cnt + 2 + par, 1ull)] = ci;
+        }
+      }
+    }
+    if (t0 == 0) {
+      t.cnt[cur ^ 1] = 0;
+      t.cnt[2 + (par ^ 1)] = 0;  // read by the previous round's phase 2, done
+      t.cnt[4 + (par ^ 1)] = 0;
+    }
+    grid.sync();
+    // (2a) newly matched members leave every active centre's counts
+    const int64_t M = (int64_t)vload(t.cnt + 4 + par);
+    for (int64_t k = w0; k < M; k += nw) {
+      const int v = t.mlist[k];
+      const int64_t b = g.offs[v], e = g.offs[v + 1];
+      const int mc = t.lcur[v] >= 0 ? g.adj[b + t.lcur[v]] : -1;
+      for (int64_t j = b + lane; j < e; j += 32) {
+        const int c = g.adj[j];
+        if (!t.cact[c]) continue;
+        const int ci = t.cidx[c];
+        atomicSub(&t.ucnt[ci], 1);
+        if (c == mc) atomicSub(&t.good[ci], 1);
+        thf_queue(t, ci, round, cout, t.cnt + (cur ^ 1));
+      }
+    }
+    // (2b) unmatched members whose minc just retired move to their next
+    // active centre (a warp per retired centre; one thread per member)
+    const int64_t D = (int64_t)vload(t.cnt + 2 + par);
+    for (int64_t k = w0; k < D; k += nw) {
+      const int ci = t.dlist[k];
+      const int c = t.centres[ci];
+      const int64_t b = t.coff[ci], e = t.coff[ci + 1];
+      for (int64_t j = b + lane; j < e; j += 32) {
+        const int u = t.members[j];
+        if (t.partner[u] >= 0 || t.lcur[u] < 0) continue;
+        const int64_t rb = g.offs[u], re = g.offs[u + 1];
+        if (g.adj[rb + t.lcur[u]] != c) continue;
+        int64_t q = rb + t.lcur[u] + 1;
+        while (q < re && !t.cact[g.adj[q]]) ++q;
+        if (q < re) {
+          t.lcur[u] = (int32_t)(q - rb);
+          const int ci2 = t.cidx[g.adj[q]];
+          atomicAdd(&t.good[ci2], 1);
+          thf_queue(t, ci2, round, cout, t.cnt + (cur ^ 1));
+        } else {
+          t.lcur[u] = -1;
+        }
+      }
+    }
+    if (t0 == 0) t.cnt[6] += 1;
+    cur ^= 1;
     grid.sync();
   }
 }
@@ -472,7 +643,42 @@ static void two_hop(Ctx& c, const DGraph& g, int32_t* partner) {
   int32_t* minc_p = c.scratch<int32_t>(20, n);
   dzero(c, cact_p, n);
   th_mark(c, centres.get(), nc, cact_p);
-  TwoHop t{partner, centres.get(), coff.get(), v1_p, cact_p, ready_p, minc_p, nc};
+  static const bool mstats = getenv("JET_MATCH_STATS") && getenv("JET_MATCH_STATS")[0] == '1';
+  static const bool old_th = getenv("JET_TWO_HOP_ROUNDS") && getenv("JET_TWO_HOP_ROUNDS")[0] == '1';
+  // few leftovers (meshes): the full-pass rounds are cheaper than the
+  // frontier bookkeeping; many (skewed graphs: 10^5-10^6 leftovers under hub
+  // centres, hundreds of rounds) -> frontier
+  if (!old_th && nl > 16384) {
+    int32_t* ints = c.scratch<int32_t>(25, 2 * n + 5 * nc + nl + 64);
+    unsigned long long* tc = c.scratch<unsigned long long>(26, 8);
+    dzero(c, tc, 8);
+    int32_t *cidx = ints, *lcur = ints + n, *ucnt = ints + 2 * n, *good = ucnt + nc,
+            *cflag = good + nc, *cand = cflag + nc, *dlist = cand + 2 * nc, *mlist = dlist + nc;
+    dzero(c, cflag, nc);
+    TwoHopF f{partner, centres.get(), coff.get(), v1_p, cact_p, cidx, ucnt, good, cflag, lcur,
+              cand, dlist, mlist, tc, nc};
+    // a warp per centre in the first round
+    const int blocks = std::min<int64_t>(coop_blocks(c, (const void*)k_two_hop_frontier, 1024),
+                                         std::max<int64_t>(1, (std::max(nc, nl) + 31) / 32));
+    const int32_t* lp = left_p;
+    void* args[] = {&f, (void*)&gv, (void*)&lp, (void*)&nl};
+    launch(c, "two_hop", 0.0, [&] {
+      CK(cudaLaunchCooperativeKernel((const void*)k_two_hop_frontier, dim3(blocks), dim3(1024),
+                                     args, 0, c.stream));
+    });
+    if (mstats) {
+      unsigned long long r[8];
+      d2h(c, r, tc, 8);
+      c.sync();
+      fprintf(stderr, "TWOHOPF n=%lld leftovers=%lld centres=%lld blocks=%d rounds=%llu\n",
+              (long long)n, (long long)nl, (long long)nc, blocks, r[6]);
+    }
+    return;
+  }
+  DBuf<unsigned long long> thst(1, c.stream);
+  dzero(c, thst.get(), 1);
+  TwoHop t{partner, centres.get(), coff.get(), v1_p, cact_p, ready_p, minc_p, nc,
+           mstats ? thst.get() : nullptr};
   DBuf<unsigned long long> act(1, c.stream);
   dzero(c, act.get(), 1);
   const int64_t want = std::max<int64_t>(nc, nl);
@@ -485,6 +691,18 @@ static void two_hop(Ctx& c, const DGraph& g, int32_t* partner) {
     CK(cudaLaunchCooperativeKernel((const void*)k_two_hop, dim3(blocks), dim3(1024), args, 0,
                                    c.stream));
   });
+  if (mstats) {
+    unsigned long long r = 0;
+    int64_t mx = 0;
+    d2h(c, &r, thst.get(), 1);
+    c.sync();
+    std::vector<int64_t> hc(nc + 1);
+    d2h(c, hc.data(), coff.get(), nc + 1);
+    c.sync();
+    for (int64_t i = 0; i < nc; ++i) mx = std::max(mx, hc[i + 1] - hc[i]);
+    fprintf(stderr, "TWOHOP n=%lld leftovers=%lld pairs=%lld centres=%lld max_members=%lld blocks=%d rounds=%llu\n",
+            (long long)n, (long long)nl, (long long)np, (long long)nc, (long long)mx, blocks, r);
+  }
 }
 
 // ---------------------------------------------------------------------------
