@@ -139,6 +139,26 @@ int jet_graph_download(jet_ctx* ctx, const jet_graph* g, int64_t* row_offsets,
                        int64_t* vertex_weights);
 void jet_graph_free(jet_graph* g);
 
+/* ---- 1D vertex sharding ----------------------------------
+ * With a communicator of size > 1 attached, levels of at least
+ * `shard_min_vertices` vertices (default 2^20) refine with sharded Jetlp
+ * sweeps: each rank sweeps its block of vertices (balanced by entries) and
+ * the ranks all-gather the candidates (id, destination, gain) and the moves;
+ * coarse levels, rebalancing and the apply step run replicated. Every rank
+ * computes the same partition, bit-identical to the unsharded run.
+ * NCCL (one process per GPU): rank 0 calls jet_comm_nccl_id, the id is
+ * broadcast out of band (torch.distributed), every rank attaches.
+ * Local groups: `size` contexts in one process (one thread each) on one GPU
+ * share a group -- the same code path, for testing without several GPUs. */
+typedef struct jet_group jet_group;
+int jet_comm_nccl_id(uint8_t* id128);
+int jet_comm_attach_nccl(jet_ctx* ctx, const uint8_t* id128, int32_t rank, int32_t size);
+int jet_comm_local_group(int32_t size, jet_group** out);
+void jet_comm_local_group_free(jet_group* g);
+int jet_comm_attach_local(jet_ctx* ctx, jet_group* g, int32_t rank);
+int jet_comm_detach(jet_ctx* ctx);
+int jet_set_shard_min_vertices(jet_ctx* ctx, int64_t n);
+
 /* ---- on-device benchmark inputs (generators.py, graph.py:132-200) ---- */
 /* The reference's rmat_graph(scale, edge_factor, seed, probs)
  * (generators.py:32-55) and geometric_graph(n, radius, seed)

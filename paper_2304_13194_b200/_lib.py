@@ -93,6 +93,13 @@ _SIGS = {
     "jet_graph_download": (C.c_int, [P, P, P, P, P, P]),
     "jet_graph_free": (None, [P]),
     "jet_generate_rmat": (C.c_int, [P, i32, i32, C.c_uint64, P, C.POINTER(P)]),
+    "jet_comm_nccl_id": (C.c_int, [P]),
+    "jet_comm_attach_nccl": (C.c_int, [P, P, i32, i32]),
+    "jet_comm_local_group": (C.c_int, [i32, C.POINTER(P)]),
+    "jet_comm_local_group_free": (None, [P]),
+    "jet_comm_attach_local": (C.c_int, [P, P, i32]),
+    "jet_comm_detach": (C.c_int, [P]),
+    "jet_set_shard_min_vertices": (C.c_int, [P, i64]),
     "jet_generate_geometric": (C.c_int, [P, i64, C.c_double, C.c_uint64, C.POINTER(P)]),
     "jet_cutsize": (C.c_int, [P, P, P, P]),
     "jet_part_weights": (C.c_int, [P, P, P, i32, P]),
@@ -237,6 +244,45 @@ class Context:
 
     def flush_l2(self):
         check(lib().jet_flush_l2(self.handle))
+
+    # 1D vertex sharding (include/jet.h) ------------------------------------
+    def attach_local(self, group: "LocalGroup", rank: int):
+        check(lib().jet_comm_attach_local(self.handle, group.handle, int(rank)))
+        self._group = group  # keep the group alive while attached
+
+    def attach_nccl(self, nccl_id: bytes, rank: int, size: int):
+        buf = C.create_string_buffer(bytes(nccl_id), 128)
+        check(lib().jet_comm_attach_nccl(self.handle, buf, int(rank), int(size)))
+
+    def detach(self):
+        check(lib().jet_comm_detach(self.handle))
+        self._group = None
+
+    def set_shard_min_vertices(self, n: int):
+        check(lib().jet_set_shard_min_vertices(self.handle, int(n)))
+
+
+class LocalGroup:
+    """`size` virtual ranks (one context + host thread each) in one process."""
+
+    def __init__(self, size: int):
+        h = P()
+        check(lib().jet_comm_local_group(int(size), C.byref(h)))
+        self.handle, self.size = h, int(size)
+
+    def __del__(self):  # pragma: no cover
+        try:
+            if self.handle:
+                lib().jet_comm_local_group_free(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib().jet_comm_nccl_id(buf))
+    return buf.raw
 
 
 class DeviceGraph:

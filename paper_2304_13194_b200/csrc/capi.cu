@@ -3,12 +3,14 @@
 #include "common.cuh"
 #include "graph.cuh"
 #include "coarsen.cuh"
+#include "comm.cuh"
 #include "refine.cuh"
 #include "controller.cuh"
 #include "initpart.h"
 #include "rng.h"
 #include <chrono>
 #include <cstring>
+#include <cstdlib>
 
 struct jet_graph {
   std::unique_ptr<jet::DGraph> g;
@@ -87,6 +89,63 @@ int jet_graph_upload(jet_ctx* ctx, int64_t n, const int64_t* row_offsets, const 
   jg->ctx = &c;
   ctx_retain(&c);
   *out = jg;
+  API_END
+}
+
+struct jet_group {
+  jet::LocalGroup g;
+  explicit jet_group(int n) : g(n) {}
+};
+
+int jet_comm_nccl_id(uint8_t* id128) {
+  API_BEGIN
+  JET_REQUIRE(id128, JET_EINVAL, "id is NULL");
+  JET_REQUIRE(nccl_unique_id(id128), JET_EUNSUPPORTED, "ncclGetUniqueId failed (libnccl.so.2)");
+  API_END
+}
+
+int jet_comm_attach_nccl(jet_ctx* ctx, const uint8_t* id128, int32_t rank, int32_t size) {
+  API_BEGIN
+  Ctx& c = C(ctx);
+  JET_REQUIRE(id128 && size >= 1 && rank >= 0 && rank < size, JET_EINVAL, "bad rank/size");
+  Comm* m = make_nccl_comm(id128, rank, size);
+  delete c.comm;
+  c.comm = m;
+  API_END
+}
+
+int jet_comm_local_group(int32_t size, jet_group** out) {
+  API_BEGIN
+  JET_REQUIRE(out && size >= 1, JET_EINVAL, "bad group size");
+  *out = new jet_group(size);
+  API_END
+}
+
+void jet_comm_local_group_free(jet_group* g) { delete g; }
+
+int jet_comm_attach_local(jet_ctx* ctx, jet_group* g, int32_t rank) {
+  API_BEGIN
+  Ctx& c = C(ctx);
+  JET_REQUIRE(g && rank >= 0 && rank < g->g.size, JET_EINVAL, "bad rank");
+  delete c.comm;
+  c.comm = new LocalComm(&g->g, rank);
+  API_END
+}
+
+int jet_comm_detach(jet_ctx* ctx) {
+  API_BEGIN
+  Ctx& c = C(ctx);
+  delete c.comm;
+  c.comm = nullptr;
+  API_END
+}
+
+int jet_set_shard_min_vertices(jet_ctx* ctx, int64_t n) {
+  API_BEGIN
+  JET_REQUIRE(n >= 1, JET_EINVAL, "shard_min_vertices must be >= 1");
+  C(ctx).shard_min_n = n;
+  const char* e = getenv("JET_SHARD_SINGLE");
+  C(ctx).shard_single = e && e[0] == '1';
   API_END
 }
 

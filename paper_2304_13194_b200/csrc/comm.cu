@@ -1,0 +1,146 @@
+// comm.cu — transports of the sharded refinement's exchange step (comm.cuh).
+#include "comm.cuh"
+#include <dlfcn.h>
+#include <algorithm>
+#include <numeric>
+#include <string>
+
+namespace jet {
+
+void LocalGroup::barrier() {
+  std::unique_lock<std::mutex> lk(m);
+  const int64_t gen = generation;
+  if (++arrived == size) {
+    arrived = 0;
+    ++generation;
+    cv.notify_all();
+  } else {
+    cv.wait(lk, [&] { return generation != gen; });
+  }
+}
+
+void LocalComm::allgatherv(Ctx& c, const void* dsend, int64_t bytes, DBuf<uint8_t>& recv,
+                           std::vector<int64_t>& counts) {
+  c.sync();  // the send buffer is complete
+  g->ptrs[rank] = dsend;
+  g->bytes[rank] = bytes;
+  g->barrier();
+  counts = g->bytes;
+  const int64_t total = std::accumulate(counts.begin(), counts.end(), (int64_t)0);
+  recv.ensure((size_t)std::max<int64_t>(total, 1), c.stream);
+  int64_t off = 0;
+  for (int r = 0; r < size; ++r) {
+    if (counts[r])
+      CK(cudaMemcpyAsync(recv.get() + off, g->ptrs[r], (size_t)counts[r], cudaMemcpyDeviceToDevice,
+                         c.stream));
+    off += counts[r];
+  }
+  c.sync();
+  g->barrier();  // no rank reuses its send buffer before every copy is done
+}
+
+// ---- NCCL, opened at run time (no link-time dependency) -------------------
+namespace {
+typedef struct {
+  char internal[128];
+} NcclId;
+typedef void* NcclComm_t;
+typedef int (*PGetUniqueId)(NcclId*);
+typedef int (*PCommInitRank)(NcclComm_t*, int, NcclId, int);
+typedef int (*PAllGather)(const void*, void*, size_t, int, NcclComm_t, cudaStream_t);
+typedef int (*PCommDestroy)(NcclComm_t);
+typedef const char* (*PGetErrorString)(int);
+constexpr int NCCL_INT8 = 0;
+
+struct NcclApi {
+  void* h = nullptr;
+  PGetUniqueId get_id = nullptr;
+  PCommInitRank init = nullptr;
+  PAllGather allgather = nullptr;
+  PCommDestroy destroy = nullptr;
+  PGetErrorString err = nullptr;
+  bool load() {
+    if (h) return true;
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    get_id = (PGetUniqueId)dlsym(h, "ncclGetUniqueId");
+    init = (PCommInitRank)dlsym(h, "ncclCommInitRank");
+    allgather = (PAllGather)dlsym(h, "ncclAllGather");
+    destroy = (PCommDestroy)dlsym(h, "ncclCommDestroy");
+    err = (PGetErrorString)dlsym(h, "ncclGetErrorString");
+    return get_id && init && allgather && destroy;
+  }
+};
+NcclApi& nccl() {
+  static NcclApi a;
+  return a;
+}
+
+void nck(int rc, const char* what) {
+  if (rc != 0)
+    throw Error(JET_ECUDA, std::string(what) + ": " + (nccl().err ? nccl().err(rc) : "nccl error"));
+}
+
+struct NcclComm : Comm {
+  NcclComm_t comm = nullptr;
+  DBuf<int64_t> cnt;
+  DBuf<uint8_t> stage, padded;
+  ~NcclComm() override {
+    if (comm) nccl().destroy(comm);
+  }
+  void allgatherv(Ctx& c, const void* dsend, int64_t bytes, DBuf<uint8_t>& recv,
+                  std::vector<int64_t>& counts) override {
+    cnt.ensure((size_t)size + 1, c.stream);
+    h2d(c, cnt.get() + size, &bytes, 1);
+    nck(nccl().allgather(cnt.get() + size, cnt.get(), sizeof(int64_t), NCCL_INT8, comm, c.stream),
+        "ncclAllGather(counts)");
+    counts.assign(size, 0);
+    d2h(c, counts.data(), cnt.get(), size);
+    c.sync();
+    const int64_t mx = std::max<int64_t>(1, *std::max_element(counts.begin(), counts.end()));
+    stage.ensure((size_t)mx, c.stream);
+    padded.ensure((size_t)mx * size, c.stream);
+    if (bytes)
+      CK(cudaMemcpyAsync(stage.get(), dsend, (size_t)bytes, cudaMemcpyDeviceToDevice, c.stream));
+    nck(nccl().allgather(stage.get(), padded.get(), (size_t)mx, NCCL_INT8, comm, c.stream),
+        "ncclAllGather");
+    const int64_t total = std::accumulate(counts.begin(), counts.end(), (int64_t)0);
+    recv.ensure((size_t)std::max<int64_t>(total, 1), c.stream);
+    int64_t off = 0;
+    for (int r = 0; r < size; ++r) {
+      if (counts[r])
+        CK(cudaMemcpyAsync(recv.get() + off, padded.get() + (size_t)r * mx, (size_t)counts[r],
+                           cudaMemcpyDeviceToDevice, c.stream));
+      off += counts[r];
+    }
+  }
+};
+}  // namespace
+
+bool nccl_unique_id(unsigned char id[128]) {
+  if (!nccl().load()) return false;
+  NcclId x;
+  if (nccl().get_id(&x) != 0) return false;
+  std::copy(x.internal, x.internal + 128, id);
+  return true;
+}
+
+Comm* make_nccl_comm(const unsigned char id[128], int rank, int size) {
+  JET_REQUIRE(nccl().load(), JET_EUNSUPPORTED, "libnccl.so.2 not found");
+  NcclId x;
+  std::copy(id, id + 128, x.internal);
+  auto* c = new NcclComm();
+  c->rank = rank;
+  c->size = size;
+  const int rc = nccl().init(&c->comm, size, x, rank);
+  if (rc != 0) {
+    delete c;
+    nck(rc, "ncclCommInitRank");
+  }
+  return c;
+}
+
+}  // namespace jet

@@ -165,8 +165,16 @@ struct CtxExt {
   virtual ~CtxExt() = default;
 };
 
+struct Comm;  // comm.cuh: exchange step of the sharded refinement
+
 struct Ctx {
   int device = 0;
+  // 1D vertex sharding: with a communicator of size > 1,
+  // levels of at least shard_min_n vertices refine with sharded Jetlp
+  // sweeps (this rank's vertex block) and exchange the candidates / moves.
+  Comm* comm = nullptr;
+  int64_t shard_min_n = 1 << 20;
+  bool shard_single = false;  // run the sharded path with one rank (transport tests)
   // Graphs and hierarchies allocated on this context's stream hold a
   // reference, so the stream outlives every buffer freed on it whatever
   // order the caller (e.g. interpreter teardown) releases handles in.

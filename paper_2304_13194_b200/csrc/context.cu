@@ -1,5 +1,6 @@
 // context.cu — jet_ctx lifetime, error reporting and launch profiling.
 #include "common.cuh"
+#include "comm.cuh"
 #include <algorithm>
 #include <cstdlib>
 #include <cstdlib>
@@ -95,6 +96,8 @@ static void ctx_teardown(Ctx* c) {
   c->cub_tmp.release();
   c->flush_buf.release();
   c->level_ext.reset();
+  delete c->comm;
+  c->comm = nullptr;
   for (auto& b : c->scratch_slots) b.release();
   if (c->timer_a) cudaEventDestroy(c->timer_a);
   if (c->timer_b) cudaEventDestroy(c->timer_b);

@@ -3,6 +3,7 @@
 // device passes. Per iteration the only device->host traffic is the counter
 // block (move counts, doubled cut delta) plus the k part weights.
 #include "controller.cuh"
+#include "comm.cuh"
 #include "coarsen.cuh"
 #include "initpart.h"
 #include "rng.h"
@@ -21,7 +22,12 @@ static double now_s() {
 void refine_level(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, int64_t& cut,
                   const jet_config& cfg, bool finest, int level, jet_level_stats& st,
                   DBuf<int32_t>& keep) {
-  if (!c.host_levels && refine_level_device(c, w, g, parts, cut, cfg, finest, level, st, keep))
+  // sharded levels run the host-driven passes: the exchange
+  // steps are collectives between ranks, outside any kernel
+  const bool sharded = c.comm && (c.comm->size > 1 || c.shard_single) && g.n >= c.shard_min_n &&
+                       cfg.afterburner != 0;
+  if (!sharded && !c.host_levels &&
+      refine_level_device(c, w, g, parts, cut, cfg, finest, level, st, keep))
     return;
   const int k = cfg.k;
   const int64_t limit = cfg.limit, sigma = cfg.sigma;
@@ -29,6 +35,8 @@ void refine_level(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, int64_t
   w.bind_level(g);
   h2d(c, w.d_pw(), w.h_pw.data(), k);
   keep.ensure(g.n, c.stream);
+  ShardLists sh;
+  if (sharded) build_shard_lists(c, g, c.comm->rank, c.comm->size, sh);
 
   LpParams lp;
   lp.c_num = finest ? cfg.c_finest_num : cfg.c_other_num;
@@ -62,7 +70,8 @@ void refine_level(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, int64_t
       rebal_streak = 0;
       locks_all_clear = !cfg.locking || locked == 0;
       lp.lock_epoch = epoch;
-      lp_pass(c, w, g, parts, k, lp, nullptr);
+      if (sharded) lp_pass_sharded(c, w, g, parts, k, lp, sh);
+      else lp_pass(c, w, g, parts, k, lp, nullptr);
       is_lp = true;
       st.lp_passes++;
     } else {

@@ -11,6 +11,7 @@
 //   weak/strong passes   rebalance.py:139-240
 //   ConnectivityTable.apply (parts, part weights, exact cut delta) conn.py:215-254
 #include "refine_dev.cuh"
+#include "comm.cuh"
 #include "rng.h"
 #include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
@@ -304,6 +305,220 @@ __global__ void k_distribute(const int32_t* __restrict__ cand, int64_t ncand,
     for (int tt = 0; tt < NBINS; ++tt)
       warp_append(t == tt, v, lists + segs.b[tt], cnts + tt);
   }
+}
+
+// ---------------------------------------------------------------------------
+// 1D vertex sharding of the Jetlp pass (comm.cuh for the exchange).
+__global__ void k_shard_bounds(const int64_t* __restrict__ offs, int64_t n, int size,
+                               int64_t* bounds) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > size) return;
+  const int64_t nnz = offs[n];
+  const int64_t want = r == size ? nnz + 1 : (nnz * r) / size;
+  int64_t lo = 0, hi = n;  // first v with offs[v] >= want (v = n if none)
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (offs[mid] < want) lo = mid + 1;
+    else hi = mid;
+  }
+  bounds[r] = r == 0 ? 0 : (r == size ? n : lo);
+}
+
+// [first, last) of the ascending tier list inside [lo, hi)
+__global__ void k_sublist(const int32_t* __restrict__ list, int64_t cnt, int64_t lo, int64_t hi,
+                          int64_t* out) {
+  if (threadIdx.x > 1) return;
+  const int64_t key = threadIdx.x == 0 ? lo : hi;
+  int64_t a = 0, b = cnt;
+  while (a < b) {
+    const int64_t mid = (a + b) >> 1;
+    if (list[mid] < key) a = mid + 1;
+    else b = mid;
+  }
+  out[threadIdx.x] = a;
+}
+
+__global__ void k_iota(int32_t* p, int64_t lo, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = (int32_t)(lo + i);
+}
+
+void build_shard_lists(Ctx& c, const DGraph& g, int rank, int size, ShardLists& s) {
+  s.scratch.ensure((size_t)size + 1 + 2 * NBINS, c.stream);
+  k_shard_bounds<<<1, 1024, 0, c.stream>>>(g.offs.get(), g.n, size, s.scratch.get());
+  CK(cudaGetLastError());
+  std::vector<int64_t> b(size + 1);
+  d2h(c, b.data(), s.scratch.get(), size + 1);
+  c.sync();
+  s.lo = b[rank];
+  s.hi = b[rank + 1];
+  unsigned long long cnts[NBINS] = {};
+  for (int t = 0; t < NBINS; ++t) {
+    s.list[t] = nullptr;
+    if (!g.bin_cnt[t]) continue;
+    const int32_t* full = tier_list(g, t);
+    if (!full) {  // identity tier: every vertex
+      s.iota.ensure((size_t)std::max<int64_t>(1, s.hi - s.lo), c.stream);
+      k_iota<<<grid_for(c, s.hi - s.lo, 256), 256, 0, c.stream>>>(s.iota.get(), s.lo, s.hi - s.lo);
+      CK(cudaGetLastError());
+      s.list[t] = s.iota.get();
+      cnts[t] = (unsigned long long)(s.hi - s.lo);
+      continue;
+    }
+    int64_t* o = s.scratch.get() + size + 1 + 2 * t;
+    k_sublist<<<1, 32, 0, c.stream>>>(full, g.bin_cnt[t], s.lo, s.hi, o);
+    CK(cudaGetLastError());
+    int64_t ab[2];
+    d2h(c, ab, o, 2);
+    c.sync();
+    s.list[t] = const_cast<int32_t*>(full) + ab[0];
+    cnts[t] = (unsigned long long)(ab[1] - ab[0]);
+  }
+  s.dcnt.ensure(NBINS, c.stream);
+  h2d(c, s.dcnt.get(), cnts, NBINS);
+  c.sync();
+}
+
+struct CandRec {
+  int32_t v, dest;
+  long long F;
+};
+
+__global__ void k_pack_cands(SegLists sl, const int32_t* __restrict__ cdest,
+                             const long long* __restrict__ F, CandRec* out) {
+  int64_t base = 0;
+  for (int t = 0; t < NBINS; ++t) {
+    const int64_t cnt = (int64_t)sl.cnt[t];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const int v = sl.list[t][i];
+      out[base + i] = CandRec{v, cdest[v], F[v]};
+    }
+    base += cnt;
+  }
+}
+
+// remote records only: [0, skip_lo) and [skip_hi, total)
+__global__ void k_unpack_cands(const CandRec* __restrict__ in, int64_t total, int64_t skip_lo,
+                               int64_t skip_hi, int32_t* cdest, long long* F) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i >= skip_lo && i < skip_hi) continue;
+    const CandRec r = in[i];
+    cdest[r.v] = r.dest;
+    F[r.v] = r.F;
+  }
+}
+
+__global__ void k_pack_moves(SegLists sl, const int32_t* __restrict__ mv, int2* out) {
+  int64_t base = 0;
+  for (int t = 0; t < NBINS; ++t) {
+    const int64_t cnt = (int64_t)sl.cnt[t];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const int v = sl.list[t][i];
+      out[base + i] = make_int2(v, mv[v]);
+    }
+    base += cnt;
+  }
+}
+
+__global__ void k_unpack_moves(const int2* __restrict__ in, int64_t total, int64_t skip_lo,
+                               int64_t skip_hi, int32_t* mv, const int64_t* __restrict__ offs,
+                               TierMap tm, int32_t* move_lists, RbSegsDev seg,
+                               unsigned long long* move_cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i >= skip_lo && i < skip_hi) continue;
+    const int2 r = in[i];
+    mv[r.x] = r.y;
+    const int t = tm(offs[r.x + 1] - offs[r.x]);
+    move_lists[seg.b[t] + atomicAdd(move_cnt + t, 1ull)] = r.x;
+  }
+}
+
+void lp_pass_sharded(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts, int k,
+                     const LpParams& p, ShardLists& sh) {
+  JET_REQUIRE(c.comm && p.afterburner, JET_EUNSUPPORTED,
+              "sharded Jetlp needs a communicator and the afterburner");
+  Comm& cm = *c.comm;
+  dzero(c, w.ctr.get(), CTR_PW);
+  launch(c, "shard_fill", 4.0 * g.n, [&] {
+    k_fill_i32<<<grid_for(c, g.n, 256), 256, 0, c.stream>>>(w.cdest.get(), g.n, -1);
+  });
+  auto mk = [&](int t) {
+    LpOp::Args a{};
+    a.parts = parts;
+    a.cdest = w.cdest.get();
+    a.F = w.F.get();
+    a.mv = w.mv.get();
+    a.lock = w.lock.get();
+    a.p = p;
+    a.out_list = w.cand_list(t);
+    a.out_cnt = w.ctr.get() + CTR_CAND + t;
+    a.cut2 = w.ctr.get() + CTR_CUT2;
+    return a;
+  };
+  run_agg<LpOp>(c, g, mk, parts, k, "lp_gains", 20.0, sh.list, sh.dcnt.get());
+  // candidates: (id, destination, gain) of every rank
+  unsigned long long hc[2 * NBINS];
+  d2h(c, hc, w.ctr.get(), 2 * NBINS);
+  c.sync();
+  int64_t nc = 0;
+  for (int t = 0; t < NBINS; ++t) nc += (int64_t)hc[CTR_CAND + t];
+  sh.send.ensure((size_t)std::max<int64_t>(1, nc) * sizeof(CandRec), c.stream);
+  const SegLists cl = seg_lists(w, false);
+  launch(c, "shard_pack", 16.0 * nc, [&] {
+    k_pack_cands<<<grid_for(c, nc, 256), 256, 0, c.stream>>>(cl, w.cdest.get(), w.F.get(),
+                                                              (CandRec*)sh.send.get());
+  });
+  std::vector<int64_t> counts;
+  cm.allgatherv(c, sh.send.get(), nc * (int64_t)sizeof(CandRec), sh.recv, counts);
+  int64_t total = 0, mine_lo = 0;
+  for (int r = 0; r < cm.size; ++r) {
+    if (r == cm.rank) mine_lo = total;
+    total += counts[r];
+  }
+  total /= (int64_t)sizeof(CandRec);
+  mine_lo /= (int64_t)sizeof(CandRec);
+  launch(c, "shard_unpack", 16.0 * total, [&] {
+    k_unpack_cands<<<grid_for(c, total, 256), 256, 0, c.stream>>>(
+        (const CandRec*)sh.recv.get(), total, mine_lo, mine_lo + nc, w.cdest.get(), w.F.get());
+  });
+  // afterburner on owned candidates -> owned moves
+  AbArgs ab{};
+  ab.parts = parts;
+  ab.cdest = w.cdest.get();
+  ab.F = w.F.get();
+  ab.mv = w.mv.get();
+  ab.move_list = w.lists.get();
+  launch_rows_reduce_ab(c, w, g, ab);
+  // moves of every rank, appended to the local move lists
+  d2h(c, hc, w.ctr.get(), 2 * NBINS);
+  c.sync();
+  int64_t nm = 0;
+  for (int t = 0; t < NBINS; ++t) nm += (int64_t)hc[CTR_MOVE + t];
+  sh.send.ensure((size_t)std::max<int64_t>(1, nm) * sizeof(int2), c.stream);
+  const SegLists ml = seg_lists(w, true);
+  launch(c, "shard_pack", 8.0 * nm, [&] {
+    k_pack_moves<<<grid_for(c, nm, 256), 256, 0, c.stream>>>(ml, w.mv.get(), (int2*)sh.send.get());
+  });
+  cm.allgatherv(c, sh.send.get(), nm * (int64_t)sizeof(int2), sh.recv, counts);
+  total = 0;
+  for (int r = 0; r < cm.size; ++r) {
+    if (r == cm.rank) mine_lo = total;
+    total += counts[r];
+  }
+  total /= (int64_t)sizeof(int2);
+  mine_lo /= (int64_t)sizeof(int2);
+  RbSegsDev ms;
+  for (int t = 0; t < NBINS; ++t) ms.b[t] = w.seg_base[t];
+  launch(c, "shard_unpack", 8.0 * total, [&] {
+    k_unpack_moves<<<grid_for(c, total, 256), 256, 0, c.stream>>>(
+        (const int2*)sh.recv.get(), total, mine_lo, mine_lo + nm, w.mv.get(), g.offs.get(), g.tm,
+        w.lists.get() + w.cap_n, ms, w.ctr.get() + CTR_MOVE);
+  });
 }
 
 void afterburner_only(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,

@@ -73,6 +73,28 @@ struct ApplyResult {
 void lp_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts, int k,
              const LpParams& p, const LpDebug* dbg);
 
+// This rank's vertex block of a level (1D sharding): the
+// block [lo, hi) balances entries (row offsets), and every tier list of the
+// level -- ascending vertex ids -- restricted to the block is a contiguous
+// sub-range, so the sweeps run on sub-lists without copying the graph.
+struct ShardLists {
+  int64_t lo = 0, hi = 0;
+  int32_t* list[NBINS] = {};
+  DBuf<int32_t> iota;                // identity tier: explicit [lo, hi)
+  DBuf<unsigned long long> dcnt;     // NBINS device counts
+  DBuf<int64_t> scratch;
+  DBuf<uint8_t> send, recv;          // exchange buffers
+};
+void build_shard_lists(Ctx& c, const DGraph& g, int rank, int size, ShardLists& s);
+
+// Jetlp pass on this rank's block: gains/filter sweep over owned vertices,
+// all-gather of the candidates (id, destination, gain) so every rank sees
+// its neighbours' afterburner inputs, afterburner on owned candidates,
+// all-gather of the moves. Every rank then holds the full move set (the
+// apply and the rebalancing passes run replicated on identical state).
+void lp_pass_sharded(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts, int k,
+                     const LpParams& p, ShardLists& sh);
+
 // Rebalancing pass (rebalance.py:139-240). Host-side scalars come from the
 // part weights in w.h_pw. Returns false when no valid destination exists
 // (RebalanceInfeasibleError). `rng` is advanced exactly as numpy's would be.
