@@ -8,8 +8,20 @@
 #include <algorithm>
 #include <cstring>
 #include <omp.h>
+#include <climits>
+#include <cstdlib>
 
 namespace jet {
+
+// host threads for the staging copies (JET_UPLOAD_THREADS, default 16)
+static int upload_threads() {
+  static const int t = [] {
+    const char* e = getenv("JET_UPLOAD_THREADS");
+    const int v = e ? atoi(e) : 16;
+    return v > 0 ? v : 16;
+  }();
+  return t;
+}
 
 // memcpy split over the host cores (pageable -> pinned staging)
 static void parallel_memcpy(void* dst, const void* src, size_t bytes) {
@@ -19,11 +31,54 @@ static void parallel_memcpy(void* dst, const void* src, size_t bytes) {
     memcpy(dst, src, bytes);
     return;
   }
-#pragma omp parallel for schedule(static) num_threads(std::min<int>(8, omp_get_num_procs()))
+#pragma omp parallel for schedule(static) num_threads(std::min<int>(upload_threads(), omp_get_num_procs()))
   for (int64_t i = 0; i < np; ++i) {
     const size_t o = (size_t)i * piece;
     memcpy((char*)dst + o, (const char*)src + o, std::min(piece, bytes - o));
   }
+}
+
+// int64 -> int32 on the host cores while staging into pinned memory, with the
+// range check; returns false when a value is outside [lo, hi]. *all_one is
+// set when every value equals 1 (unit weights need no transfer at all).
+static bool parallel_narrow(int32_t* dst, const int64_t* src, int64_t count, long long lo,
+                            long long hi, bool check_ones, bool* all_one) {
+  const int64_t piece = (int64_t)1 << 19;
+  const int64_t np = (count + piece - 1) / piece;
+  int bad = 0, notone = 0;
+#pragma omp parallel for schedule(static) num_threads(std::min<int>(upload_threads(), omp_get_num_procs())) \
+    reduction(| : bad, notone)
+  for (int64_t i = 0; i < np; ++i) {
+    const int64_t b = i * piece, e = std::min(count, b + piece);
+    long long mn = LLONG_MAX, mx = LLONG_MIN;
+    if (check_ones) {
+      // pure scan first: a unit-weight chunk is never written
+      for (int64_t j = b; j < e; ++j) {
+        const long long x = src[j];
+        mn = x < mn ? x : mn;
+        mx = x > mx ? x : mx;
+      }
+      if (mn == 1 && mx == 1) continue;
+      notone = 1;
+      mn = LLONG_MAX;
+      mx = LLONG_MIN;
+    }
+    for (int64_t j = b; j < e; ++j) {
+      const long long x = src[j];
+      mn = x < mn ? x : mn;
+      mx = x > mx ? x : mx;
+      dst[j] = (int32_t)x;
+    }
+    if (mn < lo || mx > hi) bad = 1;
+  }
+  if (all_one) *all_one = check_ones && !notone;
+  return !bad;
+}
+
+__global__ void k_fill_ones(int32_t* p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -224,9 +279,35 @@ std::unique_ptr<DGraph> upload_graph(Ctx& c, int64_t n, const int64_t* offs,
   // threads copy chunk i+1 into pinned memory while chunk i is DMA'd and
   // narrowed to int32 on the device (pageable cudaMemcpy tops out far below
   // the link rate).
+  unsigned host_bad = 0;
   auto put = [&](const void* src, int dt, int32_t* dst, int64_t count, long long lo,
                  long long hi, int flag) {
     if (count == 0) return;
+    if (dt == JET_I64) {
+      // narrow (and range-check) on the host while staging: half the bytes
+      // cross PCIe; all-ones weight chunks are not transferred but filled
+      c.ensure_upload_ring();
+      const int64_t per = (int64_t)(Ctx::UPLOAD_CHUNK / sizeof(int32_t));
+      const int64_t* s64 = static_cast<const int64_t*>(src);
+      for (int64_t e0 = 0, i = 0; e0 < count; e0 += per, ++i) {
+        const int64_t m = std::min(per, count - e0);
+        const int b = (int)(i % Ctx::UPLOAD_BUFS);
+        CK(cudaEventSynchronize(c.up_ev[b]));
+        bool ones = false;
+        int32_t* h32 = static_cast<int32_t*>(c.up_host[b]);
+        if (!parallel_narrow(h32, s64 + e0, m, lo, hi, flag != BAD_ADJ, &ones)) host_bad |= flag;
+        if (ones) {
+          launch(c, "fill_ones", 4.0 * m, [&] {
+            k_fill_ones<<<grid_for(c, m, 256), 256, 0, c.stream>>>(dst + e0, m);
+          });
+        } else {
+          CK(cudaMemcpyAsync(dst + e0, h32, (size_t)m * sizeof(int32_t), cudaMemcpyHostToDevice,
+                             c.stream));
+        }
+        CK(cudaEventRecord(c.up_ev[b], c.stream));
+      }
+      return;
+    }
     const size_t esz = dt == JET_I32 ? 4 : 8;
     staged_upload(c, src, (size_t)count * esz, [&](const void* dchunk, size_t off, size_t bytes) {
       const int64_t e0 = (int64_t)(off / esz), m = (int64_t)(bytes / esz);
@@ -250,6 +331,7 @@ std::unique_ptr<DGraph> upload_graph(Ctx& c, int64_t n, const int64_t* offs,
   unsigned hbad = 0;
   d2h(c, &hbad, bad.get(), 1);
   c.sync();
+  hbad |= host_bad;
   JET_REQUIRE(!(hbad & BAD_OFFS), JET_EINVAL, "row_offsets must be non-decreasing from 0 to nnz");
   JET_REQUIRE(!(hbad & BAD_ADJ), JET_EINVAL, "neighbor id out of range");
   JET_REQUIRE(!(hbad & BAD_EW), JET_EINVAL, "edge weights must be in [1, 2^31)");
