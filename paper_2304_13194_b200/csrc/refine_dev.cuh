@@ -998,8 +998,9 @@ static __device__ void rb_find_op(int op, const RbSel& s, const long long* __res
 
 // First index i of arr[0, len) where run + prefix_sum(arr)[i] >= D; *before =
 // run + prefix before i. Returns -1 (and *before = run + total) if never.
-static __device__ __forceinline__ int warp_cross(const unsigned long long* __restrict__ arr, int len,
-                                                 long long D, long long run, long long* before) {
+static __device__ __forceinline__ int warp_cross_linear(const unsigned long long* __restrict__ arr,
+                                                        int len, long long D, long long run,
+                                                        long long* before) {
   const int lane = threadIdx.x & 31;
   for (int b0 = 0; b0 < len; b0 += 32) {
     const int i = b0 + lane;
@@ -1021,6 +1022,43 @@ static __device__ __forceinline__ int warp_cross(const unsigned long long* __res
   }
   *before = run;
   return -1;
+}
+
+// First index where the running sum (from `run`) of arr reaches D (and was
+// below D before it), or -1; *before = running sum before that index (or the
+// total). Two levels: every lane sums a contiguous segment with independent
+// loads, the warp scans the segment sums, then only the crossing segment is
+// walked -- a few memory round trips instead of len/32 dependent ones.
+static __device__ __forceinline__ int warp_cross(const unsigned long long* __restrict__ arr, int len,
+                                                 long long D, long long run, long long* before) {
+  if (len <= 64) return warp_cross_linear(arr, len, D, run, before);
+  const int lane = threadIdx.x & 31;
+  const int seg = (len + 31) / 32;
+  const int b = min(len, lane * seg), e = min(len, b + seg);
+  long long sm = 0;
+#pragma unroll 4
+  for (int i = b; i < e; ++i) sm += (long long)arr[i];
+  long long incl = sm;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((int)lane >= o) incl += y;
+  }
+  const long long total = __shfl_sync(0xffffffffu, incl, 31);
+  if (run >= D) {  // reached before the first element: no crossing
+    *before = run + total;
+    return -1;
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, run + incl >= D);
+  if (!m) {
+    *before = run + total;
+    return -1;
+  }
+  const int l = __ffs(m) - 1;
+  const long long base = run + __shfl_sync(0xffffffffu, incl - sm, l);
+  const int lb = min(len, l * seg);
+  const int r = warp_cross_linear(arr + lb, min(seg, len - lb), D, base, before);
+  return r < 0 ? -1 : lb + r;
 }
 
 // bucket crossing (select_prefix on bucket totals): the crossing slot from
