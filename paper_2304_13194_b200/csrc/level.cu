@@ -418,6 +418,14 @@ __device__ RbSel lv_sel(const LevelArgs& A) {
   return RbSel{A.parts, A.g.vw, A.opidx, A.rkey, A.bstar, A.thr, ldv(&C->rho), ldv(&C->nch), A.CH};
 }
 
+// per-warp staging words of the short-row sweeps (largest tier variant)
+template <bool UNIT>
+__host__ __device__ constexpr int lv_stage_words() {
+  return stage_words<32, LV_RB / 2, UNIT, 2>() > stage_words<32, LV_RB, UNIT, 1>()
+             ? stage_words<32, LV_RB / 2, UNIT, 2>()
+             : stage_words<32, LV_RB, UNIT, 1>();
+}
+
 // --------------------------------------------------------- tier sweeps
 template <class Op, bool UNIT, class MakeArgs>
 __device__ void lv_sweep(const LevelArgs& A, MakeArgs mk, const int32_t* const* lists,
@@ -434,7 +442,7 @@ __device__ void lv_sweep(const LevelArgs& A, MakeArgs mk, const int32_t* const* 
     const unsigned long long* dc = dcnts ? dcnts + t : nullptr;
     const int64_t cnt = A.tcnt[t];
     uint32_t* stg = reinterpret_cast<uint32_t*>(smem) +
-                    (threadIdx.x >> 5) * stage_words<32, LV_RB / 2, UNIT>();
+                    (threadIdx.x >> 5) * lv_stage_words<UNIT>();
     switch (t) {
       case 0: agg_small<Op, 4, UNIT, LV_RB>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc, stg); break;
       case 1: agg_small<Op, 8, UNIT, LV_RB>(a, A.g, A.parts, list, cnt, wide, dc, w0, nw, acc, stg); break;
@@ -884,7 +892,7 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   const int tl_cap = (int)std::min<int64_t>(k, WARP_TIER_MAX_DEG);
   const size_t per = ((size_t)k + (size_t)(tl_cap + 3) / 2) * 8;
   size_t smem = (size_t)LV_TAIL_SMEM * 8 + LV_BLOCK * 8;
-  smem = std::max(smem, (size_t)(LV_BLOCK / 32) * stage_words<32, LV_RB / 2, false>() * 4);
+  smem = std::max(smem, (size_t)(LV_BLOCK / 32) * lv_stage_words<false>() * 4);
   if (g.bin_cnt[BIN_WARP]) smem = std::max(smem, per * (LV_BLOCK / 32));
   if (g.bin_cnt[BIN_BLOCK]) smem = std::max(smem, (size_t)k * 12);
   if (smem > (size_t)c.max_smem_optin) return false;

@@ -21,28 +21,30 @@
 namespace jet {
 
 // Kernel wrappers of the aggregation device functions (multi-kernel path).
-template <class Op, int G, bool UNIT>
+// E = entries per lane (tier 3 holds rows of up to 64 entries; levels whose
+// rows all fit 32 use one entry per lane, as the level kernel does)
+template <class Op, int G, bool UNIT, int E = tier_e<G>()>
 __global__ void __launch_bounds__(256)
     k_agg_small(typename Op::Args a, GView g, const int32_t* __restrict__ parts,
                 const int32_t* __restrict__ list, int64_t cnt, bool wide,
                 const unsigned long long* __restrict__ dcnt) {
   extern __shared__ uint32_t agg_stage[];
   long long acc = 0;
-  constexpr int RB = G == 32 ? 16 : 32;
-  agg_small<Op, G, UNIT, RB>(a, g, parts, list, cnt, wide, dcnt,
-                             (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5,
-                             ((int64_t)gridDim.x * blockDim.x) >> 5, acc,
-                             agg_stage + (threadIdx.x >> 5) * stage_words<G, RB, UNIT>());
+  constexpr int RB = G * E == 64 ? 16 : 32;
+  agg_small<Op, G, UNIT, RB, E>(a, g, parts, list, cnt, wide, dcnt,
+                                (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5,
+                                ((int64_t)gridDim.x * blockDim.x) >> 5, acc,
+                                agg_stage + (threadIdx.x >> 5) * stage_words<G, RB, UNIT, E>());
   Op::block_done(a, acc);
 }
 
-// dynamic shared memory of k_agg_small<Op, G, UNIT> (8 warps), set once
-template <class Op, int G, bool UNIT>
+// dynamic shared memory of k_agg_small<Op, G, UNIT, E> (8 warps), set once
+template <class Op, int G, bool UNIT, int E = tier_e<G>()>
 static size_t agg_small_smem() {
   static const size_t bytes = [] {
-    const size_t b = (size_t)8 * stage_words<G, (G == 32 ? 16 : 32), UNIT>() * 4;
-    CK(cudaFuncSetAttribute(k_agg_small<Op, G, UNIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)b));
+    const size_t b = (size_t)8 * stage_words<G, (G * E == 64 ? 16 : 32), UNIT, E>() * 4;
+    CK(cudaFuncSetAttribute(k_agg_small<Op, G, UNIT, E>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b));
     return b;
   }();
   return bytes;
@@ -114,14 +116,24 @@ static void run_agg(Ctx& c, const DGraph& g, MakeArgs mk, const int32_t* parts,
             case 4: AGG_K(4, true)<<<grid, 256, agg_small_smem<Op, 4, true>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
             case 8: AGG_K(8, true)<<<grid, 256, agg_small_smem<Op, 8, true>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
             case 16: AGG_K(16, true)<<<grid, 256, agg_small_smem<Op, 16, true>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
-            default: AGG_K(32, true)<<<grid, 256, agg_small_smem<Op, 32, true>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
+            default:
+              if (g.max_deg <= 32)
+                k_agg_small<Op, 32, true, 1><<<grid, 256, agg_small_smem<Op, 32, true, 1>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc);
+              else
+                AGG_K(32, true)<<<grid, 256, agg_small_smem<Op, 32, true>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc);
+              break;
           }
         } else {
           switch (G) {
             case 4: AGG_K(4, false)<<<grid, 256, agg_small_smem<Op, 4, false>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
             case 8: AGG_K(8, false)<<<grid, 256, agg_small_smem<Op, 8, false>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
             case 16: AGG_K(16, false)<<<grid, 256, agg_small_smem<Op, 16, false>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
-            default: AGG_K(32, false)<<<grid, 256, agg_small_smem<Op, 32, false>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc); break;
+            default:
+              if (g.max_deg <= 32)
+                k_agg_small<Op, 32, false, 1><<<grid, 256, agg_small_smem<Op, 32, false, 1>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc);
+              else
+                AGG_K(32, false)<<<grid, 256, agg_small_smem<Op, 32, false>(), c.stream>>>(a, gv, parts, list, cnt, wide, dc);
+              break;
           }
         }
 #undef AGG_K

@@ -188,9 +188,119 @@ __host__ __device__ constexpr int tier_e() {
   return G == 32 ? 2 : 1;
 }
 // Per-warp staging words of the short-row sweep (adjacency, parts, weights).
+// (the one-entry-per-lane 32-wide tier pads its rows to 33 words so a lane
+// can walk its own row without shared-memory bank conflicts)
 template <int G, int RB, bool UNIT, int E = tier_e<G>()>
 __host__ __device__ constexpr int stage_words() {
-  return RB * G * E * (UNIT ? 2 : 3);
+  return RB * (G == 32 && E == 1 ? 33 : G * E) * (UNIT ? 2 : 3);
+}
+
+// Tier 3 with rows of <= 32 entries (one entry per lane). Rows are staged as
+// in agg_small, but the aggregation is lane-per-row first: each lane walks
+// its own staged row (interior test + own-part sum), and only the boundary
+// rows -- a minority on refined meshes -- run the warp-cooperative part
+// grouping. The former lane-per-entry loop spent ~90 instructions per row,
+// most of them per-row broadcasts and reductions that interior rows do not
+// need (ncu: the sweep was issue-bound at 60 % issue-active).
+template <class Op, bool UNIT, int RB>
+static __device__ __forceinline__ void agg_rows32(const typename Op::Args& a, const GView& g,
+                                                  const int32_t* __restrict__ parts,
+                                                  const int32_t* __restrict__ list, int64_t cnt,
+                                                  bool wide,
+                                                  const unsigned long long* __restrict__ dcnt,
+                                                  int64_t w0, int64_t nw, long long& acc,
+                                                  uint32_t* stage) {
+  if (dcnt) cnt = (int64_t)*(const volatile unsigned long long*)dcnt;
+  constexpr int SP = 33;
+  const int lane = threadIdx.x & 31;
+  int* s_adj = reinterpret_cast<int*>(stage);
+  int* s_p = s_adj + RB * SP;
+  int* s_w = s_p + RB * SP;
+  const int64_t per_w = (cnt + nw - 1) / nw;
+  const int R = per_w >= RB ? RB : (per_w < 1 ? 1 : (int)per_w);
+  for (int64_t base = w0 * R; base < cnt; base += nw * R) {
+    const int64_t idx = base + lane;
+    int v = 0, own = -1, deg = 0;
+    int64_t beg = 0;
+    if (lane < R && idx < cnt) {
+      v = list ? list[idx] : (int)idx;
+      own = parts[v];
+      if (Op::skip(a, v, own)) {
+        own = -1;
+      } else {
+        beg = g.offs[v];
+        deg = (int)(g.offs[v + 1] - beg);
+      }
+    }
+    for (int r = 0; r < R; ++r) {
+      const int64_t rb = __shfl_sync(0xffffffffu, beg, r);
+      const int rd = __shfl_sync(0xffffffffu, deg, r);
+      if (lane < rd) {
+        cp_async4(&s_adj[r * SP + lane], g.adj + rb + lane);
+        if (!UNIT) cp_async4(&s_w[r * SP + lane], g.ew + rb + lane);
+      }
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    for (int r = 0; r < R; ++r) {
+      const int rd = __shfl_sync(0xffffffffu, deg, r);
+      if (lane < rd) cp_async4(&s_p[r * SP + lane], parts + s_adj[r * SP + lane]);
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    // lane r: its own row
+    long long my_self = 0, my_ex = 0;
+    unsigned long long my_key = 0;
+    bool outside = false;
+    if (own >= 0) {
+      const int* pr = s_p + lane * SP;
+      const int* wr = s_w + lane * SP;
+      for (int j = 0; j < deg; ++j) {
+        const int p = pr[j];
+        if (p == own) my_self += UNIT ? 1 : wr[j];
+        else outside = true;
+      }
+      my_ex = Op::extra(a, own, 1) ? my_self : 0;  // extra is linear in w
+    }
+    // boundary rows: group the parts of the row across the warp
+    unsigned bm = __ballot_sync(0xffffffffu, outside);
+    while (bm) {
+      const int r = __ffs(bm) - 1;
+      bm &= bm - 1;
+      const int rd = __shfl_sync(0xffffffffu, deg, r);
+      const int rown = __shfl_sync(0xffffffffu, own, r);
+      int p = -1, w = 0;
+      if (lane < rd) {
+        p = s_p[r * SP + lane];
+        w = UNIT ? 1 : s_w[r * SP + lane];
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, p);
+      const bool comp = p >= 0 && p != rown && Op::competes(a, p, rown);
+      unsigned long long key;
+      long long ex;
+      if (!wide) {
+        const unsigned sm = UNIT ? (unsigned)__popc(peers) : __reduce_add_sync(peers, (unsigned)w);
+        const unsigned mx = __reduce_max_sync(0xffffffffu, comp ? sm : 0u);
+        const unsigned pm =
+            __reduce_min_sync(0xffffffffu, (comp && sm == mx) ? (unsigned)p : 0xffffffffu);
+        ex = (long long)__reduce_add_sync(0xffffffffu,
+                                          p >= 0 ? (unsigned)Op::extra(a, p, w) : 0u);
+        key = mx ? pack_best((long long)mx, (int)pm) : 0ull;
+      } else {
+        const long long sm = UNIT ? (long long)__popc(peers) : peer_sum(peers, w, wide);
+        const bool lead = p >= 0 && (__ffs(peers) - 1) == lane;
+        key = (lead && comp) ? pack_best(sm, p) : 0ull;
+        key = gmax<32>(key, 0xffffffffu);
+        ex = gsum<32>(p >= 0 ? (long long)Op::extra(a, p, w) : 0ll, 0xffffffffu);
+      }
+      if (lane == r) {
+        my_key = key;
+        my_ex = ex;
+      }
+    }
+    __syncwarp();  // the next batch reuses the stage
+    if (own >= 0) Op::finish(a, v, own, my_self, my_key, my_ex, acc);
+  }
 }
 
 // Tiers 0-3 (rows of <= G*E entries). A warp owns R <= RB consecutive list
@@ -213,6 +323,10 @@ static __device__ __forceinline__ void agg_small(const typename Op::Args& a, con
                                                  const unsigned long long* __restrict__ dcnt,
                                                  int64_t w0, int64_t nw, long long& acc,
                                                  uint32_t* stage) {
+  if constexpr (G == 32 && E == 1) {
+    agg_rows32<Op, UNIT, RB>(a, g, parts, list, cnt, wide, dcnt, w0, nw, acc, stage);
+    return;
+  }
   if (dcnt) cnt = (int64_t)*(const volatile unsigned long long*)dcnt;
   static_assert(E == 1 || G == 32, "two entries per lane only for one row per step");
   constexpr int S = G * E;     // slots per row
