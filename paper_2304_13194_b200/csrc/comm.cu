@@ -4,8 +4,28 @@
 #include <algorithm>
 #include <numeric>
 #include <string>
+#include <chrono>
 
 namespace jet {
+
+__global__ void k_sum_slices(const unsigned long long* __restrict__ in, int64_t count, int size,
+                             unsigned long long* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long s = 0;
+    for (int r = 0; r < size; ++r) s += in[(size_t)r * count + i];
+    out[i] = s;
+  }
+}
+
+void Comm::allreduce_sum(Ctx& c, unsigned long long* d, int64_t count) {
+  if (count <= 0) return;
+  std::vector<int64_t> counts;
+  allgatherv(c, d, count * (int64_t)sizeof(unsigned long long), red_buf, counts);
+  k_sum_slices<<<grid_for(c, count, 256), 256, 0, c.stream>>>(
+      reinterpret_cast<const unsigned long long*>(red_buf.get()), count, size, d);
+  CK(cudaGetLastError());
+}
 
 void LocalGroup::barrier() {
   std::unique_lock<std::mutex> lk(m);
@@ -15,7 +35,9 @@ void LocalGroup::barrier() {
     ++generation;
     cv.notify_all();
   } else {
-    cv.wait(lk, [&] { return generation != gen; });
+    // a rank that failed never arrives: give up instead of hanging the others
+    if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return generation != gen; }))
+      throw Error(JET_EINTERNAL, "local group: a rank did not reach the exchange (120 s)");
   }
 }
 

@@ -85,7 +85,8 @@ void refine_level(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, int64_t
       Pcg64 rng = level >= 0 ? default_rng({cfg.seed, (uint64_t)level, (uint64_t)pass_index})
                              : default_rng({cfg.seed, (uint64_t)pass_index});
       const bool strong = rebal_streak >= 2;
-      if (!rebalance_pass(c, w, g, parts, k, limit, sigma, cfg.sub_buckets, strong, rng, nullptr)) {
+      if (!rebalance_pass(c, w, g, parts, k, limit, sigma, cfg.sub_buckets, strong, rng, nullptr,
+                          sharded ? &sh : nullptr)) {
         st.rebalance_stuck = 1;
         break;
       }

@@ -450,6 +450,73 @@ __global__ void k_unpack_moves(const int2* __restrict__ in, int64_t total, int64
   }
 }
 
+// candidates of this rank's block [lo, hi) (warp-uniform trip counts)
+__global__ void k_rb_collect_range(const int32_t* __restrict__ parts,
+                                   const int32_t* __restrict__ opidx,
+                                   const int64_t* __restrict__ offs, TierMap tm, int64_t lo,
+                                   int64_t hi, int32_t* lists, RbSegsDev seg,
+                                   unsigned long long* cnts) {
+  const int64_t span = (hi - lo + 31) / 32 * 32;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < span;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = lo + i;
+    int t = -1;
+    if (v < hi && opidx[parts[v]] >= 0) t = tm(offs[v + 1] - offs[v]);
+    if (__ballot_sync(0xffffffffu, t >= 0) == 0) continue;
+    for (int tt = 0; tt < NBINS; ++tt) warp_append(t == tt, (int32_t)v, lists + seg.b[tt], cnts + tt);
+  }
+}
+
+__global__ void k_rb_find_a(RbSel s, const long long* __restrict__ deficit,
+                            const long long* __restrict__ cum_before,
+                            const int32_t* __restrict__ opart, int64_t n, int nb, int nover,
+                            int64_t lo, int64_t hi, int32_t* ch, long long* cb,
+                            unsigned long long* ew) {
+  const int op = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (op < nover) rb_find_a(op, s, deficit, cum_before, opart, n, nb, lo, hi, ch, cb, ew);
+}
+
+__global__ void k_rb_find_b(RbSel s, const long long* __restrict__ deficit,
+                            const long long* __restrict__ required, int nb, int nover,
+                            const int32_t* __restrict__ ch, const long long* __restrict__ cb,
+                            const unsigned long long* __restrict__ ew, int32_t* thr) {
+  const int op = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (op < nover) rb_find_b(op, s, deficit, required, nb, ch, cb, ew, thr);
+}
+
+// The pending moves of every rank (this rank's move lists, packed as
+// (id, destination)) gathered and appended to every rank's move lists.
+void share_moves(Ctx& c, Workspace& w, const DGraph& g, ShardLists& sh) {
+  Comm& cm = *c.comm;
+  unsigned long long hc[2 * NBINS];
+  std::vector<int64_t> counts;
+  int64_t total = 0, mine_lo = 0;
+  d2h(c, hc, w.ctr.get(), 2 * NBINS);
+  c.sync();
+  int64_t nm = 0;
+  for (int t = 0; t < NBINS; ++t) nm += (int64_t)hc[CTR_MOVE + t];
+  sh.send.ensure((size_t)std::max<int64_t>(1, nm) * sizeof(int2), c.stream);
+  const SegLists ml = seg_lists(w, true);
+  launch(c, "shard_pack", 8.0 * nm, [&] {
+    k_pack_moves<<<grid_for(c, nm, 256), 256, 0, c.stream>>>(ml, w.mv.get(), (int2*)sh.send.get());
+  });
+  cm.allgatherv(c, sh.send.get(), nm * (int64_t)sizeof(int2), sh.recv, counts);
+  total = 0;
+  for (int r = 0; r < cm.size; ++r) {
+    if (r == cm.rank) mine_lo = total;
+    total += counts[r];
+  }
+  total /= (int64_t)sizeof(int2);
+  mine_lo /= (int64_t)sizeof(int2);
+  RbSegsDev ms;
+  for (int t = 0; t < NBINS; ++t) ms.b[t] = w.seg_base[t];
+  launch(c, "shard_unpack", 8.0 * total, [&] {
+    k_unpack_moves<<<grid_for(c, total, 256), 256, 0, c.stream>>>(
+        (const int2*)sh.recv.get(), total, mine_lo, mine_lo + nm, w.mv.get(), g.offs.get(), g.tm,
+        w.lists.get() + w.cap_n, ms, w.ctr.get() + CTR_MOVE);
+  });
+}
+
 void lp_pass_sharded(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts, int k,
                      const LpParams& p, ShardLists& sh) {
   JET_REQUIRE(c.comm && p.afterburner, JET_EUNSUPPORTED,
@@ -506,31 +573,7 @@ void lp_pass_sharded(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts
   ab.mv = w.mv.get();
   ab.move_list = w.lists.get();
   launch_rows_reduce_ab(c, w, g, ab);
-  // moves of every rank, appended to the local move lists
-  d2h(c, hc, w.ctr.get(), 2 * NBINS);
-  c.sync();
-  int64_t nm = 0;
-  for (int t = 0; t < NBINS; ++t) nm += (int64_t)hc[CTR_MOVE + t];
-  sh.send.ensure((size_t)std::max<int64_t>(1, nm) * sizeof(int2), c.stream);
-  const SegLists ml = seg_lists(w, true);
-  launch(c, "shard_pack", 8.0 * nm, [&] {
-    k_pack_moves<<<grid_for(c, nm, 256), 256, 0, c.stream>>>(ml, w.mv.get(), (int2*)sh.send.get());
-  });
-  cm.allgatherv(c, sh.send.get(), nm * (int64_t)sizeof(int2), sh.recv, counts);
-  total = 0;
-  for (int r = 0; r < cm.size; ++r) {
-    if (r == cm.rank) mine_lo = total;
-    total += counts[r];
-  }
-  total /= (int64_t)sizeof(int2);
-  mine_lo /= (int64_t)sizeof(int2);
-  RbSegsDev ms;
-  for (int t = 0; t < NBINS; ++t) ms.b[t] = w.seg_base[t];
-  launch(c, "shard_unpack", 8.0 * total, [&] {
-    k_unpack_moves<<<grid_for(c, total, 256), 256, 0, c.stream>>>(
-        (const int2*)sh.recv.get(), total, mine_lo, mine_lo + nm, w.mv.get(), g.offs.get(), g.tm,
-        w.lists.get() + w.cap_n, ms, w.ctr.get() + CTR_MOVE);
-  });
+  share_moves(c, w, g, sh);
 }
 
 void afterburner_only(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
@@ -851,6 +894,19 @@ __global__ void k_rb_commit(RbCommit a, int64_t L) {
   }
 }
 
+// global evicted ids from the gathered keys; in direct mode every evicted
+// vertex lacks a valid connection, so its rbest is -1 (remote vertices' rbest
+// entries are stale on this rank and are reset here)
+__global__ void k_keys_to_ids(const unsigned long long* __restrict__ keys, int64_t L,
+                              int32_t* ids, int32_t* rbest) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = (int)(keys[i] & 0xffffffffu);
+    ids[i] = v;
+    rbest[v] = -1;
+  }
+}
+
 static int ceil_log2(int64_t x) {
   int r = 0;
   while ((1LL << r) < x) ++r;
@@ -878,7 +934,8 @@ struct Packer {
 
 bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
                     int k, int64_t limit, int64_t sigma, int sub_buckets,
-                    bool strong, Pcg64& rng, RebalanceOut* out) {
+                    bool strong, Pcg64& rng, RebalanceOut* out, ShardLists* sh) {
+  JET_REQUIRE(!sh || (c.comm && out == nullptr), JET_EINTERNAL, "sharded rebalance misuse");
   const std::vector<int64_t>& pw = w.h_pw;
   std::vector<int32_t> h_opidx(k, -1), h_valid_list, h_opart;
   std::vector<uint8_t> h_valid(k, 0);
@@ -921,7 +978,7 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
   const int nb = ns * rho;
   const int nch = (int)(((g.n + rho - 1) / rho + 31) / 32);
   // per part at most deficit/min_w + 1 vertices leave (selected prefix < deficit)
-  const bool fast = out == nullptr && max_evict <= TAIL_CAP;
+  const bool fast = out == nullptr && max_evict <= TAIL_CAP && sh == nullptr;
   const bool direct = out == nullptr;
 
   std::vector<uint8_t>& up = w.h_up;
@@ -961,11 +1018,19 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
     cseg.b[t] = w.seg_base[t];
     mseg.b[t] = w.seg_base[t];
   }
-  launch(c, "rb_collect", 8.0 * g.n, [&] {
-    k_rb_collect<<<grid_for(c, g.n, 256), 256, 0, c.stream>>>(parts, d_opidx, g.offs.get(), g.tm, g.n,
-                                                             w.lists.get(), cseg,
-                                                             w.ctr.get() + CTR_CAND);
-  });
+  if (sh) {  // candidates of this rank's block only
+    launch(c, "rb_collect", 8.0 * (sh->hi - sh->lo), [&] {
+      k_rb_collect_range<<<grid_for(c, sh->hi - sh->lo, 256), 256, 0, c.stream>>>(
+          parts, d_opidx, g.offs.get(), g.tm, sh->lo, sh->hi, w.lists.get(), cseg,
+          w.ctr.get() + CTR_CAND);
+    });
+  } else {
+    launch(c, "rb_collect", 8.0 * g.n, [&] {
+      k_rb_collect<<<grid_for(c, g.n, 256), 256, 0, c.stream>>>(parts, d_opidx, g.offs.get(), g.tm,
+                                                               g.n, w.lists.get(), cseg,
+                                                               w.ctr.get() + CTR_CAND);
+    });
+  }
   RbOp::Args ra{};
   ra.parts = parts;
   ra.vw = g.vw.get();
@@ -988,6 +1053,10 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
   for (int t = 0; t < NBINS; ++t) clists[t] = w.cand_list(t);
   run_agg<RbOp>(c, g, [&](int) { return ra; }, parts, k, "rb_stats", 16.0, clists,
                 w.ctr.get() + CTR_CAND);
+  if (sh) {  // global bucket histograms
+    c.comm->allreduce_sum(c, w.H.get(), (int64_t)nover * nb);
+    c.comm->allreduce_sum(c, w.Hs.get(), (int64_t)nover * ns);
+  }
 
   int32_t* bstar = w.bstar.get();
   RbSel s{parts, g.vw.get(), d_opidx, w.rkey.get(), bstar, w.thr.get(), rho, nch, w.CH.get()};
@@ -1073,10 +1142,29 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
   launch(c, "rb_chunk", 0.0, [&] {
     k_rb_chunk<<<grid_for(c, g.n, 256), 256, 0, c.stream>>>(s, w.rcand.get(), rc);
   });
-  launch(c, "rb_find", 8.0 * nover * nch, [&] {
-    k_rb_find<<<(nover + 7) / 8, 256, 0, c.stream>>>(s, d_def, d_req, w.cum_before.get(), d_opart,
-                                                     g.n, nb, nover, w.thr.get());
-  });
+  if (sh) {
+    // crossing chunk from the global chunk histogram; the chunk's element
+    // weights are contributed by their owners and summed
+    c.comm->allreduce_sum(c, w.CH.get(), (int64_t)nover * nch);
+    DBuf<int32_t> fch(nover, c.stream);
+    DBuf<long long> fcb(nover, c.stream);
+    DBuf<unsigned long long> few((size_t)nover * 32, c.stream);
+    launch(c, "rb_find", 8.0 * nover * nch, [&] {
+      k_rb_find_a<<<(nover + 7) / 8, 256, 0, c.stream>>>(s, d_def, w.cum_before.get(), d_opart,
+                                                         g.n, nb, nover, sh->lo, sh->hi,
+                                                         fch.get(), fcb.get(), few.get());
+    });
+    c.comm->allreduce_sum(c, few.get(), (int64_t)nover * 32);
+    launch(c, "rb_find", 8.0 * nover * 32, [&] {
+      k_rb_find_b<<<(nover + 7) / 8, 256, 0, c.stream>>>(s, d_def, d_req, nb, nover, fch.get(),
+                                                         fcb.get(), few.get(), w.thr.get());
+    });
+  } else {
+    launch(c, "rb_find", 8.0 * nover * nch, [&] {
+      k_rb_find<<<(nover + 7) / 8, 256, 0, c.stream>>>(s, d_def, d_req, w.cum_before.get(),
+                                                       d_opart, g.n, nb, nover, w.thr.get());
+    });
+  }
   launch(c, "rb_select", 0.0, [&] {
     k_rb_select<<<grid_for(c, g.n, 256), 256, 0, c.stream>>>(
         s, w.rcand.get(), rc, w.rbest.get(), strong, direct ? 1 : 0, w.evict.get(),
@@ -1089,6 +1177,31 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
   int64_t L = 0;
   d2h(c, &L, reinterpret_cast<int64_t*>(w.ctr.get() + CTR_EVICT), 1);
   c.sync();
+  if (sh) {
+    // direct moves (evicted vertices with a valid connection) of every rank
+    share_moves(c, w, g, *sh);
+    // the evicted sets of every rank, as sort keys
+    w.keys.ensure((size_t)g.n + 1, c.stream);
+    w.keys_alt.ensure((size_t)g.n + 1, c.stream);
+    if (L)
+      launch(c, "rb_keys", 16.0 * L, [&] {
+        k_rb_keys<<<grid_for(c, L, 256), 256, 0, c.stream>>>(w.evict.get(), L, parts, d_opidx,
+                                                             w.rkey.get(), nb, w.keys.get());
+      });
+    std::vector<int64_t> counts;
+    c.comm->allgatherv(c, w.keys.get(), L * 8, sh->recv, counts);
+    int64_t tot = 0;
+    for (int64_t b : counts) tot += b;
+    L = tot / 8;
+    if (L)
+      CK(cudaMemcpyAsync(w.keys.get(), sh->recv.get(), (size_t)L * 8, cudaMemcpyDeviceToDevice,
+                         c.stream));
+    if (L == 0) return true;
+    launch(c, "rb_evict_ids", 8.0 * L, [&] {
+      k_keys_to_ids<<<grid_for(c, L, 256), 256, 0, c.stream>>>(w.keys.get(), L, w.evict.get(),
+                                                               w.rbest.get());
+    });
+  }
   if (L == 0) {
     if (out) {
       out->v->clear();
@@ -1097,10 +1210,11 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
     }
     return true;
   }
-  launch(c, "rb_keys", 16.0 * L, [&] {
-    k_rb_keys<<<grid_for(c, L, 256), 256, 0, c.stream>>>(w.evict.get(), L, parts, d_opidx,
-                                                         w.rkey.get(), nb, w.keys.get());
-  });
+  if (!sh)
+    launch(c, "rb_keys", 16.0 * L, [&] {
+      k_rb_keys<<<grid_for(c, L, 256), 256, 0, c.stream>>>(w.evict.get(), L, parts, d_opidx,
+                                                           w.rkey.get(), nb, w.keys.get());
+    });
   const int gbits = ceil_log2((int64_t)nover * nb + 1);
   {
     size_t tmp = 0;

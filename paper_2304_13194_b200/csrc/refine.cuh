@@ -94,6 +94,7 @@ void build_shard_lists(Ctx& c, const DGraph& g, int rank, int size, ShardLists& 
 // apply and the rebalancing passes run replicated on identical state).
 void lp_pass_sharded(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts, int k,
                      const LpParams& p, ShardLists& sh);
+void share_moves(Ctx& c, Workspace& w, const DGraph& g, ShardLists& sh);
 
 // Rebalancing pass (rebalance.py:139-240). Host-side scalars come from the
 // part weights in w.h_pw. Returns false when no valid destination exists
@@ -105,9 +106,12 @@ struct RebalanceOut {
   std::vector<double>* gain = nullptr;
   bool exact_rng = false;  // draw exactly #missing values (API mode)
 };
+// sh != nullptr: sharded (candidates of this rank's block; histograms and
+// crossing-chunk element weights all-reduced, direct moves and evicted sets
+// all-gathered; the ordered tail runs replicated on the global evicted set).
 bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
                     int k, int64_t limit, int64_t sigma, int sub_buckets,
-                    bool strong, Pcg64& rng, RebalanceOut* out);
+                    bool strong, Pcg64& rng, RebalanceOut* out, ShardLists* sh = nullptr);
 
 // Apply the pending moves (conn.py:215-254): parts, part weights, exact cut
 // delta, locks. Reads back the part weights into w.h_pw.

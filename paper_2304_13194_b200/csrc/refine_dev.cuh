@@ -1238,6 +1238,64 @@ static __device__ void rb_find_warp(int op, const RbSel& s, const long long* __r
   if (!m && lane == 0) thr[op] = 0x7fffffff;  // unreachable by construction
 }
 
+// Sharded form of rb_find_warp: (a) every rank locates the crossing chunk
+// from the all-reduced chunk histogram and contributes the weights of the
+// chunk's elements it owns; (b) after the element weights are all-reduced,
+// every rank finds the crossing element (same rule as rb_find_warp).
+static __device__ void rb_find_a(int op, const RbSel& s, const long long* __restrict__ deficit,
+                                 const long long* __restrict__ cum_before,
+                                 const int32_t* __restrict__ opart, int64_t n, int nb,
+                                 int64_t lo, int64_t hi, int32_t* ch_out, long long* cb_out,
+                                 unsigned long long* ew) {
+  const int lane = threadIdx.x & 31;
+  const int bs = s.bstar[op];
+  long long w = 0, cb = 0;
+  int ch = -1;
+  if (bs < nb) {
+    ch = warp_cross(s.CH + (size_t)op * s.nch, s.nch, deficit[op], cum_before[op], &cb);
+    const int64_t v64 = ((int64_t)ch * 32 + lane) * s.rho + bs % s.rho;
+    if (ch >= 0 && v64 < n && v64 >= lo && v64 < hi) {
+      const int v = (int)v64;
+      if (s.parts[v] == opart[op] && s.rkey[v] == bs) w = s.vw[v];
+    }
+  }
+  ew[(size_t)op * 32 + lane] = (unsigned long long)w;
+  if (lane == 0) {
+    ch_out[op] = ch;
+    cb_out[op] = cb;
+  }
+}
+
+static __device__ void rb_find_b(int op, const RbSel& s, const long long* __restrict__ deficit,
+                                 const long long* __restrict__ required, int nb,
+                                 const int32_t* __restrict__ ch_in,
+                                 const long long* __restrict__ cb_in,
+                                 const unsigned long long* __restrict__ ew, int32_t* thr) {
+  const int lane = threadIdx.x & 31;
+  const int bs = s.bstar[op];
+  if (bs >= nb) {
+    if (lane == 0) thr[op] = 0x7fffffff;
+    return;
+  }
+  const long long D = deficit[op], w = (long long)ew[(size_t)op * 32 + lane];
+  const int ch = ch_in[op];
+  const int64_t v64 = ((int64_t)ch * 32 + lane) * s.rho + bs % s.rho;
+  long long incl = w;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const long long cum = cb_in[op] + incl;
+  const unsigned m = __ballot_sync(0xffffffffu, w > 0 && cum >= D && cum - w < D);
+  if (m && lane == __ffs(m) - 1) {
+    const long long prev = cum - w;
+    const bool include = (cum - D <= D - prev) || (prev < required[op]);
+    thr[op] = (int)v64 + (include ? 1 : 0);
+  }
+  if (!m && lane == 0) thr[op] = 0x7fffffff;
+}
+
 static __device__ void rb_select(const RbSel& s, const int32_t* __restrict__ rcand,
                           const unsigned long long* __restrict__ cnt_ptr,
                           const int32_t* __restrict__ rbest, int strong, int direct,

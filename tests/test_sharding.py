@@ -33,14 +33,17 @@ def _run_sharded(g, cfg, size, shard_min):
         except Exception as e:  # pragma: no cover - reported below
             errs.append(e)
 
-    th = [threading.Thread(target=work, args=(r,)) for r in range(size)]
+    th = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(size)]
     for t in th:
         t.start()
     for t in th:
         t.join(timeout=600)
     assert not errs, errs
+    assert not any(t.is_alive() for t in th), "a rank did not finish"
     rep = ctxs[0].profile_report()
     assert rep.get("shard_pack", {}).get("launches", 0) > 0, "sharded path not taken"
+    assert rep.get("rb_evict_ids", {}).get("launches", 0) + rep.get("rb_collect", {}).get(
+        "launches", 0) > 0, "no sharded rebalancing pass"
     for c in ctxs:
         c.detach()
     return out
