@@ -36,6 +36,13 @@ __device__ __forceinline__ unsigned long long vload(const unsigned long long* p)
   return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
+// grid barrier; a one-block grid needs only __syncthreads (which also
+// orders global memory within the block) -- the grid protocol costs ~1.5 us
+__device__ __forceinline__ void grid_or_block_sync(cg::grid_group& grid) {
+  if (gridDim.x == 1) __syncthreads();
+  else grid.sync();
+}
+
 static int coop_blocks(Ctx& c, const void* kern, int block) {
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, 0));
@@ -345,15 +352,15 @@ __global__ void __launch_bounds__(1024)
   while (true) {
     if (t.stats && blockIdx.x == 0 && threadIdx.x == 0) t.stats[0] += 1;
     th_retire(t, active, w0, ws);
-    grid.sync();
+    grid_or_block_sync(grid);
     if (vload(active) == 0) return;
     th_minc(t, g, left, nl, w0, ws);
-    grid.sync();
+    grid_or_block_sync(grid);
     th_ready(t, w0, ws);
-    grid.sync();
+    grid_or_block_sync(grid);
     if (w0 == 0 && (threadIdx.x & 31) == 0) *active = 0;
     th_pair(t, w0, ws);
-    grid.sync();
+    grid_or_block_sync(grid);
   }
 }
 
@@ -402,7 +409,7 @@ __global__ void __launch_bounds__(1024)
     t.good[ci] = 0;
     t.cidx[t.centres[ci]] = (int32_t)ci;
   }
-  grid.sync();
+  grid_or_block_sync(grid);
   // every neighbour of a leftover is a centre, all active: minc = first entry
   for (int64_t i = t0; i < nl; i += nt) {
     const int v = left[i];
@@ -414,7 +421,7 @@ __global__ void __launch_bounds__(1024)
       t.lcur[v] = -1;
     }
   }
-  grid.sync();
+  grid_or_block_sync(grid);
   int cur = 0;
   for (int round = 1;; ++round) {
     const bool all = round == 1;
@@ -479,7 +486,7 @@ __global__ void __launch_bounds__(1024)
       t.cnt[2 + (par ^ 1)] = 0;  // read by the previous round's phase 2, done
       t.cnt[4 + (par ^ 1)] = 0;
     }
-    grid.sync();
+    grid_or_block_sync(grid);
     // (2a) newly matched members leave every active centre's counts
     const int64_t M = (int64_t)vload(t.cnt + 4 + par);
     for (int64_t k = w0; k < M; k += nw) {
@@ -521,7 +528,7 @@ __global__ void __launch_bounds__(1024)
     }
     if (t0 == 0) t.cnt[6] += 1;
     cur ^= 1;
-    grid.sync();
+    grid_or_block_sync(grid);
   }
 }
 
@@ -870,9 +877,9 @@ __global__ void __launch_bounds__(1024) k_resolve(Resolve R) {
     if (live == 0) return;
     if (live <= R.small) break;
     resolve_a(R, in, out, t0, nt);
-    grid.sync();
+    grid_or_block_sync(grid);
     resolve_b(R, in, out, t0, nt);
-    grid.sync();
+    grid_or_block_sync(grid);
     ++r;
   }
   if (blockIdx.x != 0) return;
@@ -996,7 +1003,7 @@ __global__ void __launch_bounds__(1024) k_resolve_frontier(Frontier F) {
     }
     warp_append(rd, v, F.fr, F.fcnt);
   }
-  grid.sync();
+  grid_or_block_sync(grid);
   int cur = 0;
   for (int round = 1;; ++round) {
     const int64_t L = (int64_t)vload(F.fcnt + cur);
@@ -1013,7 +1020,7 @@ __global__ void __launch_bounds__(1024) k_resolve_frontier(Frontier F) {
       F.fcnt[cur ^ 1] = 0;
       F.fcnt[2] = 0;
     }
-    grid.sync();
+    grid_or_block_sync(grid);
     // (2) unmatched vertices sharing an edge with a newly matched one (their
     // head edge may have died), deduplicated; long incidence lists (hubs)
     // are walked by a warp
@@ -1055,7 +1062,7 @@ __global__ void __launch_bounds__(1024) k_resolve_frontier(Frontier F) {
       }
       __syncthreads();
     }
-    grid.sync();
+    grid_or_block_sync(grid);
     // (3) refresh each affected head; queue it if it is also the lowest live
     // edge at its other endpoint
     const int64_t A = (int64_t)vload(F.fcnt + 2);
@@ -1092,7 +1099,7 @@ __global__ void __launch_bounds__(1024) k_resolve_frontier(Frontier F) {
       }
       __syncthreads();
     }
-    grid.sync();
+    grid_or_block_sync(grid);
     if (t0 == 0) F.fcnt[3] += 1;
     cur ^= 1;
   }
