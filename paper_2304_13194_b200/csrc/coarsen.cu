@@ -927,7 +927,7 @@ struct Frontier {
   int32_t* aflag;                 // n: round a vertex was refreshed in
   int32_t* fr;                    // 2 x cap
   int32_t* aff;                   // affected vertices of the round, <= n
-  unsigned long long* fcnt;       // [0,1] frontier sizes, [2] affected, [3] rounds
+  unsigned long long* fcnt;       // [0,1] frontier sizes, [2,3] affected (round parity), [4] rounds
   const int32_t* props;           // proposers
   int64_t ne, cap;
 };
@@ -1010,20 +1010,18 @@ __global__ void __launch_bounds__(1024) k_resolve_frontier(Frontier F) {
     if (L == 0) break;
     const int32_t* fin = F.fr + (size_t)cur * F.cap;
     int32_t* fout = F.fr + (size_t)(cur ^ 1) * F.cap;
-    // (1) accept the frontier
+    // (1) accept the frontier, and in the same phase (2) collect the
+    // unmatched vertices sharing an edge with a newly matched one (their head
+    // edge may have died), deduplicated; long incidence lists (hubs) are
+    // walked by a warp. A vertex matched in this round may be collected
+    // before its partner store is visible; step (3) drops it.
     for (int64_t i = t0; i < L; i += nt) {
       const int v = fin[i], u = F.prop[v];
       F.partner[v] = u;
       F.partner[u] = v;
     }
-    if (t0 == 0) {
-      F.fcnt[cur ^ 1] = 0;
-      F.fcnt[2] = 0;
-    }
-    grid_or_block_sync(grid);
-    // (2) unmatched vertices sharing an edge with a newly matched one (their
-    // head edge may have died), deduplicated; long incidence lists (hubs)
-    // are walked by a warp
+    const int par = round & 1;
+    if (t0 == 0) F.fcnt[cur ^ 1] = 0;
     auto touch = [&](int y) {
       if (F.partner[y] >= 0 || atomicExch(&F.aflag[y], round) == round) return false;
       return true;
@@ -1042,7 +1040,7 @@ __global__ void __launch_bounds__(1024) k_resolve_frontier(Frontier F) {
         } else {
           for (int q = beg; q < end; ++q) {
             const int y = fr_other(F, (int)(F.inc[q] & 0xffffffffu), x);
-            if (touch(y)) F.aff[atomicAdd(F.fcnt + 2, 1ull)] = y;
+            if (touch(y)) F.aff[atomicAdd(F.fcnt + 2 + par, 1ull)] = y;
           }
         }
       }
@@ -1057,7 +1055,7 @@ __global__ void __launch_bounds__(1024) k_resolve_frontier(Frontier F) {
             y = fr_other(F, (int)(F.inc[q] & 0xffffffffu), x);
             if (!touch(y)) y = -1;
           }
-          warp_append(y >= 0, y, F.aff, F.fcnt + 2);
+          warp_append(y >= 0, y, F.aff, F.fcnt + 2 + par);
         }
       }
       __syncthreads();
@@ -1065,12 +1063,15 @@ __global__ void __launch_bounds__(1024) k_resolve_frontier(Frontier F) {
     grid_or_block_sync(grid);
     // (3) refresh each affected head; queue it if it is also the lowest live
     // edge at its other endpoint
-    const int64_t A = (int64_t)vload(F.fcnt + 2);
+    const int64_t A = (int64_t)vload(F.fcnt + 2 + par);
+    if (t0 == 0) F.fcnt[2 + (par ^ 1)] = 0;  // next round's (last read a round ago)
     for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < A; b0 += nt) {
       if (threadIdx.x == 0) s_ndef = 0;
       __syncthreads();
       const int64_t i = b0 + threadIdx.x;
-      if (i < A) {
+      if (i < A && F.partner[F.aff[i]] >= 0) {  // matched this round
+        F.head[F.aff[i]] = F.ioff[F.aff[i] + 1];
+      } else if (i < A) {
         const int y = F.aff[i];
         int pos, pz;
         const int h = fr_first_live_t(F, y, FR_SHORT, &pos);
@@ -1090,7 +1091,7 @@ __global__ void __launch_bounds__(1024) k_resolve_frontier(Frontier F) {
       for (int d = wib; d < s_ndef; d += nwb) {
         const int y = s_def[d];
         int pos, pz;
-        const int h = fr_first_live(F, y, &pos);
+        const int h = fr_first_live(F, y, &pos);  // (y unmatched: checked above)
         if (lane == 0) F.head[y] = pos;
         if (h < 0) continue;
         const int hz = fr_first_live(F, fr_other(F, h, y), &pz);
@@ -1100,7 +1101,7 @@ __global__ void __launch_bounds__(1024) k_resolve_frontier(Frontier F) {
       __syncthreads();
     }
     grid_or_block_sync(grid);
-    if (t0 == 0) F.fcnt[3] += 1;
+    if (t0 == 0) F.fcnt[4] += 1;
     cur ^= 1;
   }
 }
@@ -1141,10 +1142,10 @@ static void resolve_frontier(Ctx& c, int64_t n, const int32_t* prop, int32_t* pa
   unsigned long long* keys = c.scratch<unsigned long long>(21, 2 * M);
   int32_t* ints = c.scratch<int32_t>(22, 5 * n + 1);
   int32_t* fr = c.scratch<int32_t>(23, 2 * ne);
-  unsigned long long* fcnt = c.scratch<unsigned long long>(24, 4);
+  unsigned long long* fcnt = c.scratch<unsigned long long>(24, 8);
   int32_t *ioff = ints, *head = ints + n + 1, *qflag = ints + 2 * n + 1, *aflag = ints + 3 * n + 1,
           *aff = ints + 4 * n + 1;
-  dzero(c, fcnt, 4);
+  dzero(c, fcnt, 8);
   dzero(c, qflag, n);
   launch(c, "match_inc", 16.0 * ne, [&] {
     k_inc_keys<<<grid_for(c, ne, 256), 256, 0, c.stream>>>(props, ne, prop, keys);
@@ -1172,11 +1173,11 @@ static void resolve_frontier(Ctx& c, int64_t n, const int32_t* prop, int32_t* pa
   });
   static const bool mstats = getenv("JET_MATCH_STATS") && getenv("JET_MATCH_STATS")[0] == '1';
   if (mstats) {
-    unsigned long long hs[4];
-    d2h(c, hs, fcnt, 4);
+    unsigned long long hs[8];
+    d2h(c, hs, fcnt, 8);
     c.sync();
     fprintf(stderr, "FRONTIER n=%lld edges=%lld blocks=%d rounds=%llu\n", (long long)n,
-            (long long)ne, blocks, hs[3]);
+            (long long)ne, blocks, hs[4]);
   }
 }
 
