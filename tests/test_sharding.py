@@ -61,6 +61,16 @@ def test_sharded_equals_unsharded(size):
         assert np.array_equal(pw, ref_pw)
 
 
+def test_sharded_skewed_rmat():
+    """Skewed degrees (hub rows, block-per-row tiers) through the sharded path."""
+    g = gen.rmat_graph(13, 16, 2)
+    cfg = J.RefinerConfig(k=32, imbalance=0.03, seed=0, deterministic=True)
+    ref_parts, ref_pw, ref_st = partition_resident(_lib.DeviceGraph.upload(g), g, cfg)
+    for parts, pw, st in _run_sharded(g, cfg, 2, shard_min=500):
+        assert st.cutsize == ref_st.cutsize
+        assert np.array_equal(parts, ref_parts)
+
+
 def test_sharded_pipeline_goldens(golden):
     """The reference's own answers on the pipeline cases, sharded over 2."""
     from conftest import graph_of
