@@ -2,18 +2,23 @@
 
 Workload (BASELINE.json configs[1]): 3D 27-point grid 128^3 (n = 2,097,152,
 m = 26,822,908), k = 64, lambda = 1.03 (imbalance 0.03), seed 0, unit
-weights, deterministic reference semantics (the cut equals the reference's).
-A step is one complete `partition` (coarsening, initial partitioning,
-uncoarsening with Jet refinement). Metric: edges/s = m / partition time.
+weights. A step is one complete `partition` (coarsening, initial
+partitioning, uncoarsening with Jet refinement). Metric: edges/s = m /
+partition time, with the cut ratio against the reference's cut.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--mode throughput|deterministic] [--shard]
 
+--mode throughput (default) is the partitioner's fast mode (north_star: cut
+within 2 % of the reference, balance always met); the bit-exact deterministic
+mode on the same workload is reported alongside ("deterministic_mode").
 `value` times jet_partition_graph on the HBM-resident CSR with CUDA events;
 `e2e` times the public `partition(graph, config)` from host int64 arrays
 (H2D of the CSR and D2H of the parts inside the timed region). The reference
 arm times the CPU oracle (oracle/, a C port of the reference algorithm) on
-the host. N > 1: every rank partitions its own replica (the path does not
-shard yet; SURVEY §8(e) sharding is the next row), value = N*m / max time.
+the host. N > 1: every rank partitions its own replica (value = N*m / max
+time), or with --shard one partition whose finest levels are sharded over
+the ranks (NCCL; value = m / max time).
 """
 
 from __future__ import annotations
@@ -204,7 +209,7 @@ EXTRA_CONFIGS = [  # BASELINE configs 3-4, generated on the device (reference ge
 ]
 
 
-def measure_extra_configs(ctx, steps=2):
+def measure_extra_configs(ctx, det=True, steps=2):
     """Device-timed partitions of configs 3-4 (inputs generated on the device,
     identical to the reference's generators); cut vs the reference's
     (tests/golden/quality.json, C oracle pinned to the reference)."""
@@ -224,7 +229,7 @@ def measure_extra_configs(ctx, steps=2):
             n = 1 << 24
             dg = gen.geometric_device(n, math.sqrt(12 / (math.pi * n)), 0, ctx=ctx)
         n, nnz, W = dg.info()
-        cfg = J.RefinerConfig(k=k, imbalance=IMB, seed=SEED, deterministic=True)
+        cfg = J.RefinerConfig(k=k, imbalance=IMB, seed=SEED, deterministic=det)
         partition_resident(dg, None, cfg, want_parts=False)  # warm
         ms = []
         for _ in range(steps):
@@ -239,7 +244,7 @@ def measure_extra_configs(ctx, steps=2):
                     "reference_cutsize": ref,
                     "cut_ratio_vs_cpu_ref": (int(st.cutsize) / ref) if ref else None,
                     "balanced": bool(st.balanced), "steps": steps,
-                    "mode": "deterministic (bit-exact reference semantics)"})
+                    "mode": "deterministic (bit-exact reference semantics)" if det else "throughput"})
         dg.free()
     return out
 
@@ -251,7 +256,8 @@ def run_ours(args, world, rank, local):
     from paper_2304_13194_b200.driver import partition_resident
 
     g = gen.grid27_graph(GRID_N)
-    cfg = J.RefinerConfig(k=K, imbalance=IMB, seed=SEED, deterministic=True)
+    det = args.mode == "deterministic"
+    cfg = J.RefinerConfig(k=K, imbalance=IMB, seed=SEED, deterministic=det)
     ctx = _lib.Context(local)
     sharded = args.shard and world > 1
     if sharded:  # one partition, finest levels sharded across the ranks (NCCL)
@@ -273,7 +279,10 @@ def run_ours(args, world, rank, local):
     dominant = max(classes, key=lambda c: classes[c]["ms"])
     step_device_ms = sum(v["ms"] for v in classes.values())
     dominant_share = classes[dominant]["ms"] / step_device_ms
-    assert st.cutsize == REF_CUT, (st.cutsize, REF_CUT)
+    if det:  # bit-exact with the reference
+        assert st.cutsize == REF_CUT, (st.cutsize, REF_CUT)
+    else:  # throughput mode: the north_star gate
+        assert st.balanced and st.cutsize <= 1.02 * REF_CUT, (st.cutsize, REF_CUT)
 
     # timed region: device-resident partitions, events around each step,
     # L2 flushed between steps; events on the dominant kernel class only
@@ -313,7 +322,7 @@ def run_ours(args, world, rank, local):
         t = time.perf_counter()
         res = J.partition(g, cfg, ctx=ctx)
         e2e.append(time.perf_counter() - t)
-        assert res.state.cutsize == REF_CUT
+        assert res.state.cutsize == st.cutsize
     barrier(world)
     e2e_s = max_over_ranks(statistics.mean(e2e), world)
     e2e_v = (1 if sharded else world) * g.m / e2e_s
@@ -325,14 +334,31 @@ def run_ours(args, world, rank, local):
                "sample": f"one full partition of the same workload on the host "
                          f"({dt:.1f} s, cut {cut}); C port of the reference algorithm"}
     clocks = clk.summary()
-    extra = measure_extra_configs(ctx) if (rank == 0 and not args.no_extra_configs) else None
+    extra = measure_extra_configs(ctx, det) if (rank == 0 and not args.no_extra_configs) else None
+    det_line = None
+    if not det and rank == 0:
+        # the deterministic (bit-exact) mode on the same workload, for reference
+        dcfg = J.RefinerConfig(k=K, imbalance=IMB, seed=SEED, deterministic=True)
+        partition_resident(dg, g, dcfg, want_parts=False)
+        dms = []
+        for _ in range(2):
+            ctx.flush_l2()
+            ctx.timer_start()
+            _, _, dst = partition_resident(dg, g, dcfg, want_parts=False)
+            dms.append(ctx.timer_stop())
+        assert dst.cutsize == REF_CUT
+        det_line = {"ms_per_step": sum(dms) / len(dms), "value": g.m / (sum(dms) / len(dms) * 1e-3),
+                    "cutsize": int(dst.cutsize), "cut_ratio_vs_cpu_ref": 1.0,
+                    "note": "bit-identical to the reference (matching, hierarchy, moves, cut)"}
     if rank == 0:
         line = {
             "metric": "edges/s", "value": value, "unit": "edges/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "mode": "deterministic (bit-exact reference semantics)",
+            "config": {"workload": WORKLOAD,
+                       "mode": ("deterministic (bit-exact reference semantics)" if det else
+                                "throughput (hashed-priority matching; cut gate: <= 1.02x reference)"),
                        "l2": "flushed (256 MB memset) before every timed step; L0 CSR is 430 MB",
                        "parallelism": (f"1D vertex-sharded Jetlp x{world} (levels >= "
                                        f"{args.shard_min_vertices} vertices), NCCL") if sharded
@@ -353,6 +379,7 @@ def run_ours(args, world, rank, local):
             "cpu_baseline": cpu,
             "clocks": clocks,
             "configs_measured": extra,
+            "deterministic_mode": det_line,
         }
         print(json.dumps(line), flush=True)
 
@@ -365,6 +392,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra-configs", action="store_true")
+    ap.add_argument("--mode", choices=["throughput", "deterministic"], default="throughput",
+                    help="throughput (default): the partitioner's fast mode, cut gated at 1.02x the "
+                         "reference; deterministic: bit-identical to the reference")
     ap.add_argument("--shard", action="store_true",
                     help="N>1: shard the finest levels across the ranks instead of replicas")
     ap.add_argument("--shard-min-vertices", type=int, default=1 << 20)
