@@ -756,6 +756,65 @@ struct SegLists {
   const unsigned long long* cnt;  // NBINS consecutive counters
 };
 
+// Afterburner over the short-row tiers: a G-lane group per row, so a warp
+// keeps 32/G rows in flight (a warp per ~10-entry row left the coarse levels
+// latency-bound).
+template <int G, bool UNIT>
+static __device__ __forceinline__ void ab_group_rows(const AbArgs& a, const GView& g,
+                                                     const int32_t* __restrict__ list, int64_t cnt,
+                                                     int t, const RbSegsDev& mseg, int64_t w0,
+                                                     int64_t ws, unsigned long long* wr,
+                                                     unsigned long long* we, long long* nmove) {
+  constexpr int RPS = 32 / G;
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1), grp = lane / G;
+  const unsigned gm = group_mask<G>();
+  for (int64_t base = w0 * RPS; base < cnt; base += ws * RPS) {
+    const int64_t i = base + grp;
+    const bool has = i < cnt;
+    int v = 0, own = -1, dv = -1;
+    long long Fv = 0;
+    int64_t b = 0, e = 0;
+    if (has) {
+      v = list[i];
+      own = a.parts[v];
+      dv = a.cdest[v];
+      Fv = a.F[v];
+      b = g.offs[v];
+      e = g.offs[v + 1];
+      if (wr && gl == 0) {
+        *wr += 1;
+        *we += (unsigned long long)(e - b);
+      }
+    }
+    long long f2 = 0;
+    for (int64_t j = b + gl; j < e; j += G) {
+      const int u = g.adj[j];
+      int eff = a.parts[u];
+      const int cu = a.cdest[u];
+      if (cu >= 0) {
+        const long long Fu = a.F[u];
+        if (Fu > Fv || (Fu == Fv && u < v)) eff = cu;
+      }
+      const int w = UNIT ? 1 : g.ew[j];
+      f2 += (eff == dv) ? w : (eff == own) ? -w : 0;
+    }
+    f2 = gsum<G>(f2, gm);
+    if (has && gl == 0) {
+      if (a.f2_out) a.f2_out[v] = f2;
+      if (f2 >= 0) {
+        if (a.move_list) {
+          a.mv[v] = dv;
+          const unsigned long long q = atomicAdd(a.move_cnt + t, 1ull);
+          a.move_list[mseg.b[t] + q] = v;
+        } else if (nmove) {
+          a.mv[v] = dv;
+          *nmove += 1;
+        }
+      }
+    }
+  }
+}
+
 // One warp per candidate over all tiers (candidate sets are small).
 // With a move list, moves are appended per row (host-driven path); without
 // one (level kernel) only mv[v] is set and the moves are counted into
@@ -810,6 +869,10 @@ static __device__ void afterburner_rows(const AbArgs& a, const GView& g, const S
           }
         }
       }
+      continue;
+    }
+    if (t < BIN_WARP) {  // short rows: 8-lane groups, four rows per warp step
+      ab_group_rows<8, UNIT>(a, g, list, cnt, t, mseg, w0, ws, wr, we, nmove);
       continue;
     }
     for (int64_t i = w0; i < cnt; i += ws) {
@@ -895,6 +958,45 @@ static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const S
           acc += mu >= 0 ? cc : 2 * cc;
         }
         if (threadIdx.x == 0) {
+          const unsigned long long wv = (unsigned long long)g.vw[v];
+          atomicAdd(&a.pw[dst], wv);
+          atomicAdd(&a.pw[old], (unsigned long long)(-(long long)wv));
+        }
+      }
+      continue;
+    }
+    if (t < BIN_WARP) {  // short rows: 8-lane groups, four rows per warp step
+      constexpr int G = 8, RPS = 4;
+      const int gl = lane & (G - 1), grp = lane / G;
+      for (int64_t base = w0 * RPS; base < cnt; base += ws * RPS) {
+        const int64_t i = base + grp;
+        int v = 0, dst = -1, old = 0;
+        int64_t b = 0, e = 0;
+        if (i < cnt) {
+          v = list[i];
+          dst = a.mv[v];
+          if (dst >= 0) {
+            old = a.parts[v];
+            b = g.offs[v];
+            e = g.offs[v + 1];
+            if (wr && gl == 0) {
+              *wr += 1;
+              *we += (unsigned long long)(e - b);
+            }
+          }
+        }
+        long long d = 0;
+        for (int64_t j = b + gl; j < e; j += G) {
+          const int u = g.adj[j];
+          const int pu = a.parts[u];
+          const int mu = a.mv[u];
+          const int nu = mu >= 0 ? mu : pu;
+          const long long w = UNIT ? 1 : g.ew[j];
+          const long long cc = w * ((long long)(nu != dst) - (long long)(pu != old));
+          d += mu >= 0 ? cc : 2 * cc;
+        }
+        acc += d;
+        if (dst >= 0 && gl == 0) {
           const unsigned long long wv = (unsigned long long)g.vw[v];
           atomicAdd(&a.pw[dst], wv);
           atomicAdd(&a.pw[old], (unsigned long long)(-(long long)wv));
