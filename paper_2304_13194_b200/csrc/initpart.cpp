@@ -52,6 +52,31 @@ void bfs_hops(const HostGraph& g, int32_t src, std::vector<int64_t>& dist,
     if (dist[v] < 0) dist[v] = n + 1;  // unreachable counts as infinitely far
 }
 
+// min_dist[v] = min(min_dist[v], hops(src, v)) without a full BFS: a vertex
+// is expanded only when src improves its distance. If hops(src, u) >=
+// min_dist[u] = hops(s', u) for an earlier seed s', no vertex behind u can
+// be closer to src than to s', so the pruned search yields exactly the
+// reference's np.minimum(min_dist, _bfs_hops(graph, src)) (initpart.py:38-40)
+// while visiting only src's new Voronoi cell.
+void bfs_improve(const HostGraph& g, int32_t src, std::vector<int64_t>& min_dist,
+                 std::vector<int32_t>& queue) {
+  queue.clear();
+  if (min_dist[src] == 0) return;
+  min_dist[src] = 0;
+  queue.push_back(src);
+  for (size_t h = 0; h < queue.size(); ++h) {
+    const int32_t v = queue[h];
+    const int64_t dv = min_dist[v] + 1;
+    for (int64_t j = g.offs[v]; j < g.offs[v + 1]; ++j) {
+      const int32_t u = (int32_t)g.adj[j];
+      if (dv < min_dist[u]) {
+        min_dist[u] = dv;
+        queue.push_back(u);
+      }
+    }
+  }
+}
+
 std::vector<int32_t> grow_single(const HostGraph& g, int k, Pcg64 rng) {
   const int64_t n = g.n;
   std::vector<int32_t> seeds;
@@ -63,9 +88,9 @@ std::vector<int32_t> grow_single(const HostGraph& g, int k, Pcg64 rng) {
   for (int j = 1; j < k; ++j) {
     int32_t nxt = (int32_t)(std::max_element(min_dist.begin(), min_dist.end()) - min_dist.begin());
     seeds.push_back(nxt);
-    bfs_hops(g, nxt, d, queue);
-    for (int64_t v = 0; v < n; ++v) min_dist[v] = std::min(min_dist[v], d[v]);
+    bfs_improve(g, nxt, min_dist, queue);
   }
+  (void)d;
 
   std::vector<int32_t> parts(n, -1);
   std::vector<int64_t> weights(k, 0);
