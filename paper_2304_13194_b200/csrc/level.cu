@@ -61,6 +61,7 @@ struct LevelArgs {
   TierMap tm;
   int wide;
   int t3_two;  // tier 3 holds rows of 33..64 entries (two per lane)
+  int tail_grid_min;  // evicted sets above this are ranked by the whole grid
   const int32_t* tlist[NBINS];
   int64_t tcnt[NBINS];
   RbSegsDev seg;
@@ -783,7 +784,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       pc.mark(13);
       // large evicted sets: order them with the whole grid, and for weak
       // passes assign the random destinations with the whole grid too
-      const bool big_tail = P2ev > LV_TAIL_SMEM / 4;
+      const bool big_tail = P2ev > A.tail_grid_min;
       if (big_tail && !lv_tail_rank(A, Lev, nb, gsync, t0, nt))
         lv_grid_sort(A, Lev, P2ev, nb, lv_smem, gsync, t0, nt);
       pc.mark(12);
@@ -952,6 +953,11 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   A.tm = g.tm;
   A.wide = g.max_wdeg >= (1LL << 31);
   A.t3_two = g.max_deg > 32;
+  static const int tail_grid_min = [] {
+    const char* e = getenv("JET_TAIL_GRID_MIN");
+    return e ? atoi(e) : LV_TAIL_SMEM / 4;
+  }();
+  A.tail_grid_min = tail_grid_min;
   for (int t = 0; t < NBINS; ++t) {
     A.tlist[t] = tier_list(g, t);
     A.tcnt[t] = g.bin_cnt[t];
