@@ -50,3 +50,23 @@ def test_throughput_matching_is_a_matching():
     res = J.partition(g, J.RefinerConfig(k=16, seed=0, deterministic=False))
     assert res.metrics["balanced"]
     assert len(np.unique(res.state.parts)) == 16
+
+
+@pytest.mark.parametrize("name", ["rmat22", "rgg16m"])
+def test_large_configs_gate(name):
+    """BASELINE configs 3-4 (device-generated, identical to the reference's
+    generators) in throughput mode: balanced, cut <= 1.02x the reference's."""
+    from paper_2304_13194_b200.driver import partition_resident
+    case = QUALITY[name]
+    spec = case["spec"]
+    dg = gen.rmat_device(spec[1], spec[2], spec[3]) if spec[0] == "rmat" else \
+        gen.geometric_device(spec[1], spec[2], spec[3])
+    try:
+        cfg = J.RefinerConfig(k=case["k"], imbalance=case["imbalance"], seed=0, deterministic=False)
+        _, pw, st = partition_resident(dg, None, cfg, want_parts=False)
+        n, _, W = dg.info()
+        assert st.balanced
+        assert int(pw.max()) <= J.part_weight_limit(W, case["k"], case["imbalance"])
+        assert st.cutsize <= 1.02 * case["cuts"]["0"], (st.cutsize, case["cuts"]["0"])
+    finally:
+        dg.free()
