@@ -1044,7 +1044,13 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   }();
   const int64_t want = std::max((g.n + rows_per_block - 1) / rows_per_block,
                                 (g.nnz + LV_ENTRIES_PER_BLOCK - 1) / LV_ENTRIES_PER_BLOCK);
-  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * c.num_sms));
+  static const int64_t one_block_n = [] {
+    const char* e = getenv("JET_LV_ONE_BLOCK_N");
+    return e ? (int64_t)atoll(e) : (int64_t)0;
+  }();
+  const int blocks = g.n <= one_block_n
+                         ? 1
+                         : (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * c.num_sms));
   void* args[] = {&A};
   launch(c, "refine_level", 0.0, [&] {
     CK(cudaLaunchCooperativeKernel(kern, dim3(blocks), dim3(LV_BLOCK), args, smem, c.stream));
