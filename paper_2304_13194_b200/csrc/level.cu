@@ -75,6 +75,7 @@ struct LevelArgs {
   int32_t* cand_lists;
   int32_t* move_lists;
   unsigned long long* ctr;
+  unsigned long long* ctr2;  // second per-pass counter block (CTR_PW words)
   long long* keep_pw;
   int32_t* rkey;
   int32_t* rbest;
@@ -150,7 +151,8 @@ __device__ __forceinline__ int dev_ceil_log2(long long x) {
 }
 
 // ---------------------------------------------------------------- decide
-__device__ void lv_decide(const LevelArgs& A) {
+// P: the per-pass counter block of the pass being decided (zeroed here)
+__device__ void lv_decide(const LevelArgs& A, unsigned long long* P) {
   typedef cub::BlockScan<int, LV_BLOCK> BScan;
   typedef cub::BlockReduce<long long, LV_BLOCK> BRed;
   __shared__ typename BScan::TempStorage ts;
@@ -185,7 +187,7 @@ __device__ void lv_decide(const LevelArgs& A) {
     s_kind = kind;
     C->kind = kind;
   }
-  for (int i = tid; i < CTR_PW; i += LV_BLOCK) A.ctr[i] = 0;
+  for (int i = tid; i < CTR_PW; i += LV_BLOCK) P[i] = 0;
   __syncthreads();
   if (s_kind < 2) return;
 
@@ -276,7 +278,7 @@ __device__ void lv_decide(const LevelArgs& A) {
 }
 
 // -------------------------------------------------------------- bookkeep
-__device__ void lv_bookkeep(const LevelArgs& A) {
+__device__ void lv_bookkeep(const LevelArgs& A, const unsigned long long* P) {
   typedef cub::BlockReduce<long long, LV_BLOCK> BRed;
   __shared__ typename BRed::TempStorage tr;
   __shared__ int s_copy;
@@ -289,9 +291,9 @@ __device__ void lv_bookkeep(const LevelArgs& A) {
   if (tid == 0) {
     const int kind = C->kind;
     long long nm = 0;
-    for (int t = 0; t < NBINS; ++t) nm += (long long)__ldcg(A.ctr + CTR_MOVE + t);
-    nm += (long long)__ldcg(A.ctr + CTR_NMOVE);
-    const long long d2 = (long long)__ldcg(A.ctr + CTR_CUT2D);
+    for (int t = 0; t < NBINS; ++t) nm += (long long)__ldcg(P + CTR_MOVE + t);
+    nm += (long long)__ldcg(P + CTR_NMOVE);
+    const long long d2 = (long long)__ldcg(P + CTR_CUT2D);
     C->cut += d2 / 2;
     if (kind == 1) {
       C->lp++;
@@ -330,9 +332,9 @@ __device__ void lv_bookkeep(const LevelArgs& A) {
     if (A.trace && C->iterations <= A.trace_cap) {
       long long* t = A.trace + 10 * (C->iterations - 1);
       long long ncand = 0;
-      for (int q = 0; q < NBINS; ++q) ncand += (long long)__ldcg(A.ctr + CTR_CAND + q);
+      for (int q = 0; q < NBINS; ++q) ncand += (long long)__ldcg(P + CTR_CAND + q);
       t[6] = ncand;
-      t[7] = (long long)__ldcg(A.ctr + CTR_RCAND);
+      t[7] = (long long)__ldcg(P + CTR_RCAND);
       t[8] = kind >= 2 ? C->max_evict : 0;
       t[9] = kind >= 2 ? C->nover : 0;
       t[0] = kind;
@@ -662,21 +664,30 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
     cands.list[t] = A.cand_lists + A.seg.b[t];
     moves.list[t] = A.move_lists + A.seg.b[t];
   }
-  cands.cnt = A.ctr + CTR_CAND;
-  moves.cnt = A.ctr + CTR_MOVE;
   int32_t* clists[NBINS];
   for (int t = 0; t < NBINS; ++t) clists[t] = A.cand_lists + A.seg.b[t];
 
   PhaseClock pc(A.phase_clk);
   WorkAcc wk;
+  // Per-pass counters alternate between two blocks by pass parity, so block
+  // 0 can book-keep pass i and decide pass i+1 (zeroing the other block)
+  // while the other blocks still commit pass i: one grid barrier per pass
+  // fewer. The part weights (A.ctr + CTR_PW) are not per pass.
+  if (blockIdx.x == 0) lv_decide(A, A.ctr);  // pass_index 0 -> A.ctr
+  gsync();
   while (true) {
-    pc.mark(15);
-    if (blockIdx.x == 0) lv_decide(A);
-    gsync();
     pc.mark(0);
     const int kind = ldv(&C->kind);
     pc.kind = kind;
     if (kind == 0) break;
+    const int pass = ldv(&C->pass_index);
+    unsigned long long* P = (pass & 1) ? A.ctr2 : A.ctr;
+    cands.cnt = P + CTR_CAND;
+    moves.cnt = P + CTR_MOVE;
+    // the previous pass's state became the kept one: copy it while this
+    // pass's first phase runs (only the commit phase writes parts)
+    if (ldv(&C->copy_keep))
+      for (int64_t v = t0; v < A.n; v += nt) A.keep[v] = A.parts[v];
     long long acc = 0;
     if (kind == 1) {
       // ---- Jetlp (refine.py:159-183)
@@ -697,8 +708,8 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
         a.lock = A.lock;
         a.p = lp;
         a.out_list = (A.afterburner ? A.cand_lists : A.move_lists) + A.seg.b[t];
-        a.out_cnt = A.ctr + (A.afterburner ? CTR_CAND : CTR_MOVE) + t;
-        a.cut2 = A.ctr + CTR_CUT2;
+        a.out_cnt = P + (A.afterburner ? CTR_CAND : CTR_MOVE) + t;
+        a.cut2 = P + CTR_CUT2;
         return a;
       };
       // per-warp tables start at lv_smem + warp * per inside agg_warp
@@ -715,7 +726,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
         ab.move_cnt = nullptr;
         long long nmv = 0;
         afterburner_rows<UNIT>(ab, A.g, cands, A.seg, w0, nw, &wk.v[2], &wk.v[3], &nmv);
-        block_sum_atomic_any(nmv, A.ctr + CTR_NMOVE);
+        block_sum_atomic_any(nmv, P + CTR_NMOVE);
         gsync();
         pc.mark(2);
       }
@@ -727,7 +738,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       for (int64_t i = t0; i < (int64_t)nover * (nb / ldv(&C->rho)); i += nt) A.Hs[i] = 0;
       for (int64_t i = t0; i < (int64_t)nover * nch; i += nt) A.CH[i] = 0;
       if (!strong) lv_draws(A, t0, nt);
-      rb_collect(A.parts, A.opidx, A.g.offs, A.tm, A.n, A.cand_lists, A.seg, A.ctr + CTR_CAND, t0, nt,
+      rb_collect(A.parts, A.opidx, A.g.offs, A.tm, A.n, A.cand_lists, A.seg, P + CTR_CAND, t0, nt,
                  &wk.v[0], &wk.v[1]);
       gsync();
       pc.mark(3);
@@ -746,10 +757,10 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       ra.rbest = A.rbest;
       ra.rloss = A.rloss;
       ra.rcand = A.rcand;
-      ra.rcand_cnt = A.ctr + CTR_RCAND;
+      ra.rcand_cnt = P + CTR_RCAND;
       ra.H = A.H;
       ra.Hs = A.Hs;
-      lv_sweep<RbOp, UNIT>(A, [&](int) { return ra; }, clists, A.ctr + CTR_CAND, lv_smem, w0, nw,
+      lv_sweep<RbOp, UNIT>(A, [&](int) { return ra; }, clists, P + CTR_CAND, lv_smem, w0, nw,
                            acc);
       gsync();
       pc.mark(4);
@@ -758,18 +769,18 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
         rb_scan_warp((int)op, A.H, A.Hs, nb, ldv(&C->rho), A.deficit, A.bstar, A.cum_before);
       gsync();
       pc.mark(5);
-      rb_chunk(s, A.rcand, A.ctr + CTR_RCAND, t0, nt);
+      rb_chunk(s, A.rcand, P + CTR_RCAND, t0, nt);
       gsync();
       pc.mark(6);
       for (int64_t op = w0; op < nover; op += nw)
         rb_find_warp((int)op, s, A.deficit, A.required, A.cum_before, A.opart, A.n, nb, A.thr);
       gsync();
       pc.mark(7);
-      rb_select(s, A.rcand, A.ctr + CTR_RCAND, A.rbest, strong, 1, A.evict, A.ctr + CTR_EVICT,
-                A.mv, A.g.offs, A.tm, A.move_lists, A.seg, A.ctr + CTR_MOVE, t0, nt);
+      rb_select(s, A.rcand, P + CTR_RCAND, A.rbest, strong, 1, A.evict, P + CTR_EVICT,
+                A.mv, A.g.offs, A.tm, A.move_lists, A.seg, P + CTR_MOVE, t0, nt);
       gsync();
       pc.mark(8);
-      const int Lev = (int)*(const volatile unsigned long long*)(A.ctr + CTR_EVICT);
+      const int Lev = (int)*(const volatile unsigned long long*)(P + CTR_EVICT);
       int P2ev = 1;
       while (P2ev < Lev) P2ev <<= 1;
       if (!strong && *(const volatile unsigned long long*)&C->rejects) {
@@ -799,12 +810,12 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
             t = A.tm(A.g.offs[v + 1] - A.g.offs[v]);
           }
           for (int tt = 0; tt < NBINS; ++tt)
-            warp_append(t == tt, v, A.move_lists + A.seg.b[tt], A.ctr + CTR_MOVE + tt);
+            warp_append(t == tt, v, A.move_lists + A.seg.b[tt], P + CTR_MOVE + tt);
         }
       } else if (blockIdx.x == 0) {
         RbTail tl{};
         tl.evict = A.evict;
-        tl.evict_cnt = A.ctr + CTR_EVICT;
+        tl.evict_cnt = P + CTR_EVICT;
         tl.parts = A.parts;
         tl.opidx = A.opidx;
         tl.rkey = A.rkey;
@@ -820,7 +831,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
         tl.mv = A.mv;
         tl.move_lists = A.move_lists;
         tl.mseg = A.seg;
-        tl.move_cnt = A.ctr + CTR_MOVE;
+        tl.move_cnt = P + CTR_MOVE;
         tl.smem_cap = LV_TAIL_SMEM;
         tl.gscratch = A.gscratch;
         tl.presorted = big_tail;
@@ -831,11 +842,11 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
     }
     // ---- apply (conn.py:215-254)
     {
-      ApArgs ap{A.parts, A.mv, A.ctr + CTR_PW, A.ctr + CTR_CUT2D, A.k};
+      ApArgs ap{A.parts, A.mv, A.ctr + CTR_PW, P + CTR_CUT2D, A.k};
       long long d = 0;
       apply_delta_rows<UNIT>(ap, A.g, (kind == 1 && A.afterburner) ? cands : moves, w0, nw, d,
                              &wk.v[4], &wk.v[5]);
-      block_sum_atomic_any(d, A.ctr + CTR_CUT2D);
+      block_sum_atomic_any(d, P + CTR_CUT2D);
     }
     gsync();
     pc.mark(10);
@@ -851,15 +862,18 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       ca.cnts = ml.cnt;
       apply_commit_rows(ca, t0, nt);
     }
-    if (blockIdx.x == 0) lv_bookkeep(A);
+    if (blockIdx.x == 0) {
+      lv_bookkeep(A, P);
+      lv_decide(A, (pass & 1) ? A.ctr : A.ctr2);
+    }
     gsync();
     pc.mark(11);
-    if (ldv(&C->copy_keep))
-      for (int64_t v = t0; v < A.n; v += nt) A.keep[v] = A.parts[v];
     (void)wtab;
   }
-  // the returned state is the best balanced one, or the fallback
-  for (int64_t v = t0; v < A.n; v += nt) A.parts[v] = A.keep[v];
+  // the returned state is the best balanced one, or the fallback; when the
+  // last pass made the kept state, parts already is it
+  if (!ldv(&C->copy_keep))
+    for (int64_t v = t0; v < A.n; v += nt) A.parts[v] = A.keep[v];
   for (int i = 0; i < 6; ++i) block_sum_atomic_any((long long)wk.v[i], A.work + i);
 }
 
@@ -877,6 +891,7 @@ struct LevelScratch : CtxExt {
   DBuf<unsigned long long> gscratch;
   DBuf<unsigned> tailbuf;
   DBuf<unsigned long long> work;
+  DBuf<unsigned long long> ctr2;
 };
 
 static LevelScratch& level_scratch(Ctx& c) {
@@ -973,6 +988,8 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   A.cand_lists = w.lists.get();
   A.move_lists = w.lists.get() + w.cap_n;
   A.ctr = w.ctr.get();
+  S.ctr2.ensure(CTR_PW, c.stream);
+  A.ctr2 = S.ctr2.get();
   A.keep_pw = S.keep_pw.get();
   A.rkey = w.rkey.get();
   A.rbest = w.rbest.get();
