@@ -61,6 +61,16 @@ def test_sharded_equals_unsharded(size):
         assert np.array_equal(pw, ref_pw)
 
 
+def test_sharded_throughput_mode():
+    """Throughput mode is deterministic run to run, so sharding reproduces it too."""
+    g = gen.grid27_graph(32)
+    cfg = J.RefinerConfig(k=16, imbalance=0.03, seed=3, deterministic=False)
+    ref_parts, _, ref_st = partition_resident(_lib.DeviceGraph.upload(g), g, cfg)
+    for parts, pw, st in _run_sharded(g, cfg, 2, shard_min=2000):
+        assert st.cutsize == ref_st.cutsize
+        assert np.array_equal(parts, ref_parts)
+
+
 def test_sharded_skewed_rmat():
     """Skewed degrees (hub rows, block-per-row tiers) through the sharded path."""
     g = gen.rmat_graph(13, 16, 2)
