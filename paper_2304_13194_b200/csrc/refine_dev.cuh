@@ -677,19 +677,30 @@ static __device__ void agg_block(const typename Op::Args& a, const GView& g,
     if (Op::skip(a, v, own)) continue;  // uniform across the block
     const int64_t b = g.offs[v], e = g.offs[v + 1];
     long long ex = 0;
-    for (int64_t j0 = b; j0 < e; j0 += blockDim.x) {
-      const int64_t j = j0 + threadIdx.x;
-      int p = -1, w = 0;
-      if (j < e) {
-        p = parts[g.adj[j]];
-        w = UNIT ? 1 : g.ew[j];
-        ex += Op::extra(a, p, w);
+    // four strides of the row in flight per step: hub rows of 10^4-10^5
+    // entries were bound by the adjacency -> part gather round trips
+    constexpr int U = 4;
+    const int64_t step = (int64_t)blockDim.x * U;
+    for (int64_t j0 = b; j0 < e; j0 += step) {
+      int uu[U], pp[U], ww[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int64_t j = j0 + (int64_t)q * blockDim.x + threadIdx.x;
+        uu[q] = j < e ? g.adj[j] : -1;
+        ww[q] = j < e ? (UNIT ? 1 : g.ew[j]) : 0;
       }
-      const unsigned peers = __match_any_sync(0xffffffffu, p);
-      const long long s = UNIT ? (long long)__popc(peers) : peer_sum(peers, w, wide);
-      if (p >= 0 && (__ffs(peers) - 1) == lane) {
-        unsigned long long old = atomicAdd(&tab[p], (unsigned long long)s);
-        if (old == 0) tl[atomicAdd(&tcnt, 1)] = p;
+#pragma unroll
+      for (int q = 0; q < U; ++q) pp[q] = uu[q] >= 0 ? parts[uu[q]] : -1;
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int p = pp[q], w = ww[q];
+        if (p >= 0) ex += Op::extra(a, p, w);
+        const unsigned peers = __match_any_sync(0xffffffffu, p);
+        const long long s = UNIT ? (long long)__popc(peers) : peer_sum(peers, w, wide);
+        if (p >= 0 && (__ffs(peers) - 1) == lane) {
+          unsigned long long old = atomicAdd(&tab[p], (unsigned long long)s);
+          if (old == 0) tl[atomicAdd(&tcnt, 1)] = p;
+        }
       }
     }
     __syncthreads();
