@@ -1289,10 +1289,19 @@ __device__ __forceinline__ unsigned edge_hash(int a, int b, unsigned salt) {
 
 // Heaviest free neighbour, ties -> highest edge hash, then lowest id. One
 // warp per row (rows of any length), 32 rows per warp batch for short rows.
+// prev (optional): the previous round's {proposers, pairs}; a round after one
+// that matched nothing does nothing (rounds are launched in groups between
+// host checks, and must stop exactly where a per-round check would)
+__device__ __forceinline__ bool fast_round_dead(const unsigned long long* prev) {
+  return prev && (prev[0] == 0 || prev[1] == 0);
+}
+
 template <bool UNIT>
 __global__ void __launch_bounds__(256)
     k_propose_fast(GView g, int64_t n, const int32_t* __restrict__ partner, int32_t* prop,
-                   int32_t* elist, unsigned long long* ecnt, unsigned salt) {
+                   int32_t* elist, unsigned long long* ecnt, unsigned salt,
+                   const unsigned long long* prev) {
+  if (fast_round_dead(prev)) return;
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1347,7 +1356,8 @@ template <bool UNIT>
 __global__ void __launch_bounds__(256)
     k_propose_fast_hub(GView g, const int32_t* __restrict__ hubs, int64_t nh,
                        const int32_t* __restrict__ partner, int32_t* prop, int32_t* elist,
-                       unsigned long long* ecnt, unsigned salt) {
+                       unsigned long long* ecnt, unsigned salt, const unsigned long long* prev) {
+  if (fast_round_dead(prev)) return;
   __shared__ unsigned s_w[8], s_h[8], s_u[8];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t i = blockIdx.x; i < nh; i += gridDim.x) {
@@ -1394,7 +1404,8 @@ __global__ void __launch_bounds__(256)
 __global__ void k_accept_mutual(const int32_t* __restrict__ prop, int32_t* partner,
                                 const int32_t* __restrict__ elist,
                                 const unsigned long long* __restrict__ ecnt,
-                                unsigned long long* npairs) {
+                                unsigned long long* npairs, const unsigned long long* prev) {
+  if (fast_round_dead(prev)) return;
   const int64_t cnt = (int64_t)*ecnt;
   long long mine = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
@@ -1496,49 +1507,62 @@ static void device_match_fast(Ctx& c, const DGraph& g, int32_t* partner) {
   if (g.nnz > 0) {
     int32_t* prop_p = c.scratch<int32_t>(10, n);
     int32_t* elist_p = c.scratch<int32_t>(11, n);
-    DBuf<unsigned long long> cnt(2, c.stream);
+    // rounds in groups of RG between host checks: each round has its own
+    // {proposers, pairs} counters, and a round after one that matched nothing
+    // is a no-op on the device (fast_round_dead), so the result is the same as
+    // checking after every round, with a quarter of the host round trips
+    constexpr int RG = 4, MAXR = 48;
+    DBuf<unsigned long long> cnt(2 * MAXR, c.stream);
+    dzero(c, cnt.get(), 2 * MAXR);
     const GView gv = view(g);
     int64_t matched = 0;
-    for (int round = 0; round < 48; ++round) {
-      dzero(c, cnt.get(), 2);
-      const unsigned salt = 0x5bd1e995u * (unsigned)(round + 1);
-      launch(c, "propose", (g.unit_ew ? 8.0 : 12.0) * g.nnz + 12.0 * n, [&] {
-        if (g.unit_ew)
-          k_propose_fast<true><<<grid_for(c, n, 256), 256, 0, c.stream>>>(
-              gv, n, partner, prop_p, elist_p, cnt.get(), salt);
-        else
-          k_propose_fast<false><<<grid_for(c, n, 256), 256, 0, c.stream>>>(
-              gv, n, partner, prop_p, elist_p, cnt.get(), salt);
-      });
-      if (g.bin_cnt[BIN_BLOCK]) {
-        const int64_t nh = g.bin_cnt[BIN_BLOCK];
-        const int32_t* hubs = tier_list(g, BIN_BLOCK);
-        const unsigned hg = (unsigned)std::min<int64_t>(nh, 4LL * c.num_sms);
-        launch(c, "propose_hub", 0.0, [&] {
+    static const bool fstats = getenv("JET_MATCH_STATS") && getenv("JET_MATCH_STATS")[0] == '1';
+    for (int r0 = 0; r0 < MAXR; r0 += RG) {
+      for (int round = r0; round < r0 + RG; ++round) {
+        unsigned long long* rc = cnt.get() + 2 * round;
+        const unsigned long long* prev = round ? rc - 2 : nullptr;
+        const unsigned salt = 0x5bd1e995u * (unsigned)(round + 1);
+        launch(c, "propose", (g.unit_ew ? 8.0 : 12.0) * g.nnz + 12.0 * n, [&] {
           if (g.unit_ew)
-            k_propose_fast_hub<true><<<hg, 256, 0, c.stream>>>(gv, hubs, nh, partner, prop_p,
-                                                               elist_p, cnt.get(), salt);
+            k_propose_fast<true><<<grid_for(c, n, 256), 256, 0, c.stream>>>(
+                gv, n, partner, prop_p, elist_p, rc, salt, prev);
           else
-            k_propose_fast_hub<false><<<hg, 256, 0, c.stream>>>(gv, hubs, nh, partner, prop_p,
-                                                                elist_p, cnt.get(), salt);
+            k_propose_fast<false><<<grid_for(c, n, 256), 256, 0, c.stream>>>(
+                gv, n, partner, prop_p, elist_p, rc, salt, prev);
+        });
+        if (g.bin_cnt[BIN_BLOCK]) {
+          const int64_t nh = g.bin_cnt[BIN_BLOCK];
+          const int32_t* hubs = tier_list(g, BIN_BLOCK);
+          const unsigned hg = (unsigned)std::min<int64_t>(nh, 4LL * c.num_sms);
+          launch(c, "propose_hub", 0.0, [&] {
+            if (g.unit_ew)
+              k_propose_fast_hub<true><<<hg, 256, 0, c.stream>>>(gv, hubs, nh, partner, prop_p,
+                                                                 elist_p, rc, salt, prev);
+            else
+              k_propose_fast_hub<false><<<hg, 256, 0, c.stream>>>(gv, hubs, nh, partner, prop_p,
+                                                                  elist_p, rc, salt, prev);
+          });
+        }
+        launch(c, "accept", 12.0 * n, [&] {
+          k_accept_mutual<<<grid_for(c, n, 256), 256, 0, c.stream>>>(prop_p, partner, elist_p, rc,
+                                                                     rc + 1, prev);
         });
       }
-      launch(c, "accept", 12.0 * n, [&] {
-        k_accept_mutual<<<grid_for(c, n, 256), 256, 0, c.stream>>>(prop_p, partner, elist_p,
-                                                                   cnt.get(), cnt.get() + 1);
-      });
-      unsigned long long h[2];
-      d2h(c, h, cnt.get(), 2);
+      unsigned long long h[2 * RG];
+      d2h(c, h, cnt.get() + 2 * r0, 2 * RG);
       c.sync();
-      matched += 2 * (int64_t)h[1];
-      // rounds until no pair is added: stopping at a 1 % yield left many
-      // leftovers to the leaf pairing, whose non-adjacent pairs made the
-      // coarse levels refine 2x longer (128^3: 143 -> 72 ms, and a 3 % lower cut)
-      static const bool fstats = getenv("JET_MATCH_STATS") && getenv("JET_MATCH_STATS")[0] == '1';
-      if (fstats)
-        fprintf(stderr, "FAST n=%lld round=%d proposers=%llu pairs=%llu matched=%lld\n",
-                (long long)n, round, h[0], h[1], (long long)matched);
-      if (h[0] == 0 || h[1] == 0) break;
+      bool done = false;
+      for (int q = 0; q < RG && !done; ++q) {
+        matched += 2 * (int64_t)h[2 * q + 1];
+        if (fstats)
+          fprintf(stderr, "FAST n=%lld round=%d proposers=%llu pairs=%llu matched=%lld\n",
+                  (long long)n, r0 + q, h[2 * q], h[2 * q + 1], (long long)matched);
+        // rounds until no pair is added: stopping at a 1 % yield left many
+        // leftovers to the leaf pairing, whose non-adjacent pairs made the
+        // coarse levels refine 2x longer (128^3: 143 -> 72 ms, 3 % lower cut)
+        done = h[2 * q] == 0 || h[2 * q + 1] == 0;
+      }
+      if (done) break;
     }
     leaf_match(c, g, partner);
   }
