@@ -208,6 +208,8 @@ struct Ctx {
   int prof_class(const char* name);
   void flush_prof();
   void ensure_pinned(size_t elems);
+  size_t pool_reserved = 0;
+  void reserve_pool(size_t bytes);
   // pinned upload ring (graph upload from pageable host arrays)
   static constexpr int UPLOAD_BUFS = 3;
   static constexpr size_t UPLOAD_CHUNK = (size_t)32 << 20;

@@ -67,6 +67,20 @@ void Ctx::ensure_pinned(size_t elems) {
   pinned_elems = want;
 }
 
+// Grow the device pool's reservation to `bytes` (one allocation, freed back to
+// the pool, whose release threshold keeps it mapped).
+void Ctx::reserve_pool(size_t bytes) {
+  if (bytes <= pool_reserved) return;
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, bytes, stream) == cudaSuccess) {
+    cudaFreeAsync(p, stream);
+    cudaStreamSynchronize(stream);
+    pool_reserved = bytes;
+  } else {
+    cudaGetLastError();
+  }
+}
+
 void Ctx::ensure_upload_ring() {
   if (up_host[0]) return;
   for (int b = 0; b < UPLOAD_BUFS; ++b) {
@@ -159,15 +173,7 @@ int jet_create(int device, jet_ctx** out) {
       CK(cudaMemGetInfo(&fr, &tot));
       size_t want = std::min<size_t>(fr / 4, (size_t)24 << 30);
       if (const char* e = getenv("JET_POOL_RESERVE_MB")) want = (size_t)atoll(e) << 20;
-      if (want) {
-        void* p = nullptr;
-        if (cudaMallocAsync(&p, want, c->stream) == cudaSuccess) {
-          cudaFreeAsync(p, c->stream);
-          cudaStreamSynchronize(c->stream);
-        } else {
-          cudaGetLastError();
-        }
-      }
+      c->reserve_pool(want);
     }
     c->ensure_pinned(1 << 16);
     const char* hl = getenv("JET_HOST_LEVELS");

@@ -188,6 +188,16 @@ void run_partition(Ctx& c, const DGraph& g0, const jet_config& cfg, int32_t* par
     return;
   }
   const int64_t target = std::max<int64_t>(std::max<int64_t>(cfg.coarse_target, 2LL * k), 32);
+  // a partition needs ~12x the level-0 CSR (hierarchy, workspaces, sort
+  // temporaries); reserve it in the pool before starting, so no allocation
+  // inside the pipeline has to map new memory (100s of ms stalls measured on
+  // dense coarse levels of R-MAT 2^25), capped at 60 % of free memory
+  {
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    const size_t csr = (size_t)g0.nnz * 8 + (size_t)g0.n * 24;
+    c.reserve_pool(std::min<size_t>(12 * csr, c.pool_reserved + fr / 10 * 6));
+  }
   Hierarchy h;
   c.prof_tag = "coarsen:";
   device_build_hierarchy(c, g0, target, h, cfg.deterministic == 0);
