@@ -33,5 +33,14 @@ for cls, a in sorted(agg.items(), key=lambda x: -x[1]["s"]):
                 "dram_gbs": a["bytes"] / a["s"] / 1e9 if a["s"] else None,
                 "source": sys.argv[1].split("/")[-1]}
 json.dump(out, open(sys.argv[2], "w"), indent=1)
-for k, v in list(out.items())[:12]:
-    print(f"{k:24s} {v['launches']:5d} x {v['ms_per_launch']:8.3f} ms  {v['dram_bytes_per_launch']/1e6:10.1f} MB/launch  {v['dram_gbs'] or 0:8.1f} GB/s")
+try:
+    peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"]
+except Exception:
+    peak = 6546.6
+tot_ms = sum(v["ms_per_launch"] * v["launches"] for v in out.values())
+print(f"{'kernel class':24s} {'launches':>8s} {'ms/launch':>10s} {'share':>6s} {'DRAM MB/launch':>15s} {'DRAM GB/s':>10s} {'% of HBM peak':>14s}")
+for k, v in list(out.items())[:16]:
+    share = v["ms_per_launch"] * v["launches"] / tot_ms
+    print(f"{k:24s} {v['launches']:8d} {v['ms_per_launch']:10.3f} {100*share:5.1f}% {v['dram_bytes_per_launch']/1e6:15.1f} "
+          f"{v['dram_gbs'] or 0:10.1f} {100*(v['dram_gbs'] or 0)/peak:13.1f}%")
+print(f"(ncu launch list: serialised, cold-cache per-launch times; peak {peak} GB/s from MEASURED_PEAKS.json)")
