@@ -80,3 +80,19 @@ def test_weighted_graph(det):
         ref = O.partition(g, k=6, imbalance=0.05, seed=2)
         assert r.state.cutsize == ref["cut"]
         assert np.array_equal(r.state.parts, ref["parts"])
+
+
+def test_device_rgg_weighted_vs_oracle():
+    """A device-generated geometric graph (2^15 points) given random integer
+    edge and vertex weights on the host: deterministic mode equals the oracle."""
+    g0 = gen.geometric_graph(1 << 15, 0.012, seed=4)
+    u = np.repeat(np.arange(g0.n), np.diff(g0.row_offsets))
+    v = g0.adjacency
+    w = 1 + (np.minimum(u, v) * 31 + np.maximum(u, v) * 17) % 7
+    vw = 1 + (np.arange(g0.n) * 13) % 3
+    g = J.Graph(g0.row_offsets, g0.adjacency, w.astype(np.int64), vw.astype(np.int64))
+    for k in (16, 100):
+        r = J.partition(g, J.RefinerConfig(k=k, imbalance=0.03, seed=1, deterministic=True))
+        ref = O.partition(g, k=k, imbalance=0.03, seed=1)
+        assert r.state.cutsize == ref["cut"], (k, r.state.cutsize, ref["cut"])
+        assert np.array_equal(r.state.parts, ref["parts"])
