@@ -6,6 +6,8 @@
 #pragma once
 #include "refine.cuh"
 #include <cub/block/block_scan.cuh>
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_merge_sort.cuh>
 
 namespace jet {
 
@@ -1474,141 +1476,348 @@ struct RbTail {
   int presorted;                    // keys already sorted in gscratch (grid sort)
 };
 
+// Warp-aggregated append slot in a shared counter (t < 0: no item).
+static __device__ __forceinline__ unsigned smem_warp_slot(unsigned* ctr, int t) {
+  const unsigned peers = __match_any_sync(0xffffffffu, t);
+  const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+  unsigned b = 0;
+  if (t >= 0 && lane == leader) b = atomicAdd(&ctr[t], (unsigned)__popc(peers));
+  b = __shfl_sync(0xffffffffu, b, leader);
+  return b + (unsigned)__popc(peers & ((1u << lane) - 1u));
+}
+
+constexpr int RB_RADIX_THREADS = 512, RB_RADIX_ITEMS = 4, RB_RANK_MAX = 512;
+#ifndef RB_RADIX_BITS
+#define RB_RADIX_BITS 4
+#endif
+struct RbLess {
+  __device__ __forceinline__ bool operator()(unsigned long long x, unsigned long long y) const {
+    return x < y;
+  }
+};
+#ifdef RB_TAIL_MERGE
+typedef cub::BlockMergeSort<unsigned long long, RB_RADIX_THREADS, RB_RADIX_ITEMS> RbRadix;
+#else
+typedef cub::BlockRadixSort<unsigned long long, RB_RADIX_THREADS, RB_RADIX_ITEMS, cub::NullType,
+                           RB_RADIX_BITS>
+    RbRadix;
+#endif
+
 static __device__ void rb_tail(const RbTail& a, unsigned long long* sk_smem) {
-  __shared__ long long s_room;
-  __shared__ int s_di, s_done;
-  __shared__ long long s_wsum[32];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, nth = blockDim.x;
   const int L = (int)*(const volatile unsigned long long*)a.evict_cnt;
   int P2 = 1;
   while (P2 < L) P2 <<= 1;
-  unsigned long long* sk =
-      (!a.presorted && (P2 <= a.smem_cap || a.gscratch == nullptr)) ? sk_smem : a.gscratch;
-  for (int i = tid; i < P2 && !a.presorted; i += blockDim.x) {
+  constexpr int RCAP = RB_RADIX_THREADS * RB_RADIX_ITEMS;
+  constexpr int RTS = (int)((sizeof(typename RbRadix::TempStorage) + 7) / 8);
+  unsigned long long* sk;
+  if (a.presorted) {
+    // ordered by the grid: bring them on chip when they fit (the next-fit
+    // walk below makes dependent accesses)
+    if (L <= a.smem_cap) {
+      for (int i = tid; i < L; i += nth) sk_smem[i] = a.gscratch[i];
+      sk = sk_smem;
+    } else {
+      sk = a.gscratch;
+    }
+  } else if (L <= nth && L <= RB_RANK_MAX && a.smem_cap >= 2 * RB_RANK_MAX) {
+    // small sets: rank = #smaller keys, one key per thread, the others read
+    // as shared-memory broadcasts (a sorting network or radix passes cost a
+    // fixed 10-30 us here whatever L is)
+    unsigned long long* tmp = sk_smem + RB_RANK_MAX;
     unsigned long long key = ~0ull;
-    if (i < L) {
-      const int v = a.evict[i];
+    if (tid < L) {
+      const int v = a.evict[tid];
       const unsigned long long grp =
           (unsigned long long)a.opidx[a.parts[v]] * (unsigned)a.nb + (unsigned)a.rkey[v];
       key = (grp << 32) | (unsigned)v;
+      tmp[tid] = key;
     }
-    sk[i] = key;
-  }
-  __syncthreads();
-  for (int size = 2; size <= P2 && !a.presorted; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = tid; i < P2; i += blockDim.x) {
-        const int j = i ^ stride;
-        if (j > i) {
-          const bool asc = (i & size) == 0;
-          const unsigned long long x = sk[i], y = sk[j];
-          if ((x > y) == asc) {
-            sk[i] = y;
-            sk[j] = x;
+    __syncthreads();
+    if (tid < ((L + 31) & ~31)) {
+      int r = 0;
+#pragma unroll 8
+      for (int j = 0; j < L; ++j) r += tmp[j] < key;
+      if (tid < L) sk_smem[r] = key;
+    }
+    sk = sk_smem;
+  } else if (nth == RB_RADIX_THREADS && L <= RCAP && a.smem_cap >= RCAP + RTS) {
+    // block radix sort of (group, id) over the bits actually used: ~5x
+    // faster than the bitonic network below at 2048 keys
+    __shared__ unsigned s_gmax, s_vmax;
+    if (tid == 0) s_gmax = s_vmax = 0;
+    __syncthreads();
+    unsigned gg[RB_RADIX_ITEMS], vv[RB_RADIX_ITEMS];
+    unsigned gm = 0, vm = 0;
+#pragma unroll
+    for (int j = 0; j < RB_RADIX_ITEMS; ++j) {
+      const int i = tid * RB_RADIX_ITEMS + j;
+      gg[j] = vv[j] = 0;
+      if (i < L) {
+        const int v = a.evict[i];
+        vv[j] = (unsigned)v;
+        gg[j] = (unsigned)a.opidx[a.parts[v]] * (unsigned)a.nb + (unsigned)a.rkey[v];
+        gm = max(gm, gg[j]);
+        vm = max(vm, vv[j]);
+      }
+    }
+    gm = __reduce_max_sync(0xffffffffu, gm);
+    vm = __reduce_max_sync(0xffffffffu, vm);
+    if ((tid & 31) == 0) {
+      atomicMax(&s_gmax, gm);
+      atomicMax(&s_vmax, vm);
+    }
+    __syncthreads();
+    const int vb = max(1, 32 - __clz((int)s_vmax)), gb = 32 - __clz((int)s_gmax);
+    unsigned long long kk[RB_RADIX_ITEMS];
+#pragma unroll
+    for (int j = 0; j < RB_RADIX_ITEMS; ++j)
+      kk[j] = tid * RB_RADIX_ITEMS + j < L ? ((unsigned long long)gg[j] << vb) | vv[j] : ~0ull;
+    auto& ts = *reinterpret_cast<typename RbRadix::TempStorage*>(sk_smem + RCAP);
+#ifdef RB_TAIL_MERGE
+    RbRadix(ts).Sort(kk, RbLess());
+#else
+    RbRadix(ts).Sort(kk, 0, vb + gb);
+#endif
+    const unsigned long long vmask = (1ull << vb) - 1;
+#pragma unroll
+    for (int j = 0; j < RB_RADIX_ITEMS; ++j) sk_smem[tid * RB_RADIX_ITEMS + j] = kk[j] & vmask;
+    sk = sk_smem;
+    __syncthreads();
+  } else {
+    sk = (P2 <= a.smem_cap || a.gscratch == nullptr) ? sk_smem : a.gscratch;
+    for (int i = tid; i < P2; i += nth) {
+      unsigned long long key = ~0ull;
+      if (i < L) {
+        const int v = a.evict[i];
+        const unsigned long long grp =
+            (unsigned long long)a.opidx[a.parts[v]] * (unsigned)a.nb + (unsigned)a.rkey[v];
+        key = (grp << 32) | (unsigned)v;
+      }
+      sk[i] = key;
+    }
+    __syncthreads();
+    for (int size = 2; size <= P2; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = tid; i < P2; i += nth) {
+          const int j = i ^ stride;
+          if (j > i) {
+            const bool asc = (i & size) == 0;
+            const unsigned long long x = sk[i], y = sk[j];
+            if ((x > y) == asc) {
+              sk[i] = y;
+              sk[j] = x;
+            }
           }
         }
+        __syncthreads();
       }
-      __syncthreads();
     }
-  }
-  if (!a.strong) {
-    // warp-aggregated appends: one atomic per warp and tier, not per move
-    const int lim = (L + 31) & ~31;
-    for (int i = tid; i < lim; i += blockDim.x) {
-      int v = 0, t = -1;
-      if (i < L) {
-        v = (int)(sk[i] & 0xffffffffu);
-        a.mv[v] = a.valid_list[a.draws[i]];
-        t = a.tm(a.offs[v + 1] - a.offs[v]);
-      }
-      for (int tt = 0; tt < NBINS; ++tt)
-        warp_append(t == tt, v, a.move_lists + a.mseg.b[tt], a.move_cnt + tt);
-    }
-    return;
-  }
-  // next-fit; sequential over runs but each run is a parallel prefix test
-  if (tid == 0) {
-    s_di = 0;
-    s_room = a.nvalid > 0 ? a.spare[0] : 0;
-    s_done = a.nvalid <= 0;
   }
   __syncthreads();
-  for (int base = 0; base < L; base += blockDim.x) {
-    const int i = base + tid;
-    const long long w = i < L ? (long long)a.vw[(int)(sk[i] & 0xffffffffu)] : 0;
-    // block inclusive scan of w
-    long long ps = w;
+  // from here sk[i] (low 32 bits) = the i-th evicted vertex in key order;
+  // each path leaves sk[i] = (dest + 1) << 32 | v for i < s_end (0: no move)
+  __shared__ int s_end, s_wide;
+  __shared__ unsigned long long s_ws[33];
+  if (!a.strong) {
+    for (int i = tid; i < L; i += nth) {
+      const unsigned v = (unsigned)(sk[i] & 0xffffffffu);
+      sk[i] = ((unsigned long long)(unsigned)(a.valid_list[a.draws[i]] + 1) << 32) | v;
+    }
+    if (tid == 0) s_end = L;
+  } else {
+    // next-fit (rebalance.py:228-236). The block packs (inclusive prefix of
+    // the sorted weights, id) into the keys; one warp then finds each part's
+    // segment [start, e) by a 32-ary search for the first prefix above
+    // start's prefix + the part's spare, and the next part by a ballot over a
+    // register window of spare[] -- a few steps per part switch, nothing per
+    // item. (A block-wide round per switch cost 30-40 us per strong pass.)
+    for (int i = tid; i < L; i += nth) {
+      const unsigned v = (unsigned)(sk[i] & 0xffffffffu);
+      sk[i] = ((unsigned long long)(unsigned)a.vw[v] << 32) | v;
+    }
+    __syncthreads();
+    const int ipt = (L + nth - 1) / nth;
+    const int lo = min(L, tid * ipt), hi = min(L, lo + ipt);
+    unsigned long long run = 0;
+    for (int i = lo; i < hi; ++i) run += sk[i] >> 32;
+    unsigned long long x = run;
+    const int lane = tid & 31, wid = tid >> 5;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const long long y = __shfl_up_sync(0xffffffffu, ps, o);
-      if ((tid & 31) >= o) ps += y;
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-    if ((tid & 31) == 31) s_wsum[tid >> 5] = ps;
+    if (lane == 31) s_ws[wid] = x;
     __syncthreads();
     if (tid < 32) {
-      long long x = s_wsum[tid];
+      unsigned long long t = tid < ((nth + 31) >> 5) ? s_ws[tid] : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const long long y = __shfl_up_sync(0xffffffffu, x, o);
-        if (tid >= o) x += y;
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, t, o);
+        if (tid >= o) t += y;
       }
-      s_wsum[tid] = x;
+      s_ws[tid] = t;
+      if (tid == 31) s_wide = t >= (1ull << 32);
     }
     __syncthreads();
-    if (tid >= 32) ps += s_wsum[(tid >> 5) - 1];
-    const int lim = L - base < (int)blockDim.x ? L - base : (int)blockDim.x;
-    // stash inclusive sums in the (already consumed) key slots' upper half:
-    // keep them in a dedicated region after the keys instead
-    long long* pbuf = reinterpret_cast<long long*>(sk + P2);
-    pbuf[tid] = ps;
-    __syncthreads();
-    int pos = 0;
-    long long before = 0;
-    while (true) {
-      if (s_done) break;
-      const long long room = s_room;
-      const bool fits = tid >= pos && tid < lim && ps - before <= room;
-      __shared__ int s_first;
-      if (tid == 0) s_first = lim;
-      __syncthreads();
-      if (tid >= pos && tid < lim && !fits) atomicMin(&s_first, tid);
-      __syncthreads();
-      const int e = s_first;
-      {
-        int v = 0, t = -1;
-        if (fits) {
-          v = (int)(sk[i] & 0xffffffffu);
-          a.mv[v] = a.valid_list[s_di];
-          t = a.tm(a.offs[v + 1] - a.offs[v]);
-        }
-        for (int tt = 0; tt < NBINS; ++tt)
-          warp_append(t == tt, v, a.move_lists + a.mseg.b[tt], a.move_cnt + tt);
+    const bool wide = s_wide;
+    if (!wide) {
+      unsigned long long pre = x - run + (wid ? s_ws[wid - 1] : 0);
+      for (int i = lo; i < hi; ++i) {
+        const unsigned long long k = sk[i];
+        pre += k >> 32;
+        sk[i] = (pre << 32) | (k & 0xffffffffu);
       }
-      __syncthreads();
-      if (e >= lim) {
-        if (tid == 0) s_room = room - (pbuf[lim - 1] - before);
-        __syncthreads();
-        break;
-      }
-      if (tid == 0) {
-        const long long prev = e > 0 ? pbuf[e - 1] : 0;
-        long long r = room - (prev - before);
-        const long long we = pbuf[e] - prev;
-        int di = s_di;
-        while (di < a.nvalid && r < we) {
-          di++;
-          r = di < a.nvalid ? a.spare[di] : 0;
-        }
-        s_di = di;
-        s_room = r;
-        if (di >= a.nvalid) s_done = 1;
-      }
-      __syncthreads();
-      pos = e;
-      before = e > 0 ? pbuf[e - 1] : 0;
     }
     __syncthreads();
-    if (s_done) break;
+    if (tid < 32) {
+      const int nvalid = a.nvalid;
+      int wb = 0;  // window of parts [wb, wb + 32) in registers
+      long long wsp = lane < nvalid ? a.spare[lane] : 0;
+      int wvl = lane < nvalid ? a.valid_list[lane] : -1;
+      int di = 0, end = nvalid > 0 ? L : 0;
+      // first later part whose whole spare holds weight we (the reference's
+      // `while r < w: di += 1; r = spare[di]`); returns false past the last
+      auto advance = [&](long long we) {
+        ++di;
+        while (di < nvalid) {
+          if (di >= wb + 32) {
+            wb = di;
+            wsp = wb + lane < nvalid ? a.spare[wb + lane] : 0;
+            wvl = wb + lane < nvalid ? a.valid_list[wb + lane] : -1;
+          }
+          const unsigned ok =
+              __ballot_sync(0xffffffffu, lane >= di - wb && wb + lane < nvalid && wsp >= we);
+          if (ok) {
+            di = wb + __ffs(ok) - 1;
+            return true;
+          }
+          di = wb + 32;
+        }
+        return false;
+      };
+      if (!wide) {
+        auto S = [&](int i) -> long long { return (long long)(sk[i] >> 32); };
+        int start = 0;
+        long long sbase = 0;  // prefix before `start`
+        while (nvalid > 0) {
+          const int dest = __shfl_sync(0xffffffffu, wvl, di - wb);
+          const long long room = __shfl_sync(0xffffffffu, wsp, di - wb);
+          // e = first index >= start whose item does not fit: S(e) - sbase > room
+          int lo2 = start, hi2 = L;
+          while (lo2 < hi2) {
+            const int step = (hi2 - lo2 + 31) >> 5;
+            const int q = lo2 + lane * step;
+            const unsigned bb = __ballot_sync(0xffffffffu, q >= hi2 || S(q) - sbase > room);
+            if (!bb) {
+              lo2 += 31 * step + 1;
+              continue;
+            }
+            const int j = __ffs(bb) - 1;
+            if (j == 0) {
+              hi2 = lo2;
+            } else {
+              hi2 = min(hi2, lo2 + j * step);
+              lo2 += (j - 1) * step + 1;
+            }
+          }
+          const int e = lo2;
+          const long long prev = e > start ? S(e - 1) : sbase;
+          const long long we = e < L ? S(e) - prev : 0;
+          __syncwarp();
+          for (int i = start + lane; i < e; i += 32)
+            sk[i] = ((unsigned long long)(unsigned)(dest + 1) << 32) | (sk[i] & 0xffffffffu);
+          if (e >= L) break;
+          if (!advance(we)) {
+            end = e;
+            break;
+          }
+          start = e;
+          sbase = prev;
+        }
+      } else {
+        // totals >= 2^32: walk the weights 32 items at a time
+        long long room = nvalid > 0 ? __shfl_sync(0xffffffffu, wsp, 0) : 0;
+        bool done = nvalid <= 0;
+        for (int base = 0; base < L && !done; base += 32) {
+          const int i = base + lane;
+          const int lim = L - base < 32 ? L - base : 32;
+          const unsigned long long k = i < L ? sk[i] : 0;
+          long long incl = (long long)(k >> 32);
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          int dest = -1, pos = 0;
+          long long before = 0;
+          while (true) {
+            const bool live = lane >= pos && lane < lim;
+            const bool fits = live && incl - before <= room;
+            const int dv = __shfl_sync(0xffffffffu, wvl, di - wb);
+            if (fits) dest = dv;
+            const unsigned m = __ballot_sync(0xffffffffu, live && !fits);
+            if (!m) {
+              room -= __shfl_sync(0xffffffffu, incl, lim - 1) - before;
+              break;
+            }
+            const int e = __ffs(m) - 1;
+            const long long prev = e > 0 ? __shfl_sync(0xffffffffu, incl, e - 1) : 0;
+            const long long we = __shfl_sync(0xffffffffu, incl, e) - prev;
+            if (!advance(we)) {
+              done = true;
+              end = base + lim;
+              break;
+            }
+            room = __shfl_sync(0xffffffffu, wsp, di - wb);
+            pos = e;
+            before = prev;
+          }
+          if (lane < lim)
+            sk[i] = (dest >= 0 ? (unsigned long long)(unsigned)(dest + 1) << 32 : 0ull) |
+                    (k & 0xffffffffu);
+        }
+      }
+      if (lane == 0) s_end = end;
+    }
+  }
+  // commit: mv[] and the per-tier move lists, one global atomic per tier
+  __shared__ unsigned s_tc[NBINS];
+  __shared__ unsigned long long s_tb[NBINS];
+  if (tid < NBINS) s_tc[tid] = 0;
+  __syncthreads();
+  const int end = s_end;
+  const int lim = (end + 31) & ~31;
+  for (int i = tid; i < lim; i += nth) {
+    int t = -1;
+    if (i < end) {
+      const unsigned long long k = sk[i];
+      const unsigned v = (unsigned)(k & 0xffffffffu);
+      if (k >> 32) {
+        a.mv[v] = (int)(k >> 32) - 1;
+        t = a.tm(a.offs[v + 1] - a.offs[v]);
+        sk[i] = ((unsigned long long)(unsigned)(t + 1) << 32) | v;
+      }
+    }
+    smem_warp_slot(s_tc, t);
+  }
+  __syncthreads();
+  if (tid < NBINS) {
+    s_tb[tid] = s_tc[tid] ? atomicAdd(a.move_cnt + tid, (unsigned long long)s_tc[tid]) : 0;
+    s_tc[tid] = 0;
+  }
+  __syncthreads();
+  for (int i = tid; i < lim; i += nth) {
+    int t = -1;
+    unsigned v = 0;
+    if (i < end) {
+      const unsigned long long k = sk[i];
+      v = (unsigned)(k & 0xffffffffu);
+      t = (int)(k >> 32) - 1;
+    }
+    const unsigned pos = smem_warp_slot(s_tc, t);
+    if (t >= 0) a.move_lists[a.mseg.b[t] + s_tb[t] + pos] = (int32_t)v;
   }
 }
 
