@@ -351,19 +351,17 @@ __device__ void lv_bookkeep(const LevelArgs& A, const unsigned long long* P) {
 }
 
 // ---------------------------------------------------------- rebalancing
-__device__ void lv_draws(const LevelArgs& A, int64_t t0, int64_t nt) {
+__device__ void lv_draws(const LevelArgs& A, const LevelCtl& S, int64_t t0, int64_t nt) {
   LevelCtl* C = A.C;
-  const int nvalid = ldv(&C->nvalid);
-  const int64_t D = (int64_t)*(const volatile long long*)&C->max_evict;
+  const int nvalid = S.nvalid;
+  const int64_t D = S.max_evict;
   if (nvalid <= 1) {  // integers(0, 1) returns 0 without drawing
     for (int64_t j = t0; j < D; j += nt) A.draws[j] = 0;
     return;
   }
   DevPcg g;
-  g.state = ((du128)*(const volatile unsigned long long*)&C->pcg_state_hi << 64) |
-            *(const volatile unsigned long long*)&C->pcg_state_lo;
-  g.inc = ((du128)*(const volatile unsigned long long*)&C->pcg_inc_hi << 64) |
-          *(const volatile unsigned long long*)&C->pcg_inc_lo;
+  g.state = ((du128)S.pcg_state_hi << 64) | S.pcg_state_lo;
+  g.inc = ((du128)S.pcg_inc_hi << 64) | S.pcg_inc_lo;
   const uint32_t excl = (uint32_t)nvalid, thr = (0xffffffffu - (uint32_t)(nvalid - 1)) % excl;
   // words [D, D + slack) are only screened: a rejection before D shifts the
   // stream onto them
@@ -380,16 +378,14 @@ __device__ void lv_draws(const LevelArgs& A, int64_t t0, int64_t nt) {
 // Rejected words are skipped by numpy's Lemire loop, so draw j is the word
 // at the (j+1)-th accepted position: w = j + #{rejected q <= w} (fixed point,
 // at most #rejections + 1 steps). Parallel over the draws.
-__device__ void lv_draws_fix_parallel(const LevelArgs& A, int64_t t0, int64_t nt) {
+__device__ void lv_draws_fix_parallel(const LevelArgs& A, const LevelCtl& S, int R, int64_t t0,
+                                      int64_t nt) {
   LevelCtl* C = A.C;
-  const int R = (int)*(const volatile unsigned long long*)&C->rejects;
-  const int64_t D = (int64_t)*(const volatile long long*)&C->max_evict;
-  const int nvalid = ldv(&C->nvalid);
+  const int64_t D = S.max_evict;
+  const int nvalid = S.nvalid;
   DevPcg g;
-  g.state = ((du128)*(const volatile unsigned long long*)&C->pcg_state_hi << 64) |
-            *(const volatile unsigned long long*)&C->pcg_state_lo;
-  g.inc = ((du128)*(const volatile unsigned long long*)&C->pcg_inc_hi << 64) |
-          *(const volatile unsigned long long*)&C->pcg_inc_lo;
+  g.state = ((du128)S.pcg_state_hi << 64) | S.pcg_state_lo;
+  g.inc = ((du128)S.pcg_inc_hi << 64) | S.pcg_inc_lo;
   long long qmin = LLONG_MAX;
   for (int r = 0; r < R; ++r) qmin = min(qmin, *(const volatile long long*)&C->rej_pos[r]);
   for (int64_t j = t0; j < D; j += nt) {
@@ -416,9 +412,8 @@ __device__ void lv_draws_fixup(const LevelArgs& A) {
   for (int64_t j = 0; j < D; ++j) A.draws[j] = (int32_t)s.below((uint32_t)C->nvalid);
 }
 
-__device__ RbSel lv_sel(const LevelArgs& A) {
-  const LevelCtl* C = A.C;
-  return RbSel{A.parts, A.g.vw, A.opidx, A.rkey, A.bstar, A.thr, ldv(&C->rho), ldv(&C->nch), A.CH};
+__device__ RbSel lv_sel(const LevelArgs& A, const LevelCtl& S) {
+  return RbSel{A.parts, A.g.vw, A.opidx, A.rkey, A.bstar, A.thr, S.rho, S.nch, A.CH};
 }
 
 // per-warp staging words of the short-row sweeps (largest tier variant)
@@ -551,10 +546,10 @@ __device__ void lv_grid_sort(const LevelArgs& A, int L, int P2, int nb, unsigned
 // large for the quadratic in-segment ranking; the caller then sorts.
 constexpr int LV_TAIL_GROUP_MAX = 512;
 template <class GSync>
-__device__ bool lv_tail_rank(const LevelArgs& A, int L, int nb, GSync gsync, int64_t t0,
+__device__ bool lv_tail_rank(const LevelArgs& A, int L, int nover, int nb, GSync gsync, int64_t t0,
                              int64_t nt) {
   LevelCtl* C = A.C;
-  const int G = ldv(&C->nover) * nb;
+  const int G = nover * nb;
   unsigned* hist = A.tailbuf;
   unsigned* base = hist + G;      // per-block exclusive prefix, G
   unsigned* fill = base + G;      // G
@@ -675,18 +670,33 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
   // fewer. The part weights (A.ctr + CTR_PW) are not per pass.
   if (blockIdx.x == 0) lv_decide(A, A.ctr);  // pass_index 0 -> A.ctr
   gsync();
+  // control words of the pass, read once per block (every warp reading them
+  // from L2 puts thousands of requests on one line per phase)
+  __shared__ LevelCtl s_ctl;
+  __shared__ unsigned long long s_bcast[2];
+  const LevelCtl& S = s_ctl;
   while (true) {
     pc.mark(0);
-    const int kind = ldv(&C->kind);
+    {
+      constexpr int W0 = (int)(offsetof(LevelCtl, rej_pos) / 4);
+      constexpr int WP = (int)(offsetof(LevelCtl, pcg_state_hi) / 4);
+      static_assert(W0 <= LV_BLOCK && sizeof(LevelCtl) / 4 - WP == 8, "LevelCtl layout");
+      const unsigned* src = reinterpret_cast<const unsigned*>(C);
+      unsigned* dst = reinterpret_cast<unsigned*>(&s_ctl);
+      if ((int)threadIdx.x < W0) dst[threadIdx.x] = __ldcg(src + threadIdx.x);
+      else if ((int)threadIdx.x < W0 + 8) dst[WP + threadIdx.x - W0] = __ldcg(src + WP + threadIdx.x - W0);
+      __syncthreads();
+    }
+    const int kind = S.kind;
     pc.kind = kind;
     if (kind == 0) break;
-    const int pass = ldv(&C->pass_index);
+    const int pass = S.pass_index;
     unsigned long long* P = (pass & 1) ? A.ctr2 : A.ctr;
     cands.cnt = P + CTR_CAND;
     moves.cnt = P + CTR_MOVE;
     // the previous pass's state became the kept one: copy it while this
     // pass's first phase runs (only the commit phase writes parts)
-    if (ldv(&C->copy_keep))
+    if (S.copy_keep)
       for (int64_t v = t0; v < A.n; v += nt) A.keep[v] = A.parts[v];
     long long acc = 0;
     if (kind == 1) {
@@ -698,7 +708,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       lp.c_use_float = A.c_float;
       lp.afterburner = A.afterburner;
       lp.locking = A.locking;
-      lp.lock_epoch = ldv(&C->epoch);
+      lp.lock_epoch = S.epoch;
       auto mk = [&](int t) {
         LpOp::Args a{};
         a.parts = A.parts;
@@ -733,11 +743,12 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
     } else {
       // ---- weak / strong rebalancing (rebalance.py:139-240)
       const int strong = kind == 3;
-      const int nover = ldv(&C->nover), nb = ldv(&C->nb), nch = ldv(&C->nch);
+      const int nover = S.nover, nb = S.nb, nch = S.nch;
       for (int64_t i = t0; i < (int64_t)nover * nb; i += nt) A.H[i] = 0;
-      for (int64_t i = t0; i < (int64_t)nover * (nb / ldv(&C->rho)); i += nt) A.Hs[i] = 0;
+      for (int64_t i = t0; i < (int64_t)nover * (nb / S.rho); i += nt) A.Hs[i] = 0;
       for (int64_t i = t0; i < (int64_t)nover * nch; i += nt) A.CH[i] = 0;
-      if (!strong) lv_draws(A, t0, nt);
+      if (!strong) lv_draws(A, S, t0, nt);
+      pc.mark(14);
       rb_collect(A.parts, A.opidx, A.g.offs, A.tm, A.n, A.cand_lists, A.seg, P + CTR_CAND, t0, nt,
                  &wk.v[0], &wk.v[1]);
       gsync();
@@ -748,10 +759,10 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       ra.opidx = A.opidx;
       ra.valid = A.valid;
       ra.hb = A.hb;
-      ra.nvalid = ldv(&C->nvalid);
+      ra.nvalid = S.nvalid;
       ra.strong = strong;
-      ra.rho = ldv(&C->rho);
-      ra.slot_min = ldv(&C->slot_min);
+      ra.rho = S.rho;
+      ra.slot_min = S.slot_min;
       ra.nb = nb;
       ra.rkey = A.rkey;
       ra.rbest = A.rbest;
@@ -764,9 +775,9 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
                            acc);
       gsync();
       pc.mark(4);
-      const RbSel s = lv_sel(A);
+      const RbSel s = lv_sel(A, S);
       for (int64_t op = w0; op < nover; op += nw)
-        rb_scan_warp((int)op, A.H, A.Hs, nb, ldv(&C->rho), A.deficit, A.bstar, A.cum_before);
+        rb_scan_warp((int)op, A.H, A.Hs, nb, S.rho, A.deficit, A.bstar, A.cum_before);
       gsync();
       pc.mark(5);
       rb_chunk(s, A.rcand, P + CTR_RCAND, t0, nt);
@@ -780,14 +791,20 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
                 A.mv, A.g.offs, A.tm, A.move_lists, A.seg, P + CTR_MOVE, t0, nt);
       gsync();
       pc.mark(8);
-      const int Lev = (int)*(const volatile unsigned long long*)(P + CTR_EVICT);
+      if (threadIdx.x == 0) {
+        s_bcast[0] = __ldcg(P + CTR_EVICT);
+        s_bcast[1] = strong ? 0ull : __ldcg(&C->rejects);
+      }
+      __syncthreads();
+      const int Lev = (int)s_bcast[0];
+      const unsigned long long rejects = s_bcast[1];
       int P2ev = 1;
       while (P2ev < Lev) P2ev <<= 1;
-      if (!strong && *(const volatile unsigned long long*)&C->rejects) {
+      if (!strong && rejects) {
         // a Lemire rejection shifted the draw stream: re-derive the draws
         // (in parallel; sequentially only past 32 rejections)
-        if (*(const volatile unsigned long long*)&C->rejects <= 32)
-          lv_draws_fix_parallel(A, t0, nt);
+        if (rejects <= 32)
+          lv_draws_fix_parallel(A, S, (int)rejects, t0, nt);
         else if (blockIdx.x == 0 && threadIdx.x == 0)
           lv_draws_fixup(A);
         gsync();
@@ -796,11 +813,11 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       // large evicted sets: order them with the whole grid, and for weak
       // passes assign the random destinations with the whole grid too
       const bool big_tail = P2ev > A.tail_grid_min;
-      if (big_tail && !lv_tail_rank(A, Lev, nb, gsync, t0, nt))
+      if (big_tail && !lv_tail_rank(A, Lev, nover, nb, gsync, t0, nt))
         lv_grid_sort(A, Lev, P2ev, nb, lv_smem, gsync, t0, nt);
       pc.mark(12);
       if (big_tail && !strong) {
-        const int nvalid = ldv(&C->nvalid);
+        const int nvalid = S.nvalid;
         const int64_t lim = ((int64_t)Lev + 31) & ~31LL;
         for (int64_t i = t0; i < lim; i += nt) {
           int v = 0, t = -1;
@@ -825,7 +842,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
         tl.valid_list = A.valid_list;
         tl.draws = A.draws;
         tl.spare = A.spare;
-        tl.nvalid = ldv(&C->nvalid);
+        tl.nvalid = S.nvalid;
         tl.nb = nb;
         tl.strong = strong;
         tl.mv = A.mv;
@@ -855,7 +872,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       ca.parts = A.parts;
       ca.mv = A.mv;
       ca.lock = A.lock;
-      ca.epoch = ldv(&C->new_epoch);
+      ca.epoch = S.new_epoch;
       ca.set_lock = kind == 1 && A.locking;
       const SegLists& ml = (kind == 1 && A.afterburner) ? cands : moves;
       for (int t = 0; t < NBINS; ++t) ca.lists[t] = ml.list[t];
@@ -872,7 +889,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
   }
   // the returned state is the best balanced one, or the fallback; when the
   // last pass made the kept state, parts already is it
-  if (!ldv(&C->copy_keep))
+  if (!S.copy_keep)
     for (int64_t v = t0; v < A.n; v += nt) A.parts[v] = A.keep[v];
   for (int i = 0; i < 6; ++i) block_sum_atomic_any((long long)wk.v[i], A.work + i);
 }
@@ -1084,7 +1101,7 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
     c.sync();
     static const char* names[16] = {"decide", "lp_sweep", "afterburner", "rb_collect", "rb_stats",
                                     "rb_scan", "rb_chunk", "rb_find", "rb_select", "rb_tail",
-                                    "apply_delta", "commit+keep", "tail_sort", "draw_fixup", "", "keep_copy"};
+                                    "apply_delta", "commit+keep", "tail_sort", "draw_fixup", "rb_prep", "keep_copy"};
     static const char* kinds[4] = {"stop", "lp", "weak", "strong"};
     const int cnt[4] = {1, h.lp, h.weak, h.strong};
     for (int kd = 1; kd < 4; ++kd) {

@@ -1824,22 +1824,76 @@ static __device__ void rb_tail(const RbTail& a, unsigned long long* sk_smem) {
 
 
 
+// Candidates of the rebalancing passes: the vertices of oversized parts, by
+// degree tier. Blocks take tiles of blockDim * RB_COL_IT consecutive ids
+// (coalesced loads, RB_COL_IT independent per thread) and reserve each
+// tier's output once per tile -- per-warp appends put tens of thousands of
+// same-address atomics on the six counters every pass. All threads of the
+// block must call it.
+constexpr int RB_COL_IT = 8;
 static __device__ void rb_collect(const int32_t* __restrict__ parts, const int32_t* __restrict__ opidx,
                            const int64_t* __restrict__ offs, TierMap tm, int64_t n, int32_t* lists,
-                           RbSegsDev seg, unsigned long long* cnts, int64_t t0, int64_t stride,
+                           RbSegsDev seg, unsigned long long* cnts, int64_t /*t0*/, int64_t /*stride*/,
                            unsigned long long* pwr = nullptr, unsigned long long* pwe = nullptr) {
-  const int64_t lim = (n + 31) / 32 * 32;
+  __shared__ unsigned s_wc[NBINS][32];
+  __shared__ unsigned long long s_base[NBINS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t tile = (int64_t)blockDim.x * RB_COL_IT;
   unsigned long long wr = 0, we = 0;
-  for (int64_t v = t0; v < lim; v += stride) {
-    int t = -1;
-    if (v < n && opidx[parts[v]] >= 0) {
-      const int64_t d = offs[v + 1] - offs[v];
-      t = tm(d);
-      wr += 1;
-      we += (unsigned long long)d;
+  for (int64_t b0 = blockIdx.x * tile; b0 < n; b0 += (int64_t)gridDim.x * tile) {
+    const int64_t wbase = b0 + (int64_t)w * 32 * RB_COL_IT;
+    int tv[RB_COL_IT];
+#pragma unroll
+    for (int j = 0; j < RB_COL_IT; ++j) {
+      const int64_t v = wbase + j * 32 + lane;
+      int t = -1;
+      if (v < n && opidx[parts[v]] >= 0) {
+        const int64_t d = offs[v + 1] - offs[v];
+        t = tm(d);
+        wr += 1;
+        we += (unsigned long long)d;
+      }
+      tv[j] = t;
     }
-    if (__ballot_sync(0xffffffffu, t >= 0) == 0) continue;
-    for (int tt = 0; tt < NBINS; ++tt) warp_append(t == tt, (int32_t)v, lists + seg.b[tt], cnts + tt);
+    unsigned c[NBINS];
+#pragma unroll
+    for (int tt = 0; tt < NBINS; ++tt) {
+      c[tt] = 0;
+#pragma unroll
+      for (int j = 0; j < RB_COL_IT; ++j) c[tt] += __popc(__ballot_sync(0xffffffffu, tv[j] == tt));
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int tt = 0; tt < NBINS; ++tt) s_wc[tt][w] = c[tt];
+    __syncthreads();
+    if (w < NBINS) {  // warp w: exclusive scan of tier w over the warps, one reservation
+      const unsigned x = lane < nw ? s_wc[w][lane] : 0u;
+      unsigned inc = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const unsigned tot = __shfl_sync(0xffffffffu, inc, 31);
+      if (lane < nw) s_wc[w][lane] = inc - x;
+      if (lane == 0) s_base[w] = tot ? atomicAdd(cnts + w, (unsigned long long)tot) : 0ull;
+    }
+    __syncthreads();
+    unsigned long long off[NBINS];
+#pragma unroll
+    for (int tt = 0; tt < NBINS; ++tt) off[tt] = seg.b[tt] + s_base[tt] + s_wc[tt][w];
+#pragma unroll
+    for (int j = 0; j < RB_COL_IT; ++j) {
+      const int t = tv[j];
+#pragma unroll
+      for (int tt = 0; tt < NBINS; ++tt) {
+        const unsigned m = __ballot_sync(0xffffffffu, t == tt);
+        if (t == tt) lists[off[tt] + __popc(m & lt)] = (int32_t)(wbase + j * 32 + lane);
+        off[tt] += __popc(m);
+      }
+    }
+    __syncthreads();  // s_wc / s_base are rewritten by the next tile
   }
   if (pwr) {  // candidate rows / entries: the stats sweep visits exactly these
     *pwr += wr;
