@@ -783,8 +783,14 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       rb_chunk(s, A.rcand, P + CTR_RCAND, t0, nt);
       gsync();
       pc.mark(6);
-      for (int64_t op = w0; op < nover; op += nw)
-        rb_find_warp((int)op, s, A.deficit, A.required, A.cum_before, A.opart, A.n, nb, A.thr);
+      if ((int)gridDim.x >= nover && nch > 512) {  // long chunk rows: a block per part
+        if ((int)blockIdx.x < nover)
+          rb_find_block<LV_BLOCK>((int)blockIdx.x, s, A.deficit, A.required, A.cum_before, A.opart,
+                                  A.n, nb, A.thr);
+      } else {
+        for (int64_t op = w0; op < nover; op += nw)
+          rb_find_warp((int)op, s, A.deficit, A.required, A.cum_before, A.opart, A.n, nb, A.thr);
+      }
       gsync();
       pc.mark(7);
       rb_select(s, A.rcand, P + CTR_RCAND, A.rbest, strong, 1, A.evict, P + CTR_EVICT,

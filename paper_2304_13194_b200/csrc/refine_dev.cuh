@@ -1265,8 +1265,15 @@ static __device__ __forceinline__ int warp_cross(const unsigned long long* __res
   const int seg = (len + 31) / 32;
   const int b = min(len, lane * seg), e = min(len, b + seg);
   long long sm = 0;
-#pragma unroll 4
-  for (int i = b; i < e; ++i) sm += (long long)arr[i];
+  int i = b;
+  for (; i + 8 <= e; i += 8) {  // 8 independent loads in flight per lane
+    unsigned long long x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = __ldcg(arr + i + u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) sm += (long long)x[u];
+  }
+  for (; i < e; ++i) sm += (long long)__ldcg(arr + i);
   long long incl = sm;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -1351,6 +1358,86 @@ static __device__ void rb_find_warp(int op, const RbSel& s, const long long* __r
     thr[op] = (int)v64 + (include ? 1 : 0);
   }
   if (!m && lane == 0) thr[op] = 0x7fffffff;  // unreachable by construction
+}
+
+// rb_find_warp with a whole block per part (level kernel, grid >= parts):
+// every thread sums a contiguous run of chunk totals with independent loads,
+// one block scan locates the crossing run, its thread walks it.
+template <int BSZ>
+static __device__ void rb_find_block(int op, const RbSel& s, const long long* __restrict__ deficit,
+                                     const long long* __restrict__ required,
+                                     const long long* __restrict__ cum_before,
+                                     const int32_t* __restrict__ opart, int64_t n, int nb,
+                                     int32_t* thr) {
+  typedef cub::BlockScan<long long, BSZ> BS;
+  __shared__ typename BS::TempStorage ts;
+  __shared__ int s_ch;
+  __shared__ long long s_cb;
+  const int bs = s.bstar[op];
+  if (bs >= nb) {
+    if (threadIdx.x == 0) thr[op] = 0x7fffffff;
+    return;
+  }
+  const long long D = deficit[op];
+  const long long base = cum_before[op];
+  const unsigned long long* chs = s.CH + (size_t)op * s.nch;
+  const int per = (s.nch + BSZ - 1) / BSZ;
+  const int b = min(s.nch, (int)threadIdx.x * per), e = min(s.nch, b + per);
+  long long sm = 0;
+  int i = b;
+  for (; i + 4 <= e; i += 4) {
+    unsigned long long x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = __ldcg(chs + i + u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) sm += (long long)x[u];
+  }
+  for (; i < e; ++i) sm += (long long)__ldcg(chs + i);
+  if (threadIdx.x == 0) s_ch = -1;
+  long long ex;
+  BS(ts).ExclusiveSum(sm, ex);
+  __syncthreads();
+  long long run = base + ex;
+  if (b < e && run < D && run + sm >= D) {  // exactly one thread's run crosses
+    for (int j = b; j < e; ++j) {
+      const long long x = (long long)__ldcg(chs + j);
+      if (run + x >= D) {
+        s_ch = j;
+        s_cb = run;
+        break;
+      }
+      run += x;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const int ch = s_ch;
+    const long long cb = s_cb;
+    const int P = opart[op];
+    const int sub = bs % s.rho;
+    const int64_t v64 = ((int64_t)ch * 32 + lane) * s.rho + sub;
+    long long w = 0;
+    if (ch >= 0 && v64 < n) {
+      const int v = (int)v64;
+      if (s.parts[v] == P && s.rkey[v] == bs) w = s.vw[v];
+    }
+    long long incl = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const long long cum = cb + incl;
+    const unsigned m = __ballot_sync(0xffffffffu, w > 0 && cum >= D && cum - w < D);
+    if (m && lane == __ffs(m) - 1) {
+      const long long prev = cum - w;
+      const bool include = (cum - D <= D - prev) || (prev < required[op]);
+      thr[op] = (int)v64 + (include ? 1 : 0);
+    }
+    if (!m && lane == 0) thr[op] = 0x7fffffff;
+  }
+  __syncthreads();
 }
 
 // Sharded form of rb_find_warp: (a) every rank locates the crossing chunk
