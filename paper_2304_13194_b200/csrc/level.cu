@@ -85,6 +85,8 @@ struct LevelArgs {
   unsigned long long* H;
   unsigned long long* Hs;
   unsigned long long* CH;
+  int32_t* ext;        // weighted external degree per vertex (boundary iff > 0)
+  int32_t* blists;     // per-tier boundary rows (segments as cand_lists)
   int32_t* opidx;
   uint8_t* valid;
   int32_t* valid_list;
@@ -664,6 +666,13 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
 
   PhaseClock pc(A.phase_clk);
   WorkAcc wk;
+  // After the first Jetlp sweep of the level has measured every vertex's
+  // external degree, the applied moves keep it current, and later sweeps
+  // visit only boundary rows: an interior row has no destination, adds
+  // nothing to the cut, and its cdest stays -1 (reset after each pass).
+  bool ext_ok = false;
+  const int32_t* blp[NBINS];
+  for (int t = 0; t < NBINS; ++t) blp[t] = A.blists + A.seg.b[t];
   // Per-pass counters alternate between two blocks by pass parity, so block
   // 0 can book-keep pass i and decide pass i+1 (zeroing the other block)
   // while the other blocks still commit pass i: one grid barrier per pass
@@ -720,11 +729,22 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
         a.out_list = (A.afterburner ? A.cand_lists : A.move_lists) + A.seg.b[t];
         a.out_cnt = P + (A.afterburner ? CTR_CAND : CTR_MOVE) + t;
         a.cut2 = P + CTR_CUT2;
+        a.ext = A.ext;
         return a;
       };
+      const bool bnd = ext_ok;
+      if (bnd) {
+        const int32_t* ext = A.ext;
+        collect_tiled([&](int v) { return __ldcg(ext + v) != 0; },
+                      A.g.offs, A.tm, A.n, A.blists, A.seg, P + CTR_BND, nullptr, nullptr);
+        gsync();
+        pc.mark(15);
+      }
       // per-warp tables start at lv_smem + warp * per inside agg_warp
-      lv_sweep<LpOp, UNIT>(A, mk, nullptr, nullptr, lv_smem, w0, nw, acc);
+      lv_sweep<LpOp, UNIT>(A, mk, bnd ? blp : nullptr, bnd ? P + CTR_BND : nullptr, lv_smem, w0,
+                           nw, acc);
       gsync();
+      ext_ok = A.ext != nullptr;
       pc.mark(1);
       if (A.afterburner) {
         AbArgs ab{};
@@ -865,7 +885,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
     }
     // ---- apply (conn.py:215-254)
     {
-      ApArgs ap{A.parts, A.mv, A.ctr + CTR_PW, P + CTR_CUT2D, A.k};
+      ApArgs ap{A.parts, A.mv, A.ctr + CTR_PW, P + CTR_CUT2D, A.k, ext_ok ? A.ext : nullptr};
       long long d = 0;
       apply_delta_rows<UNIT>(ap, A.g, (kind == 1 && A.afterburner) ? cands : moves, w0, nw, d,
                              &wk.v[4], &wk.v[5]);
@@ -883,6 +903,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       const SegLists& ml = (kind == 1 && A.afterburner) ? cands : moves;
       for (int t = 0; t < NBINS; ++t) ca.lists[t] = ml.list[t];
       ca.cnts = ml.cnt;
+      ca.cdest_reset = (kind == 1 && A.afterburner && ext_ok) ? A.cdest : nullptr;
       apply_commit_rows(ca, t0, nt);
     }
     if (blockIdx.x == 0) {
@@ -915,6 +936,8 @@ struct LevelScratch : CtxExt {
   DBuf<unsigned> tailbuf;
   DBuf<unsigned long long> work;
   DBuf<unsigned long long> ctr2;
+  DBuf<int32_t> ext;
+  DBuf<int32_t> blists;
 };
 
 static LevelScratch& level_scratch(Ctx& c) {
@@ -1008,6 +1031,11 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   A.F = w.F.get();
   A.mv = w.mv.get();
   A.lock = w.lock.get();
+  S.ext.ensure(g.n, c.stream);
+  S.blists.ensure(w.cap_n, c.stream);
+  // (external degrees are int32: levels with weighted degrees >= 2^31 sweep in full)
+  A.ext = (getenv("JET_FULL_SWEEPS") || g.max_wdeg >= (1LL << 31)) ? nullptr : S.ext.get();
+  A.blists = S.blists.get();
   A.cand_lists = w.lists.get();
   A.move_lists = w.lists.get() + w.cap_n;
   A.ctr = w.ctr.get();
@@ -1107,7 +1135,7 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
     c.sync();
     static const char* names[16] = {"decide", "lp_sweep", "afterburner", "rb_collect", "rb_stats",
                                     "rb_scan", "rb_chunk", "rb_find", "rb_select", "rb_tail",
-                                    "apply_delta", "commit+keep", "tail_sort", "draw_fixup", "rb_prep", "keep_copy"};
+                                    "apply_delta", "commit+keep", "tail_sort", "draw_fixup", "rb_prep", "bnd_collect"};
     static const char* kinds[4] = {"stop", "lp", "weak", "strong"};
     const int cnt[4] = {1, h.lp, h.weak, h.strong};
     for (int kd = 1; kd < 4; ++kd) {

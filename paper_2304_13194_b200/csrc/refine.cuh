@@ -19,6 +19,7 @@ enum {
   CTR_RCAND = 14,  // rebalance candidates
   CTR_EVICT = 15,  // evicted vertices
   CTR_NMOVE = 16,  // Jetlp moves flagged in place (level kernel)
+  CTR_BND = 17,    // 6 per-tier boundary-row counts (level kernel)
   CTR_PW = 32
 };
 

@@ -50,6 +50,7 @@ struct LpOp {
     int32_t* out_list;  // candidate list (afterburner on) or move list (off)
     unsigned long long* out_cnt;
     unsigned long long* cut2;
+    int32_t* ext;  // optional: weighted external degree of every swept row (< 2^31)
     LpDebug dbg;
   };
   static __device__ __forceinline__ bool skip(const Args&, int, int) { return false; }
@@ -61,6 +62,7 @@ struct LpOp {
                                                 unsigned long long key,
                                                 long long ex, long long& acc) {
     acc += ex - self_c;
+    if (a.ext) a.ext[v] = (int32_t)(ex - self_c);
     const bool boundary = key != 0;
     const int dest = boundary ? unpack_part(key) : own;
     const long long F = boundary ? unpack_conn(key) - self_c : NO_GAIN;
@@ -934,7 +936,21 @@ struct ApArgs {
   unsigned long long* pw;
   unsigned long long* cut2d;
   int k;
+  int32_t* ext;  // optional: weighted external degrees kept current (level kernel, < 2^31)
 };
+
+// External-degree upkeep of one entry (v moves old -> dst, neighbour u in pu,
+// moving to mu or staying): v's new external degree accumulates in ev; a
+// staying neighbour's changes by w([dst != pu] - [old != pu]). A moving
+// neighbour recomputes its own, so every counter has one writer kind.
+static __device__ __forceinline__ void ext_entry(int32_t* ext, int u, int pu, int mu, int nu,
+                                                 int dst, int old, long long w, long long& ev) {
+  ev += nu != dst ? w : 0;
+  if (mu < 0) {
+    const int du = (int)w * ((int)(dst != pu) - (int)(old != pu));
+    if (du) atomicAdd(ext + u, du);
+  }
+}
 
 // Exact cut delta of a move batch (conn.py:231-248): for a moved v and
 // neighbour u, c = w([p'(u) != dest] - [p(u) != old]); edges with both ends
@@ -961,6 +977,7 @@ static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const S
           *wr += 1;
           *we += (unsigned long long)(e - b);
         }
+        long long ev = 0;
         for (int64_t j = b + threadIdx.x; j < e; j += blockDim.x) {
           const int u = g.adj[j];
           const int pu = a.parts[u];
@@ -969,6 +986,11 @@ static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const S
           const long long w = UNIT ? 1 : g.ew[j];
           const long long cc = w * ((long long)(nu != dst) - (long long)(pu != old));
           acc += mu >= 0 ? cc : 2 * cc;
+          if (a.ext) ext_entry(a.ext, u, pu, mu, nu, dst, old, w, ev);
+        }
+        if (a.ext) {
+          ev = block_sum_all(ev);
+          if (threadIdx.x == 0) a.ext[v] = (int32_t)ev;
         }
         if (threadIdx.x == 0) {
           const unsigned long long wv = (unsigned long long)g.vw[v];
@@ -998,7 +1020,7 @@ static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const S
             }
           }
         }
-        long long d = 0;
+        long long d = 0, ev = 0;
         for (int64_t j = b + gl; j < e; j += G) {
           const int u = g.adj[j];
           const int pu = a.parts[u];
@@ -1007,8 +1029,14 @@ static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const S
           const long long w = UNIT ? 1 : g.ew[j];
           const long long cc = w * ((long long)(nu != dst) - (long long)(pu != old));
           d += mu >= 0 ? cc : 2 * cc;
+          if (a.ext) ext_entry(a.ext, u, pu, mu, nu, dst, old, w, ev);
         }
         acc += d;
+        if (a.ext) {
+#pragma unroll
+          for (int o = G / 2; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
+          if (dst >= 0 && gl == 0) a.ext[v] = (int32_t)ev;
+        }
         if (dst >= 0 && gl == 0) {
           const unsigned long long wv = (unsigned long long)g.vw[v];
           atomicAdd(&a.pw[dst], wv);
@@ -1027,7 +1055,7 @@ static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const S
         *wr += 1;
         *we += (unsigned long long)(e - b);
       }
-      long long d = 0;
+      long long d = 0, ev = 0;
       for (int64_t j = b + lane; j < e; j += 32) {
         const int u = g.adj[j];
         const int pu = a.parts[u];
@@ -1036,8 +1064,13 @@ static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const S
         const long long w = UNIT ? 1 : g.ew[j];
         const long long cc = w * ((long long)(nu != dst) - (long long)(pu != old));
         d += mu >= 0 ? cc : 2 * cc;
+        if (a.ext) ext_entry(a.ext, u, pu, mu, nu, dst, old, w, ev);
       }
       acc += d;  // per-lane partial sums: the caller reduces over the block
+      if (a.ext) {
+        ev = gsum<32>(ev, 0xffffffffu);
+        if (lane == 0) a.ext[v] = (int32_t)ev;
+      }
       if (lane == 0) {
         const unsigned long long wv = (unsigned long long)g.vw[v];
         atomicAdd(&a.pw[dst], wv);
@@ -1055,6 +1088,7 @@ struct CommitArgs {
   int set_lock;
   const int32_t* lists[NBINS];
   const unsigned long long* cnts;
+  int32_t* cdest_reset;  // optional: Jetlp destinations of the listed rows back to -1
 };
 
 static __device__ void apply_commit_rows(const CommitArgs& a, int64_t t0, int64_t stride) {
@@ -1063,6 +1097,7 @@ static __device__ void apply_commit_rows(const CommitArgs& a, int64_t t0, int64_
     const int32_t* list = a.lists[t];
     for (int64_t i = t0; i < cnt; i += stride) {
       const int v = list[i];
+      if (a.cdest_reset) a.cdest_reset[v] = -1;
       const int dst = a.mv[v];
       if (dst < 0) continue;  // unmoved candidate (level kernel, Jetlp pass)
       a.parts[v] = dst;
@@ -1918,10 +1953,11 @@ static __device__ void rb_tail(const RbTail& a, unsigned long long* sk_smem) {
 // same-address atomics on the six counters every pass. All threads of the
 // block must call it.
 constexpr int RB_COL_IT = 8;
-static __device__ void rb_collect(const int32_t* __restrict__ parts, const int32_t* __restrict__ opidx,
-                           const int64_t* __restrict__ offs, TierMap tm, int64_t n, int32_t* lists,
-                           RbSegsDev seg, unsigned long long* cnts, int64_t /*t0*/, int64_t /*stride*/,
-                           unsigned long long* pwr = nullptr, unsigned long long* pwe = nullptr) {
+template <class Take>
+static __device__ void collect_tiled(Take take, const int64_t* __restrict__ offs, TierMap tm,
+                                     int64_t n, int32_t* lists, RbSegsDev seg,
+                                     unsigned long long* cnts, unsigned long long* pwr,
+                                     unsigned long long* pwe) {
   __shared__ unsigned s_wc[NBINS][32];
   __shared__ unsigned long long s_base[NBINS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -1935,7 +1971,7 @@ static __device__ void rb_collect(const int32_t* __restrict__ parts, const int32
     for (int j = 0; j < RB_COL_IT; ++j) {
       const int64_t v = wbase + j * 32 + lane;
       int t = -1;
-      if (v < n && opidx[parts[v]] >= 0) {
+      if (v < n && take((int)v)) {
         const int64_t d = offs[v + 1] - offs[v];
         t = tm(d);
         wr += 1;
@@ -1986,6 +2022,14 @@ static __device__ void rb_collect(const int32_t* __restrict__ parts, const int32
     *pwr += wr;
     *pwe += we;
   }
+}
+
+static __device__ void rb_collect(const int32_t* __restrict__ parts, const int32_t* __restrict__ opidx,
+                           const int64_t* __restrict__ offs, TierMap tm, int64_t n, int32_t* lists,
+                           RbSegsDev seg, unsigned long long* cnts, int64_t /*t0*/, int64_t /*stride*/,
+                           unsigned long long* pwr = nullptr, unsigned long long* pwe = nullptr) {
+  collect_tiled([&](int v) { return opidx[parts[v]] >= 0; }, offs, tm, n, lists, seg, cnts, pwr,
+                pwe);
 }
 
 }  // namespace jet
