@@ -736,7 +736,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       if (bnd) {
         const int32_t* ext = A.ext;
         collect_tiled([&](int v) { return __ldcg(ext + v) != 0; },
-                      A.g.offs, A.tm, A.n, A.blists, A.seg, P + CTR_BND, nullptr, nullptr);
+                      A.g.offs, A.tm, A.n, A.blists, A.seg, P + CTR_BND, &wk.v[6], &wk.v[7]);
         gsync();
         pc.mark(15);
       }
@@ -918,7 +918,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
   // last pass made the kept state, parts already is it
   if (!S.copy_keep)
     for (int64_t v = t0; v < A.n; v += nt) A.parts[v] = A.keep[v];
-  for (int i = 0; i < 6; ++i) block_sum_atomic_any((long long)wk.v[i], A.work + i);
+  for (int i = 0; i < 8; ++i) block_sum_atomic_any((long long)wk.v[i], A.work + i);
 }
 
 // ------------------------------------------------------------------ host
@@ -1159,9 +1159,15 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
     // algorithmic bytes of the launch (roofline accounting)
     const double ebytes = g.unit_ew ? 8.0 : 12.0;  // adj + neighbour part (+ weight)
     const double list = g.identity ? 0.0 : 4.0;
-    const double lp_pass = (double)g.n * (8 + 4 + 4 + 4 + list) + (double)g.nnz * ebytes;
+    const double row_b = 8 + 4 + 4 + 4 + list;  // offsets, own part, lock, cdest (+ list id)
+    const double lp_pass = (double)g.n * row_b + (double)g.nnz * ebytes;
     const double reb_pass = (double)g.n * (4 + 8);  // collect: parts + offsets
-    double b = h.lp * lp_pass + (h.weak + h.strong) * reb_pass;
+    // Jetlp: the first sweep of the level visits every row, later ones scan
+    // the external degrees and visit the boundary rows (counted on device)
+    const int lp_full = A.ext ? std::min(h.lp, 1) : h.lp;
+    double b = lp_full * lp_pass + (h.weak + h.strong) * reb_pass;
+    b += (double)(h.lp - lp_full) * (double)g.n * 4 + (double)wk[6] * (row_b + 4 + 8) +
+         (double)wk[7] * ebytes;
     b += (double)wk[0] * (4 + 8 + 4 + 16) + (double)wk[1] * ebytes;            // rb stats
     b += (double)wk[2] * (4 + 8 + 4 + 4 + 8) + (double)wk[3] * (ebytes + 12);  // afterburner
     b += (double)wk[4] * (4 + 8 + 4 + 4 + 4 + 16) + (double)wk[5] * (ebytes + 4);  // apply

@@ -16,7 +16,9 @@ namespace jet {
 // level and reduced once at the end: global atomics per warp on two hot
 // counters cost more than the sweeps they count.
 struct WorkAcc {
-  unsigned long long v[6] = {0, 0, 0, 0, 0, 0};
+  // stats rows/entries, afterburner rows/entries, apply rows/entries,
+  // boundary-sweep rows/entries
+  unsigned long long v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 };
 
 // ===========================================================================
