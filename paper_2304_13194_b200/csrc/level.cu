@@ -135,7 +135,7 @@ struct PhaseClock {
   __device__ __forceinline__ void mark(int ph) {
     if (acc && blockIdx.x == 0 && threadIdx.x == 0) {
       const long long now = dev_clock();
-      atomicAdd(acc + 16 * kind + ph, (unsigned long long)(now - t));
+      atomicAdd(acc + 24 * kind + ph, (unsigned long long)(now - t));
       t = now;
     }
   }
@@ -152,15 +152,33 @@ __device__ __forceinline__ int dev_ceil_log2(long long x) {
   return r;
 }
 
+// Block 0 keeps the controller state in shared memory (bookkeeping and
+// decisions are chains of dependent reads on it) and publishes it to global
+// memory after each decision; the words from rej_pos on are written by the
+// other blocks' draws and are not mirrored.
+constexpr int LV_CTL_WORDS = (int)(offsetof(LevelCtl, rej_pos) / 4);
+__device__ __forceinline__ void lv_ctl_load(LevelCtl* m, const LevelCtl* g) {
+  for (int i = threadIdx.x; i < (int)(sizeof(LevelCtl) / 4); i += blockDim.x)
+    reinterpret_cast<unsigned*>(m)[i] = __ldcg(reinterpret_cast<const unsigned*>(g) + i);
+  __syncthreads();
+}
+__device__ __forceinline__ void lv_ctl_publish(LevelCtl* g, const LevelCtl* m) {
+  __syncthreads();
+  constexpr int WP = (int)(offsetof(LevelCtl, pcg_state_hi) / 4);
+  for (int i = threadIdx.x; i < LV_CTL_WORDS + 8; i += blockDim.x) {
+    const int w = i < LV_CTL_WORDS ? i : WP + i - LV_CTL_WORDS;
+    reinterpret_cast<unsigned*>(g)[w] = reinterpret_cast<const unsigned*>(m)[w];
+  }
+}
+
 // ---------------------------------------------------------------- decide
 // P: the per-pass counter block of the pass being decided (zeroed here)
-__device__ void lv_decide(const LevelArgs& A, unsigned long long* P) {
+__device__ void lv_decide(const LevelArgs& A, LevelCtl* C, unsigned long long* P) {
   typedef cub::BlockScan<int, LV_BLOCK> BScan;
   typedef cub::BlockReduce<long long, LV_BLOCK> BRed;
   __shared__ typename BScan::TempStorage ts;
   __shared__ typename BRed::TempStorage tr;
   __shared__ int s_unbal, s_kind, s_no, s_nv;
-  LevelCtl* C = A.C;
   const long long* pw = reinterpret_cast<const long long*>(A.ctr + CTR_PW);
   const int tid = threadIdx.x, k = A.k;
   if (tid == 0) s_unbal = 0;
@@ -280,11 +298,10 @@ __device__ void lv_decide(const LevelArgs& A, unsigned long long* P) {
 }
 
 // -------------------------------------------------------------- bookkeep
-__device__ void lv_bookkeep(const LevelArgs& A, const unsigned long long* P) {
+__device__ void lv_bookkeep(const LevelArgs& A, LevelCtl* C, const unsigned long long* P) {
   typedef cub::BlockReduce<long long, LV_BLOCK> BRed;
   __shared__ typename BRed::TempStorage tr;
   __shared__ int s_copy;
-  LevelCtl* C = A.C;
   const long long* pw = reinterpret_cast<const long long*>(A.ctr + CTR_PW);
   const int tid = threadIdx.x, k = A.k;
   long long worst = LLONG_MIN;
@@ -677,7 +694,12 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
   // 0 can book-keep pass i and decide pass i+1 (zeroing the other block)
   // while the other blocks still commit pass i: one grid barrier per pass
   // fewer. The part weights (A.ctr + CTR_PW) are not per pass.
-  if (blockIdx.x == 0) lv_decide(A, A.ctr);  // pass_index 0 -> A.ctr
+  __shared__ LevelCtl s_mc;  // block 0: controller mirror
+  if (blockIdx.x == 0) {
+    lv_ctl_load(&s_mc, C);
+    lv_decide(A, &s_mc, A.ctr);  // pass_index 0 -> A.ctr
+    lv_ctl_publish(C, &s_mc);
+  }
   gsync();
   // control words of the pass, read once per block (every warp reading them
   // from L2 puts thousands of requests on one line per phase)
@@ -907,8 +929,11 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       apply_commit_rows(ca, t0, nt);
     }
     if (blockIdx.x == 0) {
-      lv_bookkeep(A, P);
-      lv_decide(A, (pass & 1) ? A.ctr : A.ctr2);
+      pc.mark(16);
+      lv_bookkeep(A, &s_mc, P);
+      pc.mark(17);
+      lv_decide(A, &s_mc, (pass & 1) ? A.ctr : A.ctr2);
+      lv_ctl_publish(C, &s_mc);
     }
     gsync();
     pc.mark(11);
@@ -1095,8 +1120,8 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   static const bool phases_on = getenv("JET_PHASES") && getenv("JET_PHASES")[0] == '1';
   DBuf<unsigned long long> pclk;
   if (phases_on) {
-    pclk.alloc(64, c.stream);
-    dzero(c, pclk.get(), 64);
+    pclk.alloc(96, c.stream);
+    dzero(c, pclk.get(), 96);
     A.phase_clk = pclk.get();
   }
   const void* kern = g.unit_ew ? (const void*)k_level<true> : (const void*)k_level<false>;
@@ -1130,19 +1155,20 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   d2h(c, w.h_pw.data(), (int64_t*)S.keep_pw.get(), k);
   c.sync();
   if (phases_on) {
-    unsigned long long pc[64];
-    d2h(c, pc, pclk.get(), 64);
+    unsigned long long pc[96];
+    d2h(c, pc, pclk.get(), 96);
     c.sync();
-    static const char* names[16] = {"decide", "lp_sweep", "afterburner", "rb_collect", "rb_stats",
+    static const char* names[24] = {"decide", "lp_sweep", "afterburner", "rb_collect", "rb_stats",
                                     "rb_scan", "rb_chunk", "rb_find", "rb_select", "rb_tail",
-                                    "apply_delta", "commit+keep", "tail_sort", "draw_fixup", "rb_prep", "bnd_collect"};
+                                    "apply_delta", "commit+keep", "tail_sort", "draw_fixup", "rb_prep",
+                                    "bnd_collect", "commit_rows", "bookkeep", "", "", "", "", "", ""};
     static const char* kinds[4] = {"stop", "lp", "weak", "strong"};
     const int cnt[4] = {1, h.lp, h.weak, h.strong};
     for (int kd = 1; kd < 4; ++kd) {
       if (!cnt[kd]) continue;
       fprintf(stderr, "PHASES L%d blocks=%d %s x%d (us/pass):", level, blocks, kinds[kd], cnt[kd]);
-      for (int i = 0; i < 16; ++i)
-        if (pc[16 * kd + i]) fprintf(stderr, " %s=%.1f", names[i], pc[16 * kd + i] / 1965.0 / cnt[kd]);
+      for (int i = 0; i < 24; ++i)
+        if (pc[24 * kd + i]) fprintf(stderr, " %s=%.1f", names[i], pc[24 * kd + i] / 1965.0 / cnt[kd]);
       fprintf(stderr, "\n");
     }
   }

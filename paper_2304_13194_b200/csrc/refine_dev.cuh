@@ -1094,8 +1094,11 @@ struct CommitArgs {
 };
 
 static __device__ void apply_commit_rows(const CommitArgs& a, int64_t t0, int64_t stride) {
+  int64_t cnts[NBINS];
+#pragma unroll
+  for (int t = 0; t < NBINS; ++t) cnts[t] = (int64_t)__ldcg(a.cnts + t);
   for (int t = 0; t < NBINS; ++t) {
-    const int64_t cnt = (int64_t)*(const volatile unsigned long long*)(a.cnts + t);
+    const int64_t cnt = cnts[t];
     const int32_t* list = a.lists[t];
     for (int64_t i = t0; i < cnt; i += stride) {
       const int v = list[i];
