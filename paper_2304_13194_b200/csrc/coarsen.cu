@@ -1421,8 +1421,10 @@ __global__ void k_accept_mutual(const int32_t* __restrict__ prop, int32_t* partn
   block_sum_atomic<256>(mine, npairs);
 }
 
-// Leftovers: key = (centre, v), centre = heaviest neighbour (ties: lowest id).
-__global__ void k_leaf_keys(GView g, const int32_t* __restrict__ left, int64_t nl,
+// Leftovers: key = (centre, v) packed in 2*vb bits (vb bits hold 0..n),
+// centre = heaviest neighbour (ties: lowest id), n for an isolated vertex --
+// the radix sort then runs over the bits in use only.
+__global__ void k_leaf_keys(GView g, const int32_t* __restrict__ left, int64_t nl, int vb,
                             unsigned long long* keys) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -1438,28 +1440,30 @@ __global__ void k_leaf_keys(GView g, const int32_t* __restrict__ left, int64_t n
     }
     best = gmax<32>(best, 0xffffffffu);
     if (lane == 0) {
-      const unsigned long long c = best ? (0xffffffffu - (best & 0xffffffffu)) : 0xffffffffull;
-      keys[i] = (c << 32) | (unsigned)v;
+      const unsigned long long c =
+          best ? (0xffffffffu - (best & 0xffffffffu)) : (unsigned long long)g.n;
+      keys[i] = (c << vb) | (unsigned)v;
     }
   }
 }
 
 // Pair consecutive leftovers under the same centre: (0,1), (2,3), ... of
 // each run of the sorted keys.
-__global__ void k_leaf_pair(const unsigned long long* __restrict__ keys, int64_t nl,
-                            int32_t* partner) {
+__global__ void k_leaf_pair(const unsigned long long* __restrict__ keys, int64_t nl, int vb,
+                            int64_t n, int32_t* partner) {
+  const unsigned long long vm = (1ull << vb) - 1;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const unsigned c = (unsigned)(keys[i] >> 32);
-    if (c == 0xffffffffu) continue;  // isolated vertex
-    if (i > 0 && (unsigned)(keys[i - 1] >> 32) == c) continue;  // not a run start
+    const unsigned long long c = keys[i] >> vb;
+    if ((int64_t)c == n) continue;  // isolated vertex
+    if (i > 0 && (keys[i - 1] >> vb) == c) continue;  // not a run start
     int64_t j = i;
-    while (j + 1 < nl && (unsigned)(keys[j + 1] >> 32) == c) {
-      const int a = (int)(keys[j] & 0xffffffffu), b = (int)(keys[j + 1] & 0xffffffffu);
+    while (j + 1 < nl && (keys[j + 1] >> vb) == c) {
+      const int a = (int)(keys[j] & vm), b = (int)(keys[j + 1] & vm);
       partner[a] = b;
       partner[b] = a;
       j += 2;
-      if (j >= nl || (unsigned)(keys[j] >> 32) != c) break;
+      if (j >= nl || (keys[j] >> vb) != c) break;
     }
   }
 }
@@ -1485,17 +1489,19 @@ static void leaf_match(Ctx& c, const DGraph& g, int32_t* partner) {
   unsigned long long* k0 = c.scratch<unsigned long long>(14, nl);
   unsigned long long* k1 = c.scratch<unsigned long long>(16, nl);
   const GView gv = view(g);
+  int vb = 1;
+  while ((1LL << vb) <= n) ++vb;  // vb bits hold 0..n
   launch(c, "leaf_keys", 16.0 * nl, [&] {
-    k_leaf_keys<<<grid_for(c, nl * 32, 256), 256, 0, c.stream>>>(gv, left_p, nl, k0);
+    k_leaf_keys<<<grid_for(c, nl * 32, 256), 256, 0, c.stream>>>(gv, left_p, nl, vb, k0);
   });
   size_t tmp = 0;
-  CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k0, k1, (int)nl, 0, 64, c.stream));
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k0, k1, (int)nl, 0, 2 * vb, c.stream));
   void* p = c.cub_scratch(tmp);
   launch(c, "leaf_sort", 32.0 * nl, [&] {
-    CK(cub::DeviceRadixSort::SortKeys(p, tmp, k0, k1, (int)nl, 0, 64, c.stream));
+    CK(cub::DeviceRadixSort::SortKeys(p, tmp, k0, k1, (int)nl, 0, 2 * vb, c.stream));
   });
   launch(c, "leaf_pair", 16.0 * nl, [&] {
-    k_leaf_pair<<<grid_for(c, nl, 256), 256, 0, c.stream>>>(k1, nl, partner);
+    k_leaf_pair<<<grid_for(c, nl, 256), 256, 0, c.stream>>>(k1, nl, vb, n, partner);
   });
 }
 
