@@ -129,6 +129,11 @@ __global__ void k_level_stats(const int64_t* __restrict__ offs,
   }
   __syncthreads();
   unsigned long long tv = 0, mv = 0, md = 0, me = 0, mn = ~0ull;
+  // tier histogram in registers, reduced per warp (per-vertex shared atomics
+  // on six addresses serialised 32-way)
+  unsigned long long rc[NBINS], rn[NBINS];
+#pragma unroll
+  for (int t = 0; t < NBINS; ++t) rc[t] = rn[t] = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride) {
     int64_t d = offs[v + 1] - offs[v];
@@ -137,9 +142,21 @@ __global__ void k_level_stats(const int64_t* __restrict__ offs,
     mv = w > mv ? w : mv;
     mn = w < mn ? w : mn;
     md = (unsigned long long)d > md ? (unsigned long long)d : md;
-    int t = tm(d);
-    atomicAdd(&s_cnt[t], 1ull);
-    atomicAdd(&s_nnz[t], (unsigned long long)d);
+    const int t = tm(d);
+#pragma unroll
+    for (int q = 0; q < NBINS; ++q) {
+      rc[q] += q == t ? 1ull : 0ull;
+      rn[q] += q == t ? (unsigned long long)d : 0ull;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NBINS; ++q) {
+    const unsigned long long c2 = gsum<32>(rc[q], 0xffffffffu);
+    const unsigned long long n2 = gsum<32>(rn[q], 0xffffffffu);
+    if ((threadIdx.x & 31) == 0 && c2) {
+      atomicAdd(&s_cnt[q], c2);
+      atomicAdd(&s_nnz[q], n2);
+    }
   }
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += stride) {
     unsigned long long w = (unsigned long long)ew[e];
