@@ -87,6 +87,7 @@ struct LevelArgs {
   unsigned long long* CH;
   int32_t* ext;        // weighted external degree per vertex (boundary iff > 0)
   int32_t* blists;     // per-tier boundary rows (segments as cand_lists)
+  int32_t* wdeg;       // weighted degrees (written by the first Jetlp sweep; weighted levels)
   int32_t* opidx;
   uint8_t* valid;
   int32_t* valid_list;
@@ -752,6 +753,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
         a.out_cnt = P + (A.afterburner ? CTR_CAND : CTR_MOVE) + t;
         a.cut2 = P + CTR_CUT2;
         a.ext = A.ext;
+        a.wdeg = A.ext ? A.wdeg : nullptr;
         return a;
       };
       const bool bnd = ext_ok;
@@ -813,6 +815,8 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       ra.rcand_cnt = P + CTR_RCAND;
       ra.H = A.H;
       ra.Hs = A.Hs;
+      ra.ext = ext_ok ? A.ext : nullptr;
+      ra.wdeg = A.wdeg;
       lv_sweep<RbOp, UNIT>(A, [&](int) { return ra; }, clists, P + CTR_CAND, lv_smem, w0, nw,
                            acc);
       gsync();
@@ -963,6 +967,7 @@ struct LevelScratch : CtxExt {
   DBuf<unsigned long long> ctr2;
   DBuf<int32_t> ext;
   DBuf<int32_t> blists;
+  DBuf<int32_t> wdeg;
 };
 
 static LevelScratch& level_scratch(Ctx& c) {
@@ -1061,6 +1066,8 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   // (external degrees are int32: levels with weighted degrees >= 2^31 sweep in full)
   A.ext = (getenv("JET_FULL_SWEEPS") || g.max_wdeg >= (1LL << 31)) ? nullptr : S.ext.get();
   A.blists = S.blists.get();
+  S.wdeg.ensure(g.n, c.stream);
+  A.wdeg = g.unit_ew ? nullptr : S.wdeg.get();
   A.cand_lists = w.lists.get();
   A.move_lists = w.lists.get() + w.cap_n;
   A.ctr = w.ctr.get();

@@ -52,10 +52,13 @@ struct LpOp {
     int32_t* out_list;  // candidate list (afterburner on) or move list (off)
     unsigned long long* out_cnt;
     unsigned long long* cut2;
-    int32_t* ext;  // optional: weighted external degree of every swept row (< 2^31)
+    int32_t* ext;   // optional: weighted external degree of every swept row (< 2^31)
+    int32_t* wdeg;  // optional: weighted degree of every swept row (< 2^31)
     LpDebug dbg;
   };
   static __device__ __forceinline__ bool skip(const Args&, int, int) { return false; }
+  // Jetlp sweeps only boundary rows already (level kernel): nothing to short-cut
+  static __device__ __forceinline__ long long interior_w(const Args&, int, int, bool) { return -1; }
   static __device__ __forceinline__ bool competes(const Args&, int p, int own) { return p != own; }
   static __device__ __forceinline__ int extra(const Args&, int, int w) { return w; }
   // self_c = conn(v, own); key = best other part; ex = weighted degree
@@ -65,6 +68,7 @@ struct LpOp {
                                                 long long ex, long long& acc) {
     acc += ex - self_c;
     if (a.ext) a.ext[v] = (int32_t)(ex - self_c);
+    if (a.wdeg) a.wdeg[v] = (int32_t)ex;
     const bool boundary = key != 0;
     const int dest = boundary ? unpack_part(key) : own;
     const long long F = boundary ? unpack_conn(key) - self_c : NO_GAIN;
@@ -116,9 +120,18 @@ struct RbOp {
     unsigned long long* rcand_cnt;
     unsigned long long* H;
     unsigned long long* Hs;  // per-slot totals (ns per oversized part)
+    const int32_t* ext;      // optional (level kernel): weighted external degrees
+    const int32_t* wdeg;     // weighted degrees (weighted levels)
   };
   static __device__ __forceinline__ bool skip(const Args& a, int, int own) {
     return a.opidx[own] < 0;
+  }
+  // A candidate without neighbours outside its part needs no adjacency: its
+  // own-part connectivity is its weighted degree and no part competes.
+  // Returns that weight, or -1 when the row has to be swept.
+  static __device__ __forceinline__ long long interior_w(const Args& a, int v, int deg, bool unit) {
+    if (!a.ext || __ldcg(a.ext + v) != 0) return -1;
+    return unit ? (long long)deg : (long long)a.wdeg[v];
   }
   static __device__ __forceinline__ bool competes(const Args& a, int p, int) {
     return a.valid[p] != 0;
@@ -228,6 +241,7 @@ static __device__ __forceinline__ void agg_rows32(const typename Op::Args& a, co
     const int64_t idx = base + lane;
     int v = 0, own = -1, deg = 0;
     int64_t beg = 0;
+    long long wself = -1;  // >= 0: interior row, nothing staged
     if (lane < R && idx < cnt) {
       v = list ? list[idx] : (int)idx;
       own = parts[v];
@@ -236,6 +250,8 @@ static __device__ __forceinline__ void agg_rows32(const typename Op::Args& a, co
       } else {
         beg = g.offs[v];
         deg = (int)(g.offs[v + 1] - beg);
+        wself = Op::interior_w(a, v, deg, UNIT);
+        if (wself >= 0) deg = 0;
       }
     }
     for (int r = 0; r < R; ++r) {
@@ -305,6 +321,11 @@ static __device__ __forceinline__ void agg_rows32(const typename Op::Args& a, co
       }
     }
     __syncwarp();  // the next batch reuses the stage
+    if (wself >= 0) {
+      my_self = wself;
+      my_key = 0ull;
+      my_ex = Op::extra(a, own, 1) ? wself : 0;  // extra is linear in w
+    }
     if (own >= 0) Op::finish(a, v, own, my_self, my_key, my_ex, acc);
   }
 }
@@ -350,6 +371,7 @@ static __device__ __forceinline__ void agg_small(const typename Op::Args& a, con
     const int64_t idx = base + lane;
     int v = 0, own = -1, deg = 0;
     int64_t beg = 0;
+    long long wself = -1;  // >= 0: interior row, nothing staged
     if (lane < R && idx < cnt) {
       v = list ? list[idx] : (int)idx;
       own = parts[v];
@@ -358,6 +380,8 @@ static __device__ __forceinline__ void agg_small(const typename Op::Args& a, con
       } else {
         beg = g.offs[v];
         deg = (int)(g.offs[v + 1] - beg);
+        wself = Op::interior_w(a, v, deg, UNIT);
+        if (wself >= 0) deg = 0;
       }
     }
     // stage adjacency (+ weights)
@@ -512,6 +536,11 @@ static __device__ __forceinline__ void agg_small(const typename Op::Args& a, con
       }
     }
     __syncwarp();  // the next batch reuses the stage
+    if (wself >= 0) {
+      my_self = wself;
+      my_key = 0ull;
+      my_ex = Op::extra(a, own, 1) ? wself : 0;  // extra is linear in w
+    }
     if (own >= 0) Op::finish(a, v, own, my_self, my_key, my_ex, acc);
   }
 }
@@ -545,6 +574,7 @@ static __device__ void agg_warp(const typename Op::Args& a, const GView& g,
     const int64_t idx = base + lane;
     int v = 0, own = -1, deg = 0;
     int64_t beg = 0;
+    long long wself = -1;  // >= 0: interior row, nothing staged
     if (lane < R && idx < cnt) {
       v = list ? list[idx] : (int)idx;
       own = parts[v];
@@ -553,6 +583,8 @@ static __device__ void agg_warp(const typename Op::Args& a, const GView& g,
       } else {
         beg = g.offs[v];
         deg = (int)(g.offs[v + 1] - beg);
+        wself = Op::interior_w(a, v, deg, UNIT);
+        if (wself >= 0) deg = 0;
       }
     }
     long long my_self = 0, my_ex = 0;
@@ -656,6 +688,11 @@ static __device__ void agg_warp(const typename Op::Args& a, const GView& g,
         __syncwarp();
         (void)cur_d;
       }
+    }
+    if (wself >= 0) {
+      my_self = wself;
+      my_key = 0ull;
+      my_ex = Op::extra(a, own, 1) ? wself : 0;  // extra is linear in w
     }
     if (own >= 0) Op::finish(a, v, own, my_self, my_key, my_ex, acc);
   }
