@@ -1992,9 +1992,13 @@ static __device__ void rb_tail(const RbTail& a, unsigned long long* sk_smem) {
 // degree tier. Blocks take tiles of blockDim * RB_COL_IT consecutive ids
 // (coalesced loads, RB_COL_IT independent per thread) and reserve each
 // tier's output once per tile -- per-warp appends put tens of thousands of
-// same-address atomics on the six counters every pass. All threads of the
-// block must call it.
-constexpr int RB_COL_IT = 8;
+// same-address atomics on the six counters every pass. Two ids per thread
+// measured best (1: 44.98, 2: 44.47, 4: 45.4, 8: 47.5, 16: 51.8 ms of level
+// kernels on the headline). All threads of the block must call it.
+#ifndef RB_COL_ITEMS
+#define RB_COL_ITEMS 2
+#endif
+constexpr int RB_COL_IT = RB_COL_ITEMS;
 template <class Take>
 static __device__ void collect_tiled(Take take, const int64_t* __restrict__ offs, TierMap tm,
                                      int64_t n, int32_t* lists, RbSegsDev seg,
