@@ -37,7 +37,10 @@ constexpr int LV_TAIL_SMEM = 8192;  // evicted keys sorted in shared memory
 constexpr int LV_DRAW_SLACK = 64;
 constexpr int64_t LV_ROWS_PER_BLOCK = 128;  // measured: 512 -> 128 saves ~2 ms on 128^3
 constexpr int64_t LV_ENTRIES_PER_BLOCK = 16384;  // dense coarse levels (R-MAT)
-constexpr int LV_RB = 16;  // rows per warp batch in the staged short-row sweep
+#ifndef LV_RB_ROWS
+#define LV_RB_ROWS 8
+#endif
+constexpr int LV_RB = LV_RB_ROWS;  // rows per warp batch in the staged short-row sweep (8 measured best of 4-32)
 
 struct LevelCtl {
   long long cut, best_cut, keep_cut, keep_worst;
