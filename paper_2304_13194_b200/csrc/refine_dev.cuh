@@ -15,6 +15,14 @@ namespace jet {
 // the stats, afterburner and apply sweeps). Kept in registers for a whole
 // level and reduced once at the end: global atomics per warp on two hot
 // counters cost more than the sweeps they count.
+// lanes per row in the short-row afterburner and apply loops (tiers 0-3)
+#ifndef AB_GROUP_LANES
+#define AB_GROUP_LANES 8
+#endif
+#ifndef AP_GROUP_LANES
+#define AP_GROUP_LANES 8
+#endif
+
 struct WorkAcc {
   // stats rows/entries, afterburner rows/entries, apply rows/entries,
   // boundary-sweep rows/entries
@@ -926,7 +934,7 @@ static __device__ void afterburner_rows(const AbArgs& a, const GView& g, const S
       continue;
     }
     if (t < BIN_WARP) {  // short rows: 8-lane groups, four rows per warp step
-      ab_group_rows<8, UNIT>(a, g, list, cnt, t, mseg, w0, ws, wr, we, nmove);
+      ab_group_rows<AB_GROUP_LANES, UNIT>(a, g, list, cnt, t, mseg, w0, ws, wr, we, nmove);
       continue;
     }
     for (int64_t i = w0; i < cnt; i += ws) {
@@ -1040,7 +1048,7 @@ static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const S
       continue;
     }
     if (t < BIN_WARP) {  // short rows: 8-lane groups, four rows per warp step
-      constexpr int G = 8, RPS = 4;
+      constexpr int G = AP_GROUP_LANES, RPS = 32 / G;
       const int gl = lane & (G - 1), grp = lane / G;
       for (int64_t base = w0 * RPS; base < cnt; base += ws * RPS) {
         const int64_t i = base + grp;
