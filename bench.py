@@ -369,7 +369,8 @@ def run_ours(args, world, rank, local):
             "balanced": bool(st.balanced),
             "gpu_launches": launches,
             "e2e": {"value": e2e_v, "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "partition_time_s": e2e_s},
+                    "d2h_bytes_per_step": int(d2h), "partition_time_s": e2e_s,
+                    "steps_ms": [round(x * 1e3, 2) for x in e2e]},
             "roofline": {"bound": "hbm", "kernel": dominant,
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
