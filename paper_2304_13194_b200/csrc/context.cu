@@ -151,7 +151,12 @@ int jet_create(int device, jet_ctx** out) {
     CK(cudaGetDeviceCount(&ndev));
     JET_REQUIRE(device >= 0 && device < ndev, JET_EINVAL,
                 "device index out of range");
+    // the pipeline synchronises with the device at a few hundred points per
+    // partition (level sizes, matching rounds): spin rather than yield, so a
+    // busy host does not stretch each wait (no effect, and ignored, when the
+    // device's context already exists)
     CK(cudaSetDevice(device));
+    if (cudaSetDeviceFlags(cudaDeviceScheduleSpin) != cudaSuccess) (void)cudaGetLastError();
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, device));
     JET_REQUIRE(prop.major >= 10, JET_EUNSUPPORTED,
