@@ -1883,9 +1883,9 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
       CK(cub::DeviceScan::ExclusiveSum(p, tmp, rowlen_p, toff_p, (int)(nc + 1), c.stream));
     });
   }
-  int64_t T = 0;
-  d2h(c, &T, toff_p + nc, 1);
-  c.sync();
+  // the merged rows concatenate both members' rows: their lengths sum to the
+  // fine graph's entry count (no need to read the scan's total back)
+  const int64_t T = g.nnz;
   mark("map+scan");
   int32_t* tadj_p = c.scratch<int32_t>(7, T);
   int32_t* tew_p = c.scratch<int32_t>(8, T);

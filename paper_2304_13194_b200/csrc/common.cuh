@@ -218,7 +218,11 @@ struct Ctx {
   DBuf<uint8_t> up_dev;
   void ensure_upload_ring();
   void ensure_pinned_up(size_t bytes);
-  void sync() { CK(cudaStreamSynchronize(stream)); }
+  long long nsync = 0;  // host waits on the stream (diagnostics: JET_SYNC_STATS)
+  void sync() {
+    ++nsync;
+    CK(cudaStreamSynchronize(stream));
+  }
   void* cub_scratch(size_t bytes) {
     cub_tmp.ensure(bytes, stream);
     return cub_tmp.get();

@@ -171,6 +171,7 @@ void run_partition(Ctx& c, const DGraph& g0, const jet_config& cfg, int32_t* par
   check_partition_args(g0, cfg);
   const int k = cfg.k;
   const double t0 = now_s();
+  const long long nsync0 = c.nsync;
   jet_run_stats local{};
   jet_run_stats& S = st ? *st : local;
   const double t_up = S.t_upload;
@@ -261,6 +262,9 @@ void run_partition(Ctx& c, const DGraph& g0, const jet_config& cfg, int32_t* par
   S.max_part_weight = *std::max_element(w.h_pw.begin(), w.h_pw.end());
   S.balanced = S.max_part_weight <= cfg.limit;
   if (pw_out) std::copy(w.h_pw.begin(), w.h_pw.end(), pw_out);
+  if (getenv("JET_SYNC_STATS"))
+    fprintf(stderr, "SYNC_STATS host waits=%lld (coarsen %.3f s, uncoarsen %.3f s)\n", c.nsync - nsync0,
+            S.t_coarsen, S.t_uncoarsen);
 }
 
 }  // namespace jet
