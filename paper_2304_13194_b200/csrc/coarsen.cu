@@ -1468,6 +1468,11 @@ __global__ void k_leaf_pair(const unsigned long long* __restrict__ keys, int64_t
   }
 }
 
+// throughput-mode matching rounds launched between two host checks
+#ifndef MATCH_ROUND_GROUP
+#define MATCH_ROUND_GROUP 4
+#endif
+
 static void leaf_match(Ctx& c, const DGraph& g, int32_t* partner) {
   const int64_t n = g.n;
   int32_t* left_p = c.scratch<int32_t>(13, n);
@@ -1517,7 +1522,7 @@ static void device_match_fast(Ctx& c, const DGraph& g, int32_t* partner) {
     // {proposers, pairs} counters, and a round after one that matched nothing
     // is a no-op on the device (fast_round_dead), so the result is the same as
     // checking after every round, with a quarter of the host round trips
-    constexpr int RG = 4, MAXR = 48;
+    constexpr int RG = MATCH_ROUND_GROUP, MAXR = 48;
     DBuf<unsigned long long> cnt(2 * MAXR, c.stream);
     dzero(c, cnt.get(), 2 * MAXR);
     const GView gv = view(g);
