@@ -933,7 +933,13 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
       for (int t = 0; t < NBINS; ++t) ca.lists[t] = ml.list[t];
       ca.cnts = ml.cnt;
       ca.cdest_reset = (kind == 1 && A.afterburner && ext_ok) ? A.cdest : nullptr;
-      apply_commit_rows(ca, t0, nt);
+      // block 0 books the pass and decides the next one meanwhile (they read
+      // only counters and part weights, final since the apply barrier), so
+      // the other blocks commit the moves without it when there are any
+      if (gridDim.x == 1)
+        apply_commit_rows(ca, t0, nt);
+      else if (blockIdx.x > 0)
+        apply_commit_rows(ca, t0 - blockDim.x, nt - blockDim.x);
     }
     if (blockIdx.x == 0) {
       pc.mark(16);
