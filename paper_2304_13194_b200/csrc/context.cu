@@ -156,7 +156,9 @@ int jet_create(int device, jet_ctx** out) {
     // busy host does not stretch each wait (no effect, and ignored, when the
     // device's context already exists)
     CK(cudaSetDevice(device));
+#ifndef JET_NO_SPIN
     if (cudaSetDeviceFlags(cudaDeviceScheduleSpin) != cudaSuccess) (void)cudaGetLastError();
+#endif
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, device));
     JET_REQUIRE(prop.major >= 10, JET_EUNSUPPORTED,

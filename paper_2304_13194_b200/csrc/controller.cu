@@ -193,18 +193,27 @@ void run_partition(Ctx& c, const DGraph& g0, const jet_config& cfg, int32_t* par
   // temporaries); reserve it in the pool before starting, so no allocation
   // inside the pipeline has to map new memory (100s of ms stalls measured on
   // dense coarse levels of R-MAT 2^25), capped at 60 % of free memory
+  // (cudaMemGetInfo only when the pool has to grow: the query itself stalled
+  // the host for 50-90 ms in ~1 of 8 calls)
   {
-    size_t fr = 0, tot = 0;
-    CK(cudaMemGetInfo(&fr, &tot));
     const size_t csr = (size_t)g0.nnz * 8 + (size_t)g0.n * 24;
-    c.reserve_pool(std::min<size_t>(12 * csr, c.pool_reserved + fr / 10 * 6));
+    if (12 * csr > c.pool_reserved) {
+      size_t fr = 0, tot = 0;
+      CK(cudaMemGetInfo(&fr, &tot));
+      c.reserve_pool(std::min<size_t>(12 * csr, c.pool_reserved + fr / 10 * 6));
+    }
   }
+  const double t_res = now_s();
   Hierarchy h;
   c.prof_tag = "coarsen:";
   device_build_hierarchy(c, g0, target, h, cfg.deterministic == 0);
   c.prof_tag.clear();
+  const double t_hier = now_s();
   c.sync();
   const double t1 = now_s();
+  if (getenv("JET_SYNC_STATS"))
+    fprintf(stderr, "COARSEN_SPLIT pre %.2f ms hierarchy %.2f ms final sync %.2f ms\n",
+            (t_res - t0) * 1e3, (t_hier - t_res) * 1e3, (t1 - t_hier) * 1e3);
   S.t_coarsen = t1 - t0;
 
   const int top = h.size() - 1;
