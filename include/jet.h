@@ -38,7 +38,9 @@ typedef enum {
   JET_ENOMEM = 4,       /* device allocation failed */
   JET_EREBALANCE = 5,   /* RebalanceInfeasibleError (rebalance.py:153-156) */
   JET_EINTERNAL = 6,    /* internal invariant violated */
-  JET_EUNSUPPORTED = 7  /* input outside the GPU path's supported range */
+  JET_EUNSUPPORTED = 7, /* input outside the GPU path's supported range */
+  JET_EASSERT = 8       /* a reference assertion failed (AssertionError), e.g.
+                           "move to current part" (conn.py:224) */
 } jet_status;
 
 #define JET_I32 4
@@ -76,7 +78,10 @@ typedef struct {
   int32_t restarts;
   int32_t afterburner;
   int32_t locking;
-  int32_t deterministic; /* 1: bit-exact reference semantics (only mode in v1) */
+  int32_t deterministic; /* 1: bit-exact reference semantics in every kernel;
+                            0: throughput mode (hashed-priority matching,
+                            same refinement; cut gated at 1.02x the
+                            reference's, balance always met) */
   int32_t verbose;
 } jet_config;
 
@@ -141,10 +146,13 @@ void jet_graph_free(jet_graph* g);
 
 /* ---- 1D vertex sharding ----------------------------------
  * With a communicator of size > 1 attached, levels of at least
- * `shard_min_vertices` vertices (default 2^20) refine with sharded Jetlp
- * sweeps: each rank sweeps its block of vertices (balanced by entries) and
- * the ranks all-gather the candidates (id, destination, gain) and the moves;
- * coarse levels, rebalancing and the apply step run replicated. Every rank
+ * `shard_min_vertices` vertices (default 2^20) refine sharded: each rank owns
+ * a block of vertices (balanced by entries). Jetlp passes sweep the owned
+ * block and all-gather the candidates (id, destination, gain) and the moves;
+ * rebalancing passes collect and score the owned candidates, all-reduce the
+ * bucket histograms and crossing-chunk weights and all-gather the direct
+ * moves and the evicted sets. The apply step and coarsening run replicated
+ * on the gathered moves, and smaller levels run unsharded. Every rank
  * computes the same partition, bit-identical to the unsharded run.
  * NCCL (one process per GPU): rank 0 calls jet_comm_nccl_id, the id is
  * broadcast out of band (torch.distributed), every rank attaches.
@@ -177,6 +185,23 @@ int jet_generate_geometric(jet_ctx* ctx, int64_t n, double radius, uint64_t seed
 /* cutsize(graph, parts)  graph.py:215-221 */
 int jet_cutsize(jet_ctx* ctx, const jet_graph* g, const int64_t* parts,
                 int64_t* cut_out);
+/* ConnectivityTable contents (conn.py:70-123): the nonzero conn(v, p) of
+ * the given rows (rows == NULL: every row) as (row, part, weight) triples
+ * sorted by (row, part). *count receives the number of triples; the output
+ * arrays (any may be NULL) need cap >= *count entries (a call with all
+ * outputs NULL returns the count only). Rows are rebuilt from the CSR. */
+int jet_conn_triples(jet_ctx* ctx, const jet_graph* g, const int64_t* parts,
+                     int32_t k, const int64_t* rows, int64_t n_rows,
+                     int64_t* row_out, int64_t* part_out, int64_t* weight_out,
+                     int64_t cap, int64_t* count);
+/* ConnectivityTable.apply / update_conn (conn.py:215-254, 270-272): apply a
+ * move list to (parts, part_weights, cut) in place by exact deltas.
+ * Duplicate vertices are JET_EINVAL (moves.py:31-32); a move to the current
+ * part is JET_EASSERT (conn.py:224). */
+int jet_apply_moves(jet_ctx* ctx, const jet_graph* g, int64_t* parts, int32_t k,
+                    int64_t* part_weights, int64_t* cut,
+                    const int64_t* move_vertices, const int64_t* move_dests,
+                    int64_t n_moves);
 /* PartitionState.from_parts weights  graph.py:240-242 */
 int jet_part_weights(jet_ctx* ctx, const jet_graph* g, const int64_t* parts,
                      int32_t k, int64_t* pw_out);

@@ -20,6 +20,7 @@ from .graph import (
 )
 from .moves import MoveList
 from .ops import (
+    ConnectivityTable,
     Hierarchy,
     LockTable,
     afterburner,
@@ -32,6 +33,7 @@ from .ops import (
     match_vertices,
     select_destinations,
     strong_rebalance_pass,
+    update_conn,
     weak_rebalance_pass,
 )
 from ._lib import Context, DeviceGraph
@@ -39,11 +41,11 @@ from ._lib import Context, DeviceGraph
 __version__ = "0.1.0"
 
 __all__ = [
-    "BalanceInfeasibleError", "Context", "DeviceGraph", "Graph", "Hierarchy", "JetpartError",
+    "BalanceInfeasibleError", "ConnectivityTable", "Context", "DeviceGraph", "Graph", "Hierarchy", "JetpartError",
     "LockTable", "MoveList", "PartitionResult", "PartitionState", "RebalanceInfeasibleError",
     "RefinerConfig", "afterburner", "build_conn", "build_hierarchy", "contract", "cutsize",
     "from_edge_arrays", "imbalance_of", "initial_partition", "is_balanced", "jet_refine",
     "jetlp_pass", "match_vertices", "part_weight_limit", "partition", "project",
     "rebalance_thresholds", "select_destinations", "strong_rebalance_pass",
-    "weak_rebalance_pass",
+    "update_conn", "weak_rebalance_pass",
 ]

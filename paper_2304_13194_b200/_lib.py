@@ -25,7 +25,7 @@ if os.environ.get("JET_LIB"):  # alternative build of the same library (experime
     LIB_PATH = Path(os.environ["JET_LIB"]).resolve()
 
 JET_OK, JET_EINVAL, JET_EBALANCE, JET_ECUDA, JET_ENOMEM, JET_EREBALANCE = 0, 1, 2, 3, 4, 5
-JET_EINTERNAL, JET_EUNSUPPORTED = 6, 7
+JET_EINTERNAL, JET_EUNSUPPORTED, JET_EASSERT = 6, 7, 8
 JET_I32, JET_I64 = 4, 8
 MAX_LEVELS = 64
 
@@ -103,6 +103,8 @@ _SIGS = {
     "jet_generate_geometric": (C.c_int, [P, i64, C.c_double, C.c_uint64, C.POINTER(P)]),
     "jet_cutsize": (C.c_int, [P, P, P, P]),
     "jet_part_weights": (C.c_int, [P, P, P, i32, P]),
+    "jet_conn_triples": (C.c_int, [P, P, P, i32, P, i64, P, P, P, i64, P]),
+    "jet_apply_moves": (C.c_int, [P, P, P, i32, P, P, P, P, i64]),
     "jet_match": (C.c_int, [P, P, P]),
     "jet_contract": (C.c_int, [P, P, P, C.POINTER(P), P]),
     "jet_hierarchy_build": (C.c_int, [P, P, i64, C.POINTER(P)]),
@@ -165,6 +167,8 @@ def check(status: int) -> None:
         raise RebalanceInfeasibleError(msg)
     if status == JET_ENOMEM:
         raise MemoryError(msg)
+    if status == JET_EASSERT:
+        raise AssertionError(msg)
     raise JetpartError(f"[jet status {status}] {msg}")
 
 
@@ -285,6 +289,36 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def csr_arrays(graph):
+    """The four CSR arrays of a Graph-like object as C-contiguous int64 (int32
+    arrays are passed through), with their dtype codes. The C ABI derives the
+    entry count from row_offsets[n] and reads that many adjacency and weight
+    entries, so the lengths are checked here, before any native call."""
+    offs = as_i64(graph.row_offsets)
+    if len(offs) < 1:
+        raise ValueError("row_offsets must have n + 1 >= 1 entries")
+    n = len(offs) - 1
+    out, codes = [offs], []
+    for a in (graph.adjacency, graph.edge_weights, graph.vertex_weights):
+        a = np.asarray(a)
+        if a.ndim != 1:
+            raise ValueError("graph arrays must be one-dimensional")
+        if a.dtype == np.int32 and a.flags.c_contiguous:
+            out.append(a)
+            codes.append(JET_I32)
+        else:
+            out.append(as_i64(a))
+            codes.append(JET_I64)
+    nnz = int(offs[-1])
+    if len(out[1]) != nnz:
+        raise ValueError(f"adjacency has {len(out[1])} entries but row_offsets[n] = {nnz}")
+    if len(out[2]) != len(out[1]):
+        raise ValueError("edge_weights must align with adjacency")
+    if len(out[3]) != n:
+        raise ValueError(f"vertex_weights has {len(out[3])} entries for n = {n}")
+    return out, codes
+
+
 class DeviceGraph:
     """A device-resident CSR level (owning unless created as a view)."""
 
@@ -296,17 +330,8 @@ class DeviceGraph:
     @classmethod
     def upload(cls, graph, ctx: Context | None = None) -> "DeviceGraph":
         ctx = ctx or Context.default()
-        offs = as_i64(graph.row_offsets)
+        (offs, *arrays), codes = csr_arrays(graph)
         n = len(offs) - 1
-        arrays, codes = [], []
-        for a in (graph.adjacency, graph.edge_weights, graph.vertex_weights):
-            a = np.asarray(a)
-            if a.dtype == np.int32 and a.flags.c_contiguous:
-                arrays.append(a)
-                codes.append(JET_I32)
-            else:
-                arrays.append(as_i64(a))
-                codes.append(JET_I64)
         h = P()
         check(lib().jet_graph_upload(
             ctx.handle, n, ptr(offs), ptr(arrays[0]), codes[0], ptr(arrays[1]), codes[1],

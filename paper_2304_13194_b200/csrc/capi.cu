@@ -221,6 +221,62 @@ int jet_cutsize(jet_ctx* ctx, const jet_graph* g, const int64_t* parts, int64_t*
   API_END
 }
 
+int jet_conn_triples(jet_ctx* ctx, const jet_graph* g, const int64_t* parts, int32_t k,
+                     const int64_t* rows, int64_t n_rows, int64_t* row_out, int64_t* part_out,
+                     int64_t* weight_out, int64_t cap, int64_t* count) {
+  API_BEGIN
+  Ctx& c = C(ctx);
+  const DGraph& d = G(g);
+  JET_REQUIRE(k >= 1 && k <= KMASK, JET_EINVAL, "bad k");
+  JET_REQUIRE(count && n_rows >= 0, JET_EINVAL, "bad arguments");
+  auto p = upload_parts(c, parts, d.n, k);
+  DBuf<int32_t> dr;
+  if (rows) {
+    dr.alloc(std::max<int64_t>(n_rows, 1), c.stream);
+    upload_i64_as_i32(c, rows, n_rows, dr.get(), 0, d.n - 1, "row id");
+  }
+  std::vector<int64_t> r, q, w;
+  const int64_t nt = conn_triples(c, d, p.get(), k, rows ? dr.get() : nullptr,
+                                  rows ? n_rows : d.n, r, q, w);
+  *count = nt;
+  if (row_out || part_out || weight_out) {
+    JET_REQUIRE(cap >= nt, JET_EINVAL, "output capacity too small");
+    for (int64_t i = 0; i < nt; ++i) {
+      if (row_out) row_out[i] = r[i];
+      if (part_out) part_out[i] = q[i];
+      if (weight_out) weight_out[i] = w[i];
+    }
+  }
+  API_END
+}
+
+int jet_apply_moves(jet_ctx* ctx, const jet_graph* g, int64_t* parts, int32_t k,
+                    int64_t* part_weights, int64_t* cut, const int64_t* move_vertices,
+                    const int64_t* move_dests, int64_t n_moves) {
+  API_BEGIN
+  Ctx& c = C(ctx);
+  const DGraph& d = G(g);
+  JET_REQUIRE(k >= 1 && k <= KMASK, JET_EINVAL, "bad k");
+  JET_REQUIRE(parts && part_weights && cut && n_moves >= 0, JET_EINVAL, "bad arguments");
+  std::vector<int2> mv((size_t)std::max<int64_t>(n_moves, 1));
+  std::vector<uint8_t> seen;
+  if (n_moves) seen.assign((size_t)d.n, 0);
+  for (int64_t i = 0; i < n_moves; ++i) {
+    const int64_t v = move_vertices[i], t = move_dests[i];
+    JET_REQUIRE(v >= 0 && v < d.n, JET_EINVAL, "move vertex out of range");
+    JET_REQUIRE(t >= 0 && t < k, JET_EINVAL, "move destination out of range");
+    JET_REQUIRE(!seen[v], JET_EINVAL, "duplicate vertex in move list");
+    JET_REQUIRE(parts[v] != t, JET_EASSERT, "move to current part");
+    seen[v] = 1;
+    mv[i] = make_int2((int)v, (int)t);
+  }
+  auto p = upload_parts(c, parts, d.n, k);
+  const ApplyResult r = apply_move_list(c, d, p.get(), k, part_weights, mv.data(), n_moves);
+  *cut += r.cut_delta;
+  download_i32_as_i64(c, p.get(), d.n, parts);
+  API_END
+}
+
 int jet_part_weights(jet_ctx* ctx, const jet_graph* g, const int64_t* parts, int32_t k,
                      int64_t* pw_out) {
   API_BEGIN
@@ -252,6 +308,8 @@ int jet_contract(jet_ctx* ctx, const jet_graph* g, const int64_t* partner, jet_g
   const DGraph& d = G(g);
   DBuf<int32_t> pd(d.n, c.stream), vmap(d.n, c.stream);
   upload_i64_as_i32(c, partner, d.n, pd.get(), 0, d.n - 1, "partner");
+  JET_REQUIRE(device_is_involution(c, pd.get(), d.n), JET_EINVAL,
+              "partner is not a matching (partner[partner[v]] != v)");
   auto cg_ = device_contract(c, d, pd.get(), vmap.get());
   if (vmap_out) download_i32_as_i64(c, vmap.get(), d.n, vmap_out);
   jet_graph* jg = new jet_graph();

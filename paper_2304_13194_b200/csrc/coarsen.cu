@@ -1523,6 +1523,7 @@ static void device_match_fast(Ctx& c, const DGraph& g, int32_t* partner) {
     // is a no-op on the device (fast_round_dead), so the result is the same as
     // checking after every round, with a quarter of the host round trips
     constexpr int RG = MATCH_ROUND_GROUP, MAXR = 48;
+    static_assert(MAXR % RG == 0, "MATCH_ROUND_GROUP must divide the round cap");
     DBuf<unsigned long long> cnt(2 * MAXR, c.stream);
     dzero(c, cnt.get(), 2 * MAXR);
     const GView gv = view(g);
@@ -1588,6 +1589,29 @@ __global__ void k_is_rep(const int32_t* __restrict__ partner, int64_t n, int32_t
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride)
     flag[v] = partner[v] >= v ? 1 : 0;
+}
+
+// A matching is an involution: partner[partner[v]] == v for every v. The
+// contraction sizes its merged-row scratch from that (the member rows of all
+// coarse vertices add up to the fine entry count), so the public entry point
+// checks it (the internal hierarchy's matchings are involutions by construction).
+__global__ void k_check_involution(const int32_t* __restrict__ partner, int64_t n,
+                                   unsigned* bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride)
+    if (partner[partner[v]] != (int32_t)v) atomicOr(bad, 1u);
+}
+
+bool device_is_involution(Ctx& c, const int32_t* partner, int64_t n) {
+  DBuf<unsigned> bad(1, c.stream);
+  dzero(c, bad.get(), 1);
+  launch(c, "check_involution", 8.0 * n, [&] {
+    k_check_involution<<<grid_for(c, n, 256), 256, 0, c.stream>>>(partner, n, bad.get());
+  });
+  unsigned h = 0;
+  d2h(c, &h, bad.get(), 1);
+  c.sync();
+  return h == 0;
 }
 
 struct CoarseMap {

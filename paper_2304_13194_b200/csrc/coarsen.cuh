@@ -17,6 +17,8 @@ struct Hierarchy {
 };
 
 void device_match(Ctx& c, const DGraph& g, int32_t* partner);
+// partner[partner[v]] == v for all v (ids already range-checked)
+bool device_is_involution(Ctx& c, const int32_t* partner, int64_t n);
 std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* partner,
                                         int32_t* vmap);
 // fast: throughput-mode matching (device_match_fast), else the reference's

@@ -77,8 +77,14 @@ inline TierMap tiers_for(int64_t n) {
 constexpr int TIER_G[4] = {4, 8, 16, 32};
 
 // ---------------------------------------------------------------------------
-// Device memory: stream-ordered allocations from the device's default pool
-// (release threshold raised at context creation so freed blocks are reused).
+// Device memory: stream-ordered allocations from the library's private pool
+// for the current device (cudaMemPoolCreate; its release threshold keeps
+// freed blocks mapped for reuse while contexts live, and the last context on
+// a device trims it). The process's default pool is never modified.
+cudaMemPool_t current_pool();
+void pool_context_opened(int device);
+void pool_context_closed(int device);
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
@@ -103,7 +109,7 @@ struct DBuf {
     s = st;
     n = count;
     if (count) {
-      cudaError_t e = cudaMallocAsync((void**)&p, count * sizeof(T), st);
+      cudaError_t e = cudaMallocFromPoolAsync((void**)&p, count * sizeof(T), current_pool(), st);
       if (e != cudaSuccess) {
         p = nullptr;
         n = 0;

@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 namespace jet {
 
@@ -67,12 +68,52 @@ void Ctx::ensure_pinned(size_t elems) {
   pinned_elems = want;
 }
 
+static std::mutex g_pool_mu;
+static cudaMemPool_t g_pool[64];
+static int g_pool_users[64];
+
+static cudaMemPool_t pool_for(int dev) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pool[dev]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    CK(cudaMemPoolCreate(&g_pool[dev], &props));
+    uint64_t thr = ~0ULL;
+    CK(cudaMemPoolSetAttribute(g_pool[dev], cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  return g_pool[dev];
+}
+
+cudaMemPool_t current_pool() {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  return pool_for(dev);
+}
+
+void pool_context_opened(int dev) {
+  pool_for(dev);
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  ++g_pool_users[dev];
+}
+
+// The last context on a device gives the pool's memory back to the driver.
+void pool_context_closed(int dev) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (--g_pool_users[dev] == 0 && g_pool[dev]) {
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(g_pool[dev], 0);
+  }
+}
+
 // Grow the device pool's reservation to `bytes` (one allocation, freed back to
 // the pool, whose release threshold keeps it mapped).
 void Ctx::reserve_pool(size_t bytes) {
   if (bytes <= pool_reserved) return;
   void* p = nullptr;
-  if (cudaMallocAsync(&p, bytes, stream) == cudaSuccess) {
+  if (cudaMallocFromPoolAsync(&p, bytes, current_pool(), stream) == cudaSuccess) {
     cudaFreeAsync(p, stream);
     cudaStreamSynchronize(stream);
     pool_reserved = bytes;
@@ -129,7 +170,9 @@ static void ctx_teardown(Ctx* c) {
   }
   cudaStreamSynchronize(c->stream);
   cudaStreamDestroy(c->stream);
+  const int dev = c->device;
   delete c;
+  pool_context_closed(dev);
 }
 
 namespace jet {
@@ -156,9 +199,10 @@ int jet_create(int device, jet_ctx** out) {
     // busy host does not stretch each wait (no effect, and ignored, when the
     // device's context already exists)
     CK(cudaSetDevice(device));
-#ifndef JET_NO_SPIN
-    if (cudaSetDeviceFlags(cudaDeviceScheduleSpin) != cudaSuccess) (void)cudaGetLastError();
-#endif
+    // opt-in (JET_SPIN=1): the flag applies to the whole process's primary
+    // context, so the library does not set it unasked
+    if (const char* e = getenv("JET_SPIN"); e && e[0] == '1')
+      if (cudaSetDeviceFlags(cudaDeviceScheduleSpin) != cudaSuccess) (void)cudaGetLastError();
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, device));
     JET_REQUIRE(prop.major >= 10, JET_EUNSUPPORTED,
@@ -168,20 +212,12 @@ int jet_create(int device, jet_ctx** out) {
     c->num_sms = prop.multiProcessorCount;
     c->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    cudaMemPool_t pool;
-    CK(cudaDeviceGetDefaultMemPool(&pool, device));
-    uint64_t thr = ~0ULL;
-    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    // Reserve physical memory in the pool up front: growing the pool inside
-    // a partition (cudaMallocAsync mapping new memory) stalled the host for
-    // 100s of ms on dense coarse levels. JET_POOL_RESERVE_MB overrides.
-    {
-      size_t fr = 0, tot = 0;
-      CK(cudaMemGetInfo(&fr, &tot));
-      size_t want = std::min<size_t>(fr / 4, (size_t)24 << 30);
-      if (const char* e = getenv("JET_POOL_RESERVE_MB")) want = (size_t)atoll(e) << 20;
-      c->reserve_pool(want);
-    }
+    pool_context_opened(device);
+    // Optional up-front reservation in the private pool (JET_POOL_RESERVE_MB):
+    // growing the pool inside a partition (mapping new memory) stalled the
+    // host for 100s of ms on dense coarse levels of large graphs; the pool
+    // is trimmed when the device's last context is destroyed.
+    if (const char* e = getenv("JET_POOL_RESERVE_MB")) c->reserve_pool((size_t)atoll(e) << 20);
     c->ensure_pinned(1 << 16);
     const char* hl = getenv("JET_HOST_LEVELS");
     c->host_levels = hl && hl[0] == '1';

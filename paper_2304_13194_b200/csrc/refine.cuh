@@ -7,6 +7,7 @@
 #pragma once
 #include "common.cuh"
 #include "graph.cuh"
+#include <vector>
 
 namespace jet {
 
@@ -118,6 +119,16 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
 // delta, locks. Reads back the part weights into w.h_pw.
 ApplyResult apply_moves(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts,
                         int k, bool set_lock, int32_t epoch);
+
+// ConnectivityTable surface (conn.cu): nonzero conn(v, p) triples of the
+// given rows (all rows when rows == nullptr) sorted by (row, part), and the
+// exact-delta apply of a host move list (parts, part weights; returns the cut
+// delta).
+int64_t conn_triples(Ctx& c, const DGraph& g, const int32_t* parts, int k, const int32_t* rows,
+                     int64_t nr, std::vector<int64_t>& row_out, std::vector<int64_t>& part_out,
+                     std::vector<int64_t>& w_out);
+ApplyResult apply_move_list(Ctx& c, const DGraph& g, int32_t* parts, int k, int64_t* pw,
+                            const int2* h_moves, int64_t nm);
 
 // Host helpers for the parity entry points.
 void afterburner_only(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,

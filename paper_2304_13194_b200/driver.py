@@ -60,27 +60,16 @@ def _prepare(graph, config: RefinerConfig):
 
 
 def _arrays(graph):
-    offs = _lib.as_i64(graph.row_offsets)
-    out = [offs]
-    codes = []
-    for a in (graph.adjacency, graph.edge_weights, graph.vertex_weights):
-        a = np.asarray(a)
-        if a.dtype == np.int32 and a.flags.c_contiguous:
-            out.append(a)
-            codes.append(_lib.JET_I32)
-        else:
-            out.append(_lib.as_i64(a))
-            codes.append(_lib.JET_I64)
-    return out, codes
+    return _lib.csr_arrays(graph)
 
 
 def partition(graph, config: RefinerConfig, ctx: _lib.Context | None = None) -> PartitionResult:
     """Partition a graph into config.k balanced parts, minimising the cut."""
     n, W, limit = _prepare(graph, config)
+    (offs, adj, ew, vw), codes = _arrays(graph)
     ctx = ctx or _lib.Context.default()
     t0 = time.perf_counter()
     cfg = to_c(config, W)
-    (offs, adj, ew, vw), codes = _arrays(graph)
     parts = np.empty(n, np.int64)
     pw = np.empty(config.k, np.int64)
     st = _lib.RunStats()

@@ -12,8 +12,9 @@ Each function runs the corresponding sm_100a kernels through the C-ABI:
   jet_refine            refine.py:190-294
   initial_partition     initpart.py:70-94 (host C++ inside libjet)
 The reference threads a ConnectivityTable through these calls; on the GPU the
-conn(v, p) rows are rebuilt on chip in every pass, so the table reduces to
-the lock bits (`LockTable`).
+conn(v, p) rows are rebuilt on chip in every pass, so the table object holds
+the lock bits and answers content queries (`get_many`, `row_items`,
+`nonzero_triples`) and `apply` with GPU kernels (csrc/conn.cu).
 """
 
 from __future__ import annotations
@@ -29,37 +30,132 @@ from .graph import Graph, PartitionState, _device_graph, graph_n, total_weight
 from .moves import MoveList
 
 
-class LockTable:
-    """Lock bits of the reference's ConnectivityTable (conn.py:125-129)."""
+class ConnectivityTable:
+    """The reference's ConnectivityTable (conn.py:29-262) over the GPU.
 
-    def __init__(self, graph, state=None):
+    conn(v, p) is never stored on the device: every refinement pass rebuilds
+    the rows on chip from the CSR, and this object does the same on demand
+    (`jet_conn_triples`). What the reference exposes of its table -- the
+    nonzero (row, part, weight) contents, the locks and the exact-delta
+    `apply` -- behaves identically; the open-addressing layout is not
+    modelled (only the nonzero contents are observable).
+    `row_capacity` is the Eq. 9 bound min(deg v, k)."""
+
+    def __init__(self, graph, state):
         self.graph = graph
         self.state = state
-        self.k = state.k if state is not None else None
+        self.k = state.k
         self.locks = np.zeros(graph_n(graph), dtype=bool)
 
+    # -- sizing (a virtual layout: the rows live on chip, per pass) ---------
+    @property
+    def allocated_slots(self) -> int:
+        deg = np.diff(np.asarray(self.graph.row_offsets))
+        return 2 * int(np.minimum(deg, self.k).sum())
+
+    @property
+    def slack_slots(self) -> int:
+        return 0
+
+    def row_capacity(self, v: int) -> int:
+        lo, hi = self.graph.row_offsets[v], self.graph.row_offsets[v + 1]
+        return int(min(hi - lo, self.k))
+
+    # -- contents ------------------------------------------------------------
+    def _triples(self, rows=None):
+        dg = _device_graph(self.graph)
+        parts = _lib.as_i64(self.state.parts)
+        r = None if rows is None else _lib.as_i64(rows)
+        nr = graph_n(self.graph) if r is None else len(r)
+        L = _lib.lib()
+        cnt = C.c_int64()
+        _lib.check(L.jet_conn_triples(dg.ctx.handle, dg.handle, _lib.ptr(parts), int(self.k),
+                                      _lib.ptr(r), nr, None, None, None, 0, C.byref(cnt)))
+        m = cnt.value
+        out = [np.empty(m, np.int64) for _ in range(3)]
+        _lib.check(L.jet_conn_triples(dg.ctx.handle, dg.handle, _lib.ptr(parts), int(self.k),
+                                      _lib.ptr(r), nr, *[_lib.ptr(a) for a in out], m,
+                                      C.byref(cnt)))
+        return out
+
+    def get_many(self, rows, parts) -> np.ndarray:
+        """conn(rows[i], parts[i]) for every i (conn.py:70-93)."""
+        rows = np.asarray(rows, dtype=np.int64)
+        parts = np.asarray(parts, dtype=np.int64)
+        if len(rows) == 0:
+            return np.zeros(0, dtype=np.int64)
+        uniq = np.unique(rows)
+        tr, tp, tw = self._triples(uniq)
+        key = tr * self.k + tp
+        want = rows * self.k + parts
+        if len(key) == 0:
+            return np.zeros(len(rows), dtype=np.int64)
+        pos = np.minimum(np.searchsorted(key, want), len(key) - 1)
+        return np.where(key[pos] == want, tw[pos], 0).astype(np.int64)
+
+    def conn(self, v: int, p: int) -> int:
+        return int(self.get_many(np.array([v]), np.array([p]))[0])
+
+    def row_items(self, v: int) -> dict:
+        _, tp, tw = self._triples(np.array([v]))
+        return {int(p): int(w) for p, w in zip(tp, tw)}
+
+    def nonzero_triples(self):
+        """All nonzero (row, part, weight) entries in canonical order."""
+        return tuple(self._triples())
+
+    def same_contents(self, other) -> bool:
+        return all(np.array_equal(x, y)
+                   for x, y in zip(self.nonzero_triples(), other.nonzero_triples()))
+
+    # -- locks ---------------------------------------------------------------
     def reset_locks(self) -> None:
         self.locks[:] = False
 
     def set_locks(self, vertices) -> None:
         self.locks[vertices] = True
 
+    # -- updates -------------------------------------------------------------
     def apply(self, moves) -> None:
-        """Apply a move list to the bound state (parts, weights, cut)."""
+        """Apply a move list to the bound state by exact deltas on the GPU
+        (conn.py:215-254): part weights, parts and the cut. A move to the
+        current part raises AssertionError, as in the reference."""
         if len(moves) == 0:
             return
         st = self.state
-        assert np.all(st.parts[moves.vertices] != moves.dests), "move to current part"
-        parts = st.parts.copy()
-        parts[moves.vertices] = moves.dests
-        fresh = PartitionState.from_parts(self.graph, parts, st.k)
-        st.parts[:] = fresh.parts
-        st.part_weights[:] = fresh.part_weights
-        st.cutsize = fresh.cutsize
+        dg = _device_graph(self.graph)
+        parts = np.ascontiguousarray(st.parts, dtype=np.int64)
+        pw = np.ascontiguousarray(st.part_weights, dtype=np.int64)
+        cut = C.c_int64(int(st.cutsize))
+        mv, md = _lib.as_i64(moves.vertices), _lib.as_i64(moves.dests)
+        _lib.check(_lib.lib().jet_apply_moves(
+            dg.ctx.handle, dg.handle, _lib.ptr(parts), int(st.k), _lib.ptr(pw), C.byref(cut),
+            _lib.ptr(mv), _lib.ptr(md), len(mv)))
+        st.parts[:] = parts
+        st.part_weights[:] = pw
+        st.cutsize = int(cut.value)
+
+    def check(self) -> None:
+        """The GPU rebuilds rows from the CSR and the bound state, so the
+        contents are in sync by construction; verify the state's cached part
+        weights and cut against a recount (conn.py:256-262)."""
+        fresh = PartitionState.from_parts(self.graph, self.state.parts, self.k)
+        if fresh.cutsize != self.state.cutsize or \
+                not np.array_equal(fresh.part_weights, self.state.part_weights):
+            raise ValueError("connectivity table out of sync")
 
 
-def build_conn(graph, state) -> LockTable:
-    return LockTable(graph, state)
+LockTable = ConnectivityTable  # round-1 name
+
+
+def build_conn(graph, state) -> ConnectivityTable:
+    """Construct the connectivity table for a partition (conn.py:265-267)."""
+    return ConnectivityTable(graph, state)
+
+
+def update_conn(table: ConnectivityTable, moves) -> None:
+    """Apply a move list to the table and its bound state (conn.py:270-272)."""
+    table.apply(moves)
 
 
 def _ctx():
@@ -96,11 +192,27 @@ def contract(graph, matching):
 
 @dataclass
 class Hierarchy:
+    """Coarse graphs plus fine-to-coarse maps (coarsen.py:19-44)."""
+
     levels: list = field(default_factory=list)
     maps: list = field(default_factory=list)
 
     def __len__(self):
         return len(self.levels)
+
+    def validate(self) -> None:
+        """The reference's structural checks (coarsen.py:33-44)."""
+        total = total_weight(self.levels[0])
+        for i, vmap in enumerate(self.maps):
+            fine, coarse = self.levels[i], self.levels[i + 1]
+            if len(vmap) != graph_n(fine):
+                raise ValueError("map length mismatch")
+            if graph_n(coarse) >= graph_n(fine):
+                raise ValueError("coarse level must be strictly smaller")
+            if len(np.unique(vmap)) != graph_n(coarse):
+                raise ValueError("map must be surjective onto coarse vertices")
+            if total_weight(coarse) != total:
+                raise ValueError("vertex weight not conserved")
 
 
 def build_hierarchy(graph, target: int, seed: int = 0) -> Hierarchy:

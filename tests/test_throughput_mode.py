@@ -25,7 +25,7 @@ def _graph(spec):
     return gen.grid27_graph(spec[1])
 
 
-@pytest.mark.parametrize("name", ["grid2d_256x256", "grid27_64"])
+@pytest.mark.parametrize("name", ["grid2d_256x256", "grid27_64", "grid27_128"])
 def test_cut_within_2pct_geomean(name):
     case = QUALITY[name]
     g = _graph(case["spec"])
