@@ -33,6 +33,12 @@ namespace jet {
 #define LV_MIN_BLOCKS 2
 #endif
 constexpr int LV_BLOCK = LV_BLOCK_SIZE;
+#ifndef LV_CLUSTER_N
+#define LV_CLUSTER_N 65536  // levels up to this many vertices run as one cluster
+#endif
+#ifndef LV_CLUSTER_MAX
+#define LV_CLUSTER_MAX 16
+#endif
 constexpr int LV_TAIL_SMEM = 8192;  // evicted keys sorted in shared memory
 constexpr int LV_DRAW_SLACK = 64;
 constexpr int64_t LV_ROWS_PER_BLOCK = 128;  // measured: 512 -> 128 saves ~2 ms on 128^3
@@ -121,7 +127,15 @@ struct LevelArgs {
   int trace_cap;
   unsigned long long* phase_clk;  // optional: clock64 per phase (JET_PHASES)
   unsigned long long* work;       // {stats rows, entries, ab rows, entries, apply rows, entries}
+  int cluster_sync;  // the grid is one thread-block cluster: barrier.cluster between phases
 };
+
+// All threads of the cluster; release/acquire at cluster scope orders the
+// phases' global-memory writes for every CTA (the wait invalidates L1).
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
 
 // phase timer for block 0 / thread 0 (diagnostics only)
 __device__ __forceinline__ long long dev_clock() {
@@ -666,8 +680,10 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
   // also orders global memory within the block; the grid barrier protocol
   // costs ~1.5 us per phase even for one block
   const bool one_block = gridDim.x == 1;
+  const bool clus = A.cluster_sync != 0;
   auto gsync = [&]() {
     if (one_block) __syncthreads();
+    else if (clus) cluster_barrier();
     else grid.sync();
   };
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -960,6 +976,43 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
 }
 
 // ------------------------------------------------------------------ host
+// Largest cluster (<= 16 CTAs, non-portable above 8) the level kernel can be
+// launched with at this shared-memory size; 0 when clusters are unavailable.
+static int level_cluster_max(Ctx& c, const void* kern, size_t smem) {
+  static std::map<std::pair<const void*, size_t>, int> cache;
+  auto key = std::make_pair(kern, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int best = 0;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+    (void)cudaGetLastError();
+  for (int cs = LV_CLUSTER_MAX; cs >= 2; cs /= 2) {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(cs);
+    lc.blockDim = dim3(LV_BLOCK);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = c.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    int nclus = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclus, kern, &lc) != cudaSuccess) {
+      (void)cudaGetLastError();
+      continue;
+    }
+    if (nclus >= 1) {
+      best = cs;
+      break;
+    }
+  }
+  cache[key] = best;
+  return best;
+}
+
 static int ceil_log2_host(int64_t x) {
   int r = 0;
   while ((1LL << r) < x) ++r;
@@ -1157,12 +1210,42 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
     const char* e = getenv("JET_LV_ONE_BLOCK_N");
     return e ? (int64_t)atoll(e) : (int64_t)0;
   }();
-  const int blocks = g.n <= one_block_n
-                         ? 1
-                         : (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * c.num_sms));
+  int blocks = g.n <= one_block_n
+                   ? 1
+                   : (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * c.num_sms));
+  // Small levels: the whole grid is one thread-block cluster of up to 16
+  // CTAs synchronised with barrier.cluster (~0.2 us) instead of the
+  // cooperative grid barrier (~1.4 us); each pass has ~10-12 barriers.
+  static const int64_t cluster_n = [] {
+    const char* e = getenv("JET_LV_CLUSTER_N");
+    return e ? (int64_t)atoll(e) : (int64_t)LV_CLUSTER_N;
+  }();
+  int cl = 0;
+  if (blocks > 1 && g.n <= cluster_n) {
+    cl = std::min(blocks, level_cluster_max(c, kern, smem));
+    if (cl < 2) cl = 0;
+  }
+  A.cluster_sync = cl ? 1 : 0;
+  if (cl) blocks = cl;
   void* args[] = {&A};
   launch(c, "refine_level", 0.0, [&] {
-    CK(cudaLaunchCooperativeKernel(kern, dim3(blocks), dim3(LV_BLOCK), args, smem, c.stream));
+    if (cl) {
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(cl);
+      lc.blockDim = dim3(LV_BLOCK);
+      lc.dynamicSmemBytes = smem;
+      lc.stream = c.stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cl;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      CK(cudaLaunchKernelExC(&lc, kern, args));
+    } else {
+      CK(cudaLaunchCooperativeKernel(kern, dim3(blocks), dim3(LV_BLOCK), args, smem, c.stream));
+    }
   });
   d2h(c, &h, S.ctl.get(), 1);
   unsigned long long wk[8];
