@@ -8,7 +8,8 @@ names. All compute runs in hand-written sm_100a CUDA kernels in libjet.so.
 
 from .config import RefinerConfig, rebalance_thresholds
 from .driver import PartitionResult, partition, project
-from .errors import BalanceInfeasibleError, JetpartError, RebalanceInfeasibleError
+from .errors import (BalanceInfeasibleError, JetpartError, ParseError, PreprocessError,
+                     RebalanceInfeasibleError)
 from .graph import (
     Graph,
     PartitionState,
@@ -42,7 +43,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BalanceInfeasibleError", "ConnectivityTable", "Context", "DeviceGraph", "Graph", "Hierarchy", "JetpartError",
-    "LockTable", "MoveList", "PartitionResult", "PartitionState", "RebalanceInfeasibleError",
+    "LockTable", "MoveList", "ParseError", "PreprocessError", "PartitionResult", "PartitionState", "RebalanceInfeasibleError",
     "RefinerConfig", "afterburner", "build_conn", "build_hierarchy", "contract", "cutsize",
     "from_edge_arrays", "imbalance_of", "initial_partition", "is_balanced", "jet_refine",
     "jetlp_pass", "match_vertices", "part_weight_limit", "partition", "project",

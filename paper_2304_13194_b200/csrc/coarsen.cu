@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <climits>
 
 namespace jet {
 
@@ -1838,6 +1839,12 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+__global__ void k_rebase(const int64_t* __restrict__ off, int64_t cnt, int64_t base, int64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = off[i] - base;
+}
+
 __global__ void k_copy_rows(const int64_t* __restrict__ toff, const int64_t* __restrict__ coffs,
                             const int32_t* __restrict__ tadj, const int32_t* __restrict__ tew,
                             int32_t* cadj, int32_t* cew, int64_t nc) {
@@ -1952,7 +1959,7 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
     launch(c, "big_gather", 20.0 * BT, [&] {
       k_big_gather<<<grid_for(c, nb * 256, 256), 256, 0, c.stream>>>(rm, big_p, nb, boff.get(), bk.get());
     });
-    {
+    if (BT < (int64_t)INT_MAX) {
       size_t tmp = 0;
       CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, bk.get(), bk2.get(), (int)BT, (int)nb, boff.get(),
                                             boff.get() + 1, c.stream));
@@ -1961,6 +1968,32 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
         CK(cub::DeviceSegmentedSort::SortKeys(p, tmp, bk.get(), bk2.get(), (int)BT, (int)nb, boff.get(),
                                               boff.get() + 1, c.stream));
       });
+    } else {
+      // CUB's segmented sort counts items in 32 bits: sort groups of rows
+      // holding < 2^30 entries each, with offsets rebased to the group
+      std::vector<int64_t> hb(nb + 1);
+      d2h(c, hb.data(), boff.get(), nb + 1);
+      c.sync();
+      DBuf<int64_t> rel(nb + 1, c.stream);
+      int64_t s0 = 0;
+      while (s0 < nb) {
+        int64_t s1 = s0 + 1;
+        while (s1 < nb && hb[s1 + 1] - hb[s0] < (1LL << 30)) ++s1;
+        const int64_t base = hb[s0], cnt = hb[s1] - base, ns = s1 - s0;
+        launch(c, "big_rebase", 16.0 * ns, [&] {
+          k_rebase<<<grid_for(c, ns + 1, 256), 256, 0, c.stream>>>(boff.get() + s0, ns + 1, base,
+                                                                   rel.get());
+        });
+        size_t tmp = 0;
+        CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, bk.get() + base, bk2.get() + base,
+                                              (int)cnt, (int)ns, rel.get(), rel.get() + 1, c.stream));
+        void* p = c.cub_scratch(tmp);
+        launch(c, "big_sort", 32.0 * cnt, [&] {
+          CK(cub::DeviceSegmentedSort::SortKeys(p, tmp, bk.get() + base, bk2.get() + base, (int)cnt,
+                                                (int)ns, rel.get(), rel.get() + 1, c.stream));
+        });
+        s0 = s1;
+      }
     }
     launch(c, "big_dedup", 16.0 * BT, [&] {
       k_big_dedup<<<grid_for(c, nb * 256, 256), 256, 0, c.stream>>>(rm, big_p, nb, boff.get(), bk2.get());

@@ -360,8 +360,15 @@ std::unique_ptr<DGraph> device_rmat(Ctx& c, int scale, int edge_factor, uint64_t
   JET_REQUIRE(scale >= 1 && scale <= 30 && edge_factor >= 1, JET_EINVAL, "bad R-MAT size");
   const uint64_t n = 1ULL << scale;
   const int64_t E = (int64_t)n * edge_factor;
-  JET_REQUIRE(2 * E < (1LL << 31), JET_EUNSUPPORTED,
-              "R-MAT edge list above 2^31 directed entries: not supported on one device");
+  // two 8-byte codes per edge, sorted with a double buffer (2 x 16 B per edge
+  // at the peak), then a 4-byte adjacency and the largest component's CSR
+  {
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    const double need = 32.0 * (double)E + 8.0 * (double)n;
+    JET_REQUIRE(need < 0.9 * (double)(fr + c.pool_reserved), JET_ENOMEM,
+                "R-MAT edge list does not fit in device memory");
+  }
   DBuf<DevPcg> g0 = seed_rng(c, {seed, (uint64_t)scale, (uint64_t)edge_factor});
   DevPcg hg;
   d2h(c, &hg, g0.get(), 1);
@@ -376,30 +383,37 @@ std::unique_ptr<DGraph> device_rmat(Ctx& c, int scale, int edge_factor, uint64_t
   });
   int end_bit = 1;
   while (end_bit < 64 && (1ULL << end_bit) <= n * n) ++end_bit;
+  // 64-bit item counts (2E reaches 2^32 at scale 27, edge factor 16); the
+  // double-buffer form needs no third copy of the keys
+  const int64_t ne = 2 * E;
+  cub::DoubleBuffer<uint64_t> db(codes.get(), sorted.get());
   cub_call(c, "gen_sort", [&](void* p, size_t& t) {
-    return cub::DeviceRadixSort::SortKeys(p, t, codes.get(), sorted.get(), (int)(2 * E), 0,
-                                          end_bit, c.stream);
+    return cub::DeviceRadixSort::SortKeys(p, t, db, ne, 0, end_bit, c.stream);
   });
+  uint64_t* srt = db.Current();
+  uint64_t* uni = db.Alternate();
   DBuf<int64_t> nu(1, c.stream);
   cub_call(c, "gen_unique", [&](void* p, size_t& t) {
-    return cub::DeviceSelect::Unique(p, t, sorted.get(), codes.get(), nu.get(), (int)(2 * E),
-                                     c.stream);
+    return cub::DeviceSelect::Unique(p, t, srt, uni, nu.get(), ne, c.stream);
   });
   int64_t M = 0;
   d2h(c, &M, nu.get(), 1);
   c.sync();
   uint64_t last = 0;
   if (M) {
-    d2h(c, &last, codes.get() + M - 1, 1);
+    d2h(c, &last, uni + M - 1, 1);
     c.sync();
     if (last == n * n) --M;  // the self-loop sentinel
   }
   DBuf<int64_t> offs(n + 1, c.stream);
   DBuf<int32_t> adj(M > 0 ? M : 1, c.stream);
   launch(c, "gen_csr", 0.0, [&] {
-    k_codes_to_csr<<<grid_for(c, M + 1, 256), 256, 0, c.stream>>>(codes.get(), M, n, offs.get(),
+    k_codes_to_csr<<<grid_for(c, M + 1, 256), 256, 0, c.stream>>>(uni, M, n, offs.get(),
                                                                    adj.get());
   });
+  c.cub_tmp.release();
+  codes.release();
+  sorted.release();
   return lcc_graph(c, (int64_t)n, offs, adj);
 }
 

@@ -34,7 +34,7 @@ namespace jet {
 #endif
 constexpr int LV_BLOCK = LV_BLOCK_SIZE;
 #ifndef LV_CLUSTER_N
-#define LV_CLUSTER_N 65536  // levels up to this many vertices run as one cluster
+#define LV_CLUSTER_N 0  // levels up to this many vertices run as one cluster (0: off; measured slower)
 #endif
 #ifndef LV_CLUSTER_MAX
 #define LV_CLUSTER_MAX 16

@@ -129,6 +129,16 @@ class PartitionState:
     def copy(self) -> "PartitionState":
         return PartitionState(self.parts.copy(), self.k, self.part_weights.copy(), self.cutsize)
 
+    def check(self, graph) -> None:
+        """Verify the cached part weights and cutsize (graph.py:250-258)."""
+        fresh = PartitionState.from_parts(graph, self.parts, self.k)
+        if not np.array_equal(fresh.part_weights, self.part_weights):
+            raise ValueError("cached part weights are stale")
+        if fresh.cutsize != self.cutsize:
+            raise ValueError("cached cutsize is stale")
+        if int(np.asarray(self.part_weights).sum()) != total_weight(graph):
+            raise ValueError("part weights do not sum to total vertex weight")
+
 
 def is_balanced(state, imbalance: float, total_weight=None) -> bool:
     if total_weight is None:
