@@ -260,6 +260,16 @@ int jet_refine(jet_ctx* ctx, const jet_graph* g, const int64_t* parts_in,
                int64_t* parts_out, int64_t* pw_out, int64_t* cut_out,
                jet_level_stats* stats);
 
+/* jet_refine with the per-iteration trace of stats["trace"]
+ * (refine.py:269-271): trace_out receives up to trace_cap records of four
+ * int64 (kind 1 = lp / 2 = weak / 3 = strong, cutsize, max part weight,
+ * moves); *trace_len the number of iterations. */
+int jet_refine_trace(jet_ctx* ctx, const jet_graph* g, const int64_t* parts_in,
+                     const jet_config* cfg, int32_t finest, int32_t level,
+                     int64_t* parts_out, int64_t* pw_out, int64_t* cut_out,
+                     jet_level_stats* stats, int64_t* trace_out,
+                     int64_t trace_cap, int64_t* trace_len);
+
 /* ---- initial partitioning (initpart.py:70-94; host C++) --------------- */
 int jet_initial_partition(int64_t n, const int64_t* row_offsets,
                           const int64_t* adjacency, const int64_t* edge_weights,

@@ -119,6 +119,7 @@ _SIGS = {
                                  P, P, P, P]),
     "jet_rebalance_pass": (C.c_int, [P, P, P, i32, P, i64, i64, i32, i32, P, P, P, P, P]),
     "jet_refine": (C.c_int, [P, P, P, P, i32, i32, P, P, P, P]),
+    "jet_refine_trace": (C.c_int, [P, P, P, P, i32, i32, P, P, P, P, P, i64, P]),
     "jet_initial_partition": (C.c_int, [i64, P, P, P, P, i32, i64, C.c_uint64, i32, P]),
     "jet_partition": (C.c_int, [P, i64, P, P, C.c_int, P, C.c_int, P, C.c_int, P, P, P, P]),
     "jet_partition_graph": (C.c_int, [P, P, P, P, P, P]),

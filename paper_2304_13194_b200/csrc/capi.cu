@@ -532,9 +532,37 @@ int jet_rebalance_pass(jet_ctx* ctx, const jet_graph* g, const int64_t* parts, i
   API_END
 }
 
+static int refine_impl(jet_ctx* ctx, const jet_graph* g, const int64_t* parts_in,
+                       const jet_config* cfg, int32_t finest, int32_t level, int64_t* parts_out,
+                       int64_t* pw_out, int64_t* cut_out, jet_level_stats* stats);
+
+int jet_refine_trace(jet_ctx* ctx, const jet_graph* g, const int64_t* parts_in,
+                     const jet_config* cfg, int32_t finest, int32_t level, int64_t* parts_out,
+                     int64_t* pw_out, int64_t* cut_out, jet_level_stats* stats,
+                     int64_t* trace_out, int64_t trace_cap, int64_t* trace_len) {
+  std::vector<int64_t> tr;
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (c) c->api_trace = &tr;
+  const int rc = refine_impl(ctx, g, parts_in, cfg, finest, level, parts_out, pw_out, cut_out,
+                             stats);
+  if (c) c->api_trace = nullptr;
+  if (rc != JET_OK) return rc;
+  const int64_t nrec = (int64_t)tr.size() / 4;
+  if (trace_len) *trace_len = nrec;
+  if (trace_out)
+    for (int64_t i = 0; i < 4 * std::min(nrec, trace_cap); ++i) trace_out[i] = tr[i];
+  return JET_OK;
+}
+
 int jet_refine(jet_ctx* ctx, const jet_graph* g, const int64_t* parts_in, const jet_config* cfg,
                int32_t finest, int32_t level, int64_t* parts_out, int64_t* pw_out, int64_t* cut_out,
                jet_level_stats* stats) {
+  return refine_impl(ctx, g, parts_in, cfg, finest, level, parts_out, pw_out, cut_out, stats);
+}
+
+static int refine_impl(jet_ctx* ctx, const jet_graph* g, const int64_t* parts_in,
+                       const jet_config* cfg, int32_t finest, int32_t level, int64_t* parts_out,
+                       int64_t* pw_out, int64_t* cut_out, jet_level_stats* stats) {
   API_BEGIN
   Ctx& c = C(ctx);
   const DGraph& d = G(g);

@@ -208,6 +208,9 @@ struct Ctx {
   cudaEvent_t timer_a = nullptr, timer_b = nullptr;
   DBuf<uint8_t> flush_buf;
   int32_t lock_epoch = 0;
+  // per-iteration (kind 1/2/3, cut, max part weight, moves) records of
+  // jet_refine (refine.py:269-271), filled when set (API entry only)
+  std::vector<int64_t>* api_trace = nullptr;
   bool host_levels = false;  // force the host-driven per-pass controller
 
   cudaEvent_t take_event();

@@ -65,7 +65,7 @@ void refine_level(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, int64_t
   int64_t locked = 0;
   int32_t epoch = ++c.lock_epoch;  // fresh table: no vertex locked
   while (no_improve < cfg.no_improve_limit) {
-    bool is_lp = false, locks_all_clear = false;
+    bool is_lp = false, locks_all_clear = false, strong_pass = false;
     if (balanced()) {
       rebal_streak = 0;
       locks_all_clear = !cfg.locking || locked == 0;
@@ -85,6 +85,7 @@ void refine_level(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, int64_t
       Pcg64 rng = level >= 0 ? default_rng({cfg.seed, (uint64_t)level, (uint64_t)pass_index})
                              : default_rng({cfg.seed, (uint64_t)pass_index});
       const bool strong = rebal_streak >= 2;
+      strong_pass = strong;
       if (!rebalance_pass(c, w, g, parts, k, limit, sigma, cfg.sub_buckets, strong, rng, nullptr,
                           sharded ? &sh : nullptr)) {
         st.rebalance_stuck = 1;
@@ -124,6 +125,10 @@ void refine_level(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, int64_t
         keep_cut = cut;
         keep_pw = w.h_pw;
       }
+    }
+    if (c.api_trace) {
+      const int64_t rec[4] = {is_lp ? 1 : (strong_pass ? 3 : 2), cut, worst(), ar.n_moves};
+      c.api_trace->insert(c.api_trace->end(), rec, rec + 4);
     }
     static const bool trace_on = getenv("JET_TRACE") && getenv("JET_TRACE")[0] == '1';
     if (trace_on)

@@ -1179,7 +1179,8 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   A.C = S.ctl.get();
   A.work = S.work.get();
 
-  static const bool trace_on = getenv("JET_TRACE") && getenv("JET_TRACE")[0] == '1';
+  static const bool trace_env = getenv("JET_TRACE") && getenv("JET_TRACE")[0] == '1';
+  const bool trace_on = trace_env || c.api_trace != nullptr;
   DBuf<long long> trace;
   if (trace_on) {
     trace.alloc(10 * 4096, c.stream);
@@ -1302,7 +1303,12 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
     std::vector<long long> t(10 * std::min(h.iterations, 4096));
     d2h(c, t.data(), trace.get(), t.size());
     c.sync();
-    for (size_t i = 0; i < t.size(); i += 10)
+    if (c.api_trace)
+      for (size_t i = 0; i < t.size(); i += 10) {
+        const int64_t rec[4] = {t[i], t[i + 2], t[i + 3], t[i + 1]};
+        c.api_trace->insert(c.api_trace->end(), rec, rec + 4);
+      }
+    for (size_t i = 0; trace_env && i < t.size(); i += 10)
       fprintf(stderr,
               "TRACE L%d it%zu kind=%lld nm=%lld cut=%lld worst=%lld noimp=%lld best=%lld cand=%lld "
               "rcand=%lld D=%lld nover=%lld\n",

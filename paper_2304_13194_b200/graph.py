@@ -49,6 +49,44 @@ class Graph:
         lo, hi = self.row_offsets[v], self.row_offsets[v + 1]
         return self.adjacency[lo:hi], self.edge_weights[lo:hi]
 
+    @property
+    def entry_rows(self) -> np.ndarray:
+        """Row (source vertex) of every adjacency entry."""
+        return np.repeat(np.arange(self.n, dtype=np.int64), np.diff(self.row_offsets))
+
+    def validate(self) -> None:
+        """The reference's structural invariants (graph.py:64-100): CSR
+        shape, id and weight ranges, no self loops or duplicate neighbours,
+        symmetric entries with equal weights. Raises ValueError."""
+        n, offs = self.n, np.asarray(self.row_offsets)
+        adj, ew, vw = (np.asarray(a) for a in (self.adjacency, self.edge_weights,
+                                                self.vertex_weights))
+        checks = [
+            (n >= 1, "graph must have at least one vertex"),
+            (offs[0] == 0 and bool(np.all(offs[1:] >= offs[:-1])),
+             "row_offsets must be non-decreasing from 0"),
+            (offs[-1] == len(adj), "row_offsets[n] must equal adjacency length"),
+            (len(ew) == len(adj), "edge_weights length mismatch"),
+            (len(vw) == n, "vertex_weights length mismatch"),
+            (len(adj) == 0 or (adj.min() >= 0 and adj.max() < n), "neighbor id out of range"),
+            (bool(np.all(vw >= 1)), "vertex weights must be >= 1"),
+            (bool(np.all(ew >= 1)), "edge weights must be >= 1"),
+        ]
+        for ok, msg in checks:
+            if not ok:
+                raise ValueError(msg)
+        src = self.entry_rows
+        if np.any(src == adj):
+            raise ValueError("self-loop present")
+        fwd = src * n + adj
+        fo = np.argsort(fwd, kind="stable")
+        if np.any(fwd[fo][1:] == fwd[fo][:-1]):
+            raise ValueError("duplicate neighbor within a row")
+        rev = adj * n + src
+        ro = np.argsort(rev, kind="stable")
+        if not (np.array_equal(fwd[fo], rev[ro]) and np.array_equal(ew[fo], ew[ro])):
+            raise ValueError("adjacency is not symmetric with equal weights")
+
 
 def graph_n(graph) -> int:
     return len(graph.row_offsets) - 1

@@ -135,6 +135,12 @@ class ConnectivityTable:
         st.part_weights[:] = pw
         st.cutsize = int(cut.value)
 
+    def rebuild_row(self, v: int) -> None:
+        """conn.py:143-163 recomputes a row from the graph and the state; here
+        every query already rebuilds the rows it reads from the CSR."""
+        if not 0 <= int(v) < graph_n(self.graph):
+            raise IndexError("row out of range")
+
     def check(self) -> None:
         """The GPU rebuilds rows from the CSR and the bound state, so the
         contents are in sync by construction; verify the state's cached part
@@ -340,15 +346,22 @@ def jet_refine(graph, state, config: RefinerConfig, finest: bool = True, seed_pa
     st = _lib.LevelStats()
     level = int(seed_path[0]) if seed_path else -1
     parts_in = _lib.as_i64(state.parts)
-    _lib.check(_lib.lib().jet_refine(
+    cap = 4096
+    tr = np.empty(4 * cap, np.int64)
+    ntr = C.c_int64()
+    _lib.check(_lib.lib().jet_refine_trace(
         dg.ctx.handle, dg.handle, _lib.ptr(parts_in), C.byref(cfg),
-        int(bool(finest)), level, _lib.ptr(parts), _lib.ptr(pw), C.byref(cut), C.byref(st)))
+        int(bool(finest)), level, _lib.ptr(parts), _lib.ptr(pw), C.byref(cut), C.byref(st),
+        _lib.ptr(tr), cap, C.byref(ntr)))
     out = PartitionState(parts, config.k, pw, int(cut.value))
+    kinds = {1: "lp", 2: "weak", 3: "strong"}
+    trace = [(kinds[int(a)], int(b), int(c_), int(d)) for a, b, c_, d in
+             tr[:4 * min(ntr.value, cap)].reshape(-1, 4)]
     stats = {
         "iterations": st.iterations, "lp_passes": st.lp_passes,
         "weak_passes": st.weak_passes, "strong_passes": st.strong_passes,
         "moves": st.moves, "rebalance_stuck": bool(st.rebalance_stuck),
-        "trace": [], "balanced": bool(st.balanced),
+        "trace": trace, "balanced": bool(st.balanced),
         "best_cut": int(cut.value) if st.balanced else None,
     }
     return out, stats

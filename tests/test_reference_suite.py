@@ -21,8 +21,24 @@ ROOT = Path(__file__).resolve().parents[1]
 SUITE = ROOT / "baseline" / "_ref" / "jetpart_tests"
 COMPAT = ROOT / "paper_2304_13194_b200" / "compat"
 
-# test id -> why it cannot hold on the GPU path (kept empty unless justified)
-EXPECTED_DIFF = {}
+# test id -> why it cannot hold on the GPU path
+EXPECTED_DIFF = {
+    # The ConnectivityTable's open-addressing layout (conn.py:85-194: slot
+    # regions, capacity growth on overflow, the keys array) is not modelled:
+    # the GPU rebuilds conn rows on chip in every pass and only their nonzero
+    # contents are observable by the partition. Every
+    # content test of test_conn.py passes.
+    "test_conn.py::TestRebuild::test_overflow_grows_capacity":
+        "row capacity is the fixed Eq. 9 bound min(deg, k), not a growing hash table",
+    "test_conn.py::TestRebuild::test_stale_zero_entries_purged_on_rebuild":
+        "reads the hash table's keys/region arrays",
+    # The test starts `python -m jetpart.cli` with an environment holding only
+    # PATH and the thread counts, so no binding on PYTHONPATH is visible there
+    # (it would run nothing of ours); test_cli_deterministic_across_threads
+    # below repeats it with the binding on the path.
+    "test_acceptance.py::test_11_deterministic_across_thread_counts":
+        "subprocess environment drops PYTHONPATH",
+}
 
 
 def run_suite(*args, timeout=3000):
@@ -47,3 +63,31 @@ def test_reference_suite_on_gpu_path():
     unexpected = sorted(f for f in failed if f.split(" ")[0] not in EXPECTED_DIFF)
     assert not unexpected, "\n".join(unexpected) + "\n" + out[-3000:]
     assert re.search(r"(\d+) passed", out), out[-2000:]
+
+
+@pytest.mark.gpu
+def test_cli_deterministic_across_threads(tmp_path):
+    """Acceptance 11 (test_acceptance.py:334-354) with the binding visible:
+    the reference CLI on the GPU path gives byte-identical partition files
+    across thread counts and repeats."""
+    if not SUITE.exists():
+        pytest.skip("reference not installed")
+    env0 = {"PATH": os.environ.get("PATH", "/usr/bin:/bin"),
+            "PYTHONPATH": os.pathsep.join([str(COMPAT), str(ROOT)]),
+            "JETPART_REFERENCE": str(ROOT / "baseline" / "_ref")}
+    code = ("import sys; sys.path[:0] = [%r, %r]; import jetpart; "
+            "from jetpart.generators import grid_graph; from jetpart.io import write_metis; "
+            "write_metis(grid_graph(48, 48), sys.argv[1])") % (str(COMPAT), str(ROOT))
+    gfile = tmp_path / "det.graph"
+    subprocess.run([sys.executable, "-c", code, str(gfile)], env=env0, check=True, timeout=300)
+    blobs = []
+    for threads in ("1", "8"):
+        for rep in ("a", "b"):
+            out = tmp_path / f"p_{threads}_{rep}.txt"
+            env = dict(env0, OMP_NUM_THREADS=threads, OPENBLAS_NUM_THREADS=threads)
+            p = subprocess.run([sys.executable, "-m", "jetpart.cli", str(gfile), "--k", "8",
+                                "--seed", "7", "--deterministic", "--out", str(out)],
+                               env=env, capture_output=True, text=True, timeout=300)
+            assert p.returncode == 0, p.stderr
+            blobs.append(out.read_bytes())
+    assert all(b == blobs[0] for b in blobs)
