@@ -15,10 +15,11 @@ mode on the same workload is reported alongside ("deterministic_mode").
 `value` times jet_partition_graph on the HBM-resident CSR with CUDA events;
 `e2e` times the public `partition(graph, config)` from host int64 arrays
 (H2D of the CSR and D2H of the parts inside the timed region). The reference
-arm times the CPU oracle (oracle/, a C port of the reference algorithm) on
-the host. N > 1: every rank partitions its own replica (value = N*m / max
-time), or with --shard one partition whose finest levels are sharded over
-the ranks (NCCL; value = m / max time).
+arm times the reference package itself (baseline/_ref: the unmodified
+Python reference, single thread) on the host, or the C port of it (oracle/)
+when it is not installed. N > 1: one partition whose finest levels are
+sharded over the ranks (NCCL; value = m / max time, strong scaling), or with
+--replicas N independent partitions (value = N*m / max time).
 """
 
 from __future__ import annotations
@@ -172,8 +173,61 @@ def cpu_oracle_partition(graph):
     return time.perf_counter() - t, r["cut"]
 
 
+def run_reference_python(args, ref_dir):
+    """The unmodified reference (baseline/_ref, installed from /root/reference
+    with pip) through its public API: jetpart.driver.partition on the same
+    graph (the reference's own Graph class over the same CSR arrays), one
+    thread (the reference is single-threaded numpy). Steps run until a time
+    budget is spent (one 128^3 partition takes ~150-180 s)."""
+    from paper_2304_13194_b200 import generators as gen
+    sys.path.insert(0, str(ref_dir))
+    from jetpart.driver import partition as ref_partition
+    from jetpart.graph import Graph as RefGraph
+    from jetpart.refine import RefinerConfig as RefConfig
+    if not getattr(sys.modules["jetpart"], "__file__", "").startswith(str(ref_dir)):
+        raise RuntimeError("jetpart resolved outside baseline/_ref")
+
+    def ref_graph(g):
+        return RefGraph(g.row_offsets, g.adjacency, g.edge_weights, g.vertex_weights)
+
+    g = ref_graph(gen.grid27_graph(GRID_N))
+    small = ref_graph(gen.grid27_graph(12))
+    for _ in range(args.warmup):
+        ref_partition(small, RefConfig(k=8, imbalance=IMB, seed=SEED))
+    budget = float(os.environ.get("JET_REF_BUDGET_S", "240"))
+    times, cut = [], None
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        r = ref_partition(g, RefConfig(k=K, imbalance=IMB, seed=SEED))
+        times.append(time.perf_counter() - t)
+        cut = int(r.state.cutsize)
+        if sum(times) + times[-1] > budget:
+            break
+    return times, cut, g.m, ("the reference package itself (baseline/_ref, unmodified), "
+                             "jetpart.driver.partition on the same CSR, single thread")
+
+
 def run_reference(args, world, rank):
     if rank != 0:
+        return
+    ref_dir = ROOT / "baseline" / "_ref"
+    if (ref_dir / "jetpart" / "__init__.py").exists() and os.environ.get("JET_REF_IMPL") != "port":
+        times, cut, m, sample = run_reference_python(args, ref_dir)
+        t = statistics.mean(times)
+        v = m / t
+        line = {
+            "metric": "edges/s", "value": v, "unit": "edges/s", "n_gpus": args.gpus,
+            "steps": len(times), "steps_requested": args.steps, "warmup": args.warmup,
+            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": WORKLOAD}, "impl": "reference",
+            "partition_time_s": t, "cutsize": cut,
+            "cpu_baseline": {"value": v, "unit": "edges/s", "cores": 1, "kind": "reference",
+                             "sample": f"full workload per step ({len(times)} step(s) of "
+                                       f"{t:.1f} s within the time budget); " + sample},
+            "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
         return
     from paper_2304_13194_b200 import generators as gen
     g = gen.grid27_graph(GRID_N)
@@ -207,9 +261,14 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-EXTRA_CONFIGS = [  # BASELINE configs 3-4, generated on the device (reference generators)
+EXTRA_CONFIGS = [  # BASELINE configs 3-5, generated on the device (reference generators)
     ("rmat22", "R-MAT scale 22 edgefactor 16 (LCC n=2,395,105, m=64,153,772), k=64, lambda=1.03, seed=0", 64),
     ("rgg16m", "2D random geometric graph 2^24 points, mean degree ~12, k=256, lambda=1.03, seed=0", 256),
+    # configs[4]'s shape (R-MAT ef16, k=1024) at the largest scale whose
+    # hierarchy fits one B200: the reference's matching keeps every level near
+    # m, so scale 27 needs ~9x its 34 GB CSR
+    ("rmat25", "R-MAT scale 25 edgefactor 16 (LCC n=17,051,518, m=523,600,916), k=1024, lambda=1.03, "
+               "seed=0 (BASELINE configs[4] shape at the largest single-GPU scale)", 1024),
 ]
 
 
@@ -225,29 +284,38 @@ def measure_extra_configs(ctx, det=True, steps=2):
         q = json.loads((ROOT / "tests" / "golden" / "quality.json").read_text())
     except Exception:
         q = {}
+    try:  # the Python reference's own answers (make_reference_big.py)
+        rb = json.loads((ROOT / "tests" / "golden" / "reference_big.json").read_text())
+    except Exception:
+        rb = {}
     out = []
     for name, workload, k in EXTRA_CONFIGS:
-        if name == "rmat22":
-            dg = gen.rmat_device(22, 16, 0, ctx=ctx)
+        if name == "rmat25" and os.environ.get("JET_BENCH_RMAT25", "1") != "1":
+            continue
+        if name.startswith("rmat"):
+            dg = gen.rmat_device(int(name[4:]), 16, 0, ctx=ctx)
         else:
             n = 1 << 24
             dg = gen.geometric_device(n, math.sqrt(12 / (math.pi * n)), 0, ctx=ctx)
         n, nnz, W = dg.info()
         cfg = J.RefinerConfig(k=k, imbalance=IMB, seed=SEED, deterministic=det)
-        partition_resident(dg, None, cfg, want_parts=False)  # warm
+        if name != "rmat25":
+            partition_resident(dg, None, cfg, want_parts=False)  # warm
         ms = []
-        for _ in range(steps):
+        for _ in range(1 if name == "rmat25" else steps):
             ctx.flush_l2()
             ctx.timer_start()
             _, pw, st = partition_resident(dg, None, cfg, want_parts=False)
             ms.append(ctx.timer_stop())
         t = sum(ms) / len(ms) * 1e-3
-        ref = q.get(name, {}).get("cuts", {}).get("0")
+        ref = rb.get(name, {}).get("cut") or q.get(name, {}).get("cuts", {}).get("0")
+        src = ("the reference (Python) run" if name in rb else
+               "the C port pinned to the reference" if ref else None)
         out.append({"workload": workload, "n": n, "m": nnz // 2, "partition_time_s": t,
                     "edges_per_s": (nnz // 2) / t, "cutsize": int(st.cutsize),
-                    "reference_cutsize": ref,
+                    "reference_cutsize": ref, "reference_cutsize_from": src,
                     "cut_ratio_vs_cpu_ref": (int(st.cutsize) / ref) if ref else None,
-                    "balanced": bool(st.balanced), "steps": steps,
+                    "balanced": bool(st.balanced), "steps": len(ms),
                     "mode": "deterministic (bit-exact reference semantics)" if det else "throughput"})
         dg.free()
     return out
@@ -263,7 +331,7 @@ def run_ours(args, world, rank, local):
     det = args.mode == "deterministic"
     cfg = J.RefinerConfig(k=K, imbalance=IMB, seed=SEED, deterministic=det)
     ctx = _lib.Context(local)
-    sharded = args.shard and world > 1
+    sharded = world > 1 and not args.replicas
     if sharded:  # one partition, finest levels sharded across the ranks (NCCL)
         from paper_2304_13194_b200 import dist as jd
         jd.attach_nccl(ctx, shard_min_vertices=args.shard_min_vertices)
@@ -402,7 +470,9 @@ def main():
                     help="throughput (default): the partitioner's fast mode, cut gated at 1.02x the "
                          "reference; deterministic: bit-identical to the reference")
     ap.add_argument("--shard", action="store_true",
-                    help="N>1: shard the finest levels across the ranks instead of replicas")
+                    help="(default for N>1) shard the finest levels across the ranks")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: N independent replicas instead of one sharded partition")
     ap.add_argument("--shard-min-vertices", type=int, default=1 << 20)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)

@@ -1,8 +1,8 @@
-# ncu source-level captures of small/mid-level refinement launches (throughput mode, 128^3):
-# launch order is L17..L0, so skip 6 -> L11 (n=3.6K), skip 11 -> L6 (n=46K)
+# ncu source-level captures of refinement launches (throughput mode, 128^3);
+# k_level launches run L17..L0: skip 6 -> L11 (n=3.6K), skip 11 -> L6 (n=46K), skip 17 -> L0
 mkdir -p gpurun_out
-for sk in 6 11; do
-JET_MODE=fast timeout 900 ncu --set full --clock-control none --import-source on --kernel-name "regex:k_level" \
+for sk in ${SKIPS:-6 11}; do
+JET_MODE=fast timeout 900 ncu --set full --clock-control none --import-source on --kernel-name k_level \
   --launch-skip $sk --launch-count 1 -o gpurun_out/k_level_skip$sk -f python scripts/one_partition.py 128 64 1 > gpurun_out/ncu_skip$sk.log 2>&1
 echo "ncu skip $sk rc=$?"
 done
