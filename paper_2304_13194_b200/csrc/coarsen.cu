@@ -1955,49 +1955,59 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
     int64_t BT = 0;
     d2h(c, &BT, boff.get() + nb, 1);
     c.sync();
-    DBuf<unsigned long long> bk(BT, c.stream), bk2(BT, c.stream);
-    launch(c, "big_gather", 20.0 * BT, [&] {
-      k_big_gather<<<grid_for(c, nb * 256, 256), 256, 0, c.stream>>>(rm, big_p, nb, boff.get(), bk.get());
-    });
-    if (BT < (int64_t)INT_MAX) {
-      size_t tmp = 0;
-      CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, bk.get(), bk2.get(), (int)BT, (int)nb, boff.get(),
-                                            boff.get() + 1, c.stream));
-      void* p = c.cub_scratch(tmp);
-      launch(c, "big_sort", 32.0 * BT, [&] {
-        CK(cub::DeviceSegmentedSort::SortKeys(p, tmp, bk.get(), bk2.get(), (int)BT, (int)nb, boff.get(),
-                                              boff.get() + 1, c.stream));
-      });
+    // Long rows are gathered, sorted and deduplicated in groups of rows of at
+    // most CH entries (one row may exceed it alone): the key buffers stay a
+    // few GB however dense the level (the dense coarse levels of R-MAT 2^27
+    // route ~4 G entries through here), and CUB's 32-bit item counts hold.
+    const int64_t CH = (int64_t)1 << 28;
+    struct Grp { int64_t s0, ns, base, cnt; };
+    std::vector<Grp> groups;
+    if (BT <= CH) {
+      groups.push_back({0, nb, 0, BT});
     } else {
-      // CUB's segmented sort counts items in 32 bits: sort groups of rows
-      // holding < 2^30 entries each, with offsets rebased to the group
       std::vector<int64_t> hb(nb + 1);
       d2h(c, hb.data(), boff.get(), nb + 1);
       c.sync();
-      DBuf<int64_t> rel(nb + 1, c.stream);
       int64_t s0 = 0;
       while (s0 < nb) {
         int64_t s1 = s0 + 1;
-        while (s1 < nb && hb[s1 + 1] - hb[s0] < (1LL << 30)) ++s1;
-        const int64_t base = hb[s0], cnt = hb[s1] - base, ns = s1 - s0;
-        launch(c, "big_rebase", 16.0 * ns, [&] {
-          k_rebase<<<grid_for(c, ns + 1, 256), 256, 0, c.stream>>>(boff.get() + s0, ns + 1, base,
-                                                                   rel.get());
-        });
-        size_t tmp = 0;
-        CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, bk.get() + base, bk2.get() + base,
-                                              (int)cnt, (int)ns, rel.get(), rel.get() + 1, c.stream));
-        void* p = c.cub_scratch(tmp);
-        launch(c, "big_sort", 32.0 * cnt, [&] {
-          CK(cub::DeviceSegmentedSort::SortKeys(p, tmp, bk.get() + base, bk2.get() + base, (int)cnt,
-                                                (int)ns, rel.get(), rel.get() + 1, c.stream));
-        });
+        while (s1 < nb && hb[s1 + 1] - hb[s0] <= CH) ++s1;
+        groups.push_back({s0, s1 - s0, hb[s0], hb[s1] - hb[s0]});
         s0 = s1;
       }
     }
-    launch(c, "big_dedup", 16.0 * BT, [&] {
-      k_big_dedup<<<grid_for(c, nb * 256, 256), 256, 0, c.stream>>>(rm, big_p, nb, boff.get(), bk2.get());
-    });
+    int64_t maxcnt = 0;
+    for (const Grp& q : groups) maxcnt = std::max(maxcnt, q.cnt);
+    DBuf<unsigned long long> bk(maxcnt, c.stream), bk2(maxcnt, c.stream);
+    DBuf<int64_t> rel;
+    if (groups.size() > 1) rel.alloc(nb + 1, c.stream);
+    for (const Grp& q : groups) {
+      JET_REQUIRE(q.cnt < (int64_t)INT_MAX, JET_EUNSUPPORTED, "merged coarse row longer than 2^31 entries");
+      const int64_t* off = boff.get();
+      if (groups.size() > 1) {
+        launch(c, "big_rebase", 16.0 * q.ns, [&] {
+          k_rebase<<<grid_for(c, q.ns + 1, 256), 256, 0, c.stream>>>(boff.get() + q.s0, q.ns + 1, q.base,
+                                                                     rel.get());
+        });
+        off = rel.get();
+      }
+      launch(c, "big_gather", 20.0 * q.cnt, [&] {
+        k_big_gather<<<grid_for(c, q.ns * 256, 256), 256, 0, c.stream>>>(rm, big_p + q.s0, q.ns, off,
+                                                                         bk.get());
+      });
+      size_t tmp = 0;
+      CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, bk.get(), bk2.get(), (int)q.cnt, (int)q.ns, off,
+                                            off + 1, c.stream));
+      void* p = c.cub_scratch(tmp);
+      launch(c, "big_sort", 32.0 * q.cnt, [&] {
+        CK(cub::DeviceSegmentedSort::SortKeys(p, tmp, bk.get(), bk2.get(), (int)q.cnt, (int)q.ns, off,
+                                              off + 1, c.stream));
+      });
+      launch(c, "big_dedup", 16.0 * q.cnt, [&] {
+        k_big_dedup<<<grid_for(c, q.ns * 256, 256), 256, 0, c.stream>>>(rm, big_p + q.s0, q.ns, off,
+                                                                        bk2.get());
+      });
+    }
   }
   // final offsets
   cg_->offs.alloc(nc + 1, c.stream);
@@ -2031,16 +2041,87 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
 }
 
 // build_hierarchy (coarsen.py:141-161; MAX_LEVELS 64, stagnation 0.95 twice)
+size_t graph_bytes(const DGraph& g) {
+  return g.offs.n * sizeof(int64_t) + (g.adj.n + g.ew.n + g.vw.n + g.bin_store.n) * sizeof(int32_t);
+}
+
+size_t Hierarchy::resident_bytes() const {
+  size_t b = 0;
+  for (const auto& o : owned)
+    if (o) b += graph_bytes(*o);
+  return b;
+}
+
+bool Hierarchy::shrink_to(size_t limit, int keep_a, int keep_b) {
+  bool any = false;
+  for (int i = 1; i < size() && resident_bytes() > limit; ++i) {
+    if (i == keep_a || i == keep_b || !owned[i - 1]) continue;
+    owned[i - 1].reset();
+    ++evictions;
+    any = true;
+  }
+  return any;
+}
+
+void Hierarchy::release(int i) {
+  if (i >= 1 && i < size()) owned[i - 1].reset();
+}
+
+// Contract level i-1 into level i. On a device allocation failure the other
+// evictable levels are dropped, the pool's unused memory is returned to the
+// driver (freed blocks of other sizes may not fit the request), and the
+// contraction is retried once.
+static std::unique_ptr<DGraph> contract_level(Ctx& c, Hierarchy& h, int i, const DGraph& fine,
+                                              const int32_t* partner, int32_t* vmap) {
+  try {
+    return device_contract(c, fine, partner, vmap);
+  } catch (const Error& e) {
+    if (e.code != JET_ENOMEM || h.budget == 0) throw;
+    c.sync();
+    h.shrink_to(0, i - 1, i);
+    c.release_scratch();
+    CK(cudaStreamSynchronize(c.stream));
+    CK(cudaMemPoolTrimTo(current_pool(), 0));
+    c.pool_reserved = 0;
+    return device_contract(c, fine, partner, vmap);
+  }
+}
+
+const DGraph& hier_acquire(Ctx& c, Hierarchy& h, int i) {
+  if (h.resident(i)) return h.level(i);
+  int j = i - 1;
+  while (!h.resident(j)) --j;
+  for (int t = j + 1; t <= i; ++t) {
+    JET_REQUIRE(h.partners[t - 1].get() != nullptr, JET_EINTERNAL, "evicted level without its matching");
+    // rebuilds overwrite maps[t-1] with identical values
+    h.owned[t - 1] = contract_level(c, h, t, h.level(t - 1), h.partners[t - 1].get(),
+                                    h.maps[t - 1].get());
+    JET_REQUIRE(h.owned[t - 1]->n == h.lv_n[t] && h.owned[t - 1]->nnz == h.lv_nnz[t], JET_EINTERNAL,
+                "rebuilt level differs from the original");
+    ++h.rebuilds;
+    // keep the newest levels (the next ones uncoarsening needs): evict from
+    // the bottom of the chain
+    if (h.budget) h.shrink_to(h.budget, t, i);
+  }
+  return h.level(i);
+}
+
 void device_build_hierarchy(Ctx& c, const DGraph& g0, int64_t target, Hierarchy& h,
-                            bool fast) {
+                            bool fast, size_t budget) {
   static const bool dbg = getenv("JET_COARSEN_TIMES") && getenv("JET_COARSEN_TIMES")[0] == '1';
   h.base = &g0;
   h.owned.clear();
   h.maps.clear();
+  h.partners.clear();
+  h.lv_n.assign(1, g0.n);
+  h.lv_nnz.assign(1, g0.nnz);
+  h.budget = budget;
+  h.rebuilds = h.evictions = 0;
   int stagnant = 0;
   const DGraph* fine = &g0;
   DBuf<int32_t> partner;
   while (fine->n > target && (int)h.owned.size() + 1 < 64) {
+    if (budget) partner = DBuf<int32_t>();  // a fresh matching per level, kept for rebuilds
     partner.ensure(fine->n, c.stream);
     double t0 = 0, t1 = 0;
     if (dbg) {
@@ -2056,16 +2137,23 @@ void device_build_hierarchy(Ctx& c, const DGraph& g0, int64_t target, Hierarchy&
       t1 = wall_s();
     }
     DBuf<int32_t> vmap(fine->n, c.stream);
-    auto coarse = device_contract(c, *fine, partner.get(), vmap.get());
+    const int lv = h.size();  // the level being built
+    auto coarse = contract_level(c, h, lv, *fine, partner.get(), vmap.get());
     if (dbg) {
       c.sync();
-      fprintf(stderr, "COARSEN n=%lld match=%.2fms contract=%.2fms\n", (long long)fine->n,
-              (t1 - t0) * 1e3, (wall_s() - t1) * 1e3);
+      fprintf(stderr, "COARSEN n=%lld match=%.2fms contract=%.2fms resident=%.2fGB\n", (long long)fine->n,
+              (t1 - t0) * 1e3, (wall_s() - t1) * 1e3, h.resident_bytes() / 1e9);
     }
     if (coarse->n == fine->n) break;
     const bool stag = (double)coarse->n > 0.95 * (double)fine->n;
     h.maps.push_back(std::move(vmap));
+    h.lv_n.push_back(coarse->n);
+    h.lv_nnz.push_back(coarse->nnz);
     h.owned.push_back(std::move(coarse));
+    if (budget) {
+      h.partners.push_back(std::move(partner));
+      h.shrink_to(budget, lv, lv);  // the new level stays: it is the next fine one
+    }
     fine = h.owned.back().get();
     stagnant = stag ? stagnant + 1 : 0;
     if (stagnant >= 2) break;

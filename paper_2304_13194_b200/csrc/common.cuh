@@ -8,6 +8,7 @@
 // Sums (conn, gains, part weights, cut) are int64, matching the reference's
 // int64 numpy arithmetic (_arrays.py:5).
 #pragma once
+#include <algorithm>
 #include <atomic>
 #include <memory>
 #include <cuda_runtime.h>
@@ -247,8 +248,14 @@ struct Ctx {
   T* scratch(int slot, size_t count) {
     DBuf<uint8_t>& b = scratch_slots[slot];
     const size_t bytes = (count > 0 ? count : 1) * sizeof(T);
-    if (bytes > b.n) b.alloc(bytes + bytes / 8, stream);
+    if (bytes > b.n) b.alloc(bytes + std::min<size_t>(bytes / 8, (size_t)256 << 20), stream);
     return reinterpret_cast<T*>(b.get());
+  }
+  // Drop every scratch slot (out-of-memory hierarchies: the contraction
+  // temporaries of a 4 G-entry level are ~40 GB).
+  void release_scratch() {
+    for (auto& s : scratch_slots) s.release();
+    cub_tmp.release();
   }
 };
 

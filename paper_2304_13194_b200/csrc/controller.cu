@@ -199,26 +199,49 @@ void run_partition(Ctx& c, const DGraph& g0, const jet_config& cfg, int32_t* par
   // inside the pipeline has to map new memory (100s of ms stalls measured on
   // dense coarse levels of R-MAT 2^25), capped at 60 % of free memory
   // (cudaMemGetInfo only when the pool has to grow: the query itself stalled
-  // the host for 50-90 ms in ~1 of 8 calls)
+  // the host for 50-90 ms in ~1 of 8 calls).
+  // When the whole hierarchy cannot fit (R-MAT 2^26+: every level keeps ~m
+  // edges), the owned levels get a byte budget: what is left after the input,
+  // the contraction's working set (fine level, merged-row scratch, coarse
+  // level, sort groups ~3.3x the input CSR) and the refinement workspace;
+  // evicted levels are rebuilt on demand (coarsen.cuh Hierarchy).
+  size_t budget = 0;
   {
-    const size_t csr = (size_t)g0.nnz * 8 + (size_t)g0.n * 24;
-    if (12 * csr > c.pool_reserved) {
+    const size_t csr = graph_bytes(g0);
+    const char* eb = getenv("JET_HIER_BUDGET_MB");
+    if (eb && atoll(eb) > 0) {
+      budget = (size_t)atoll(eb) << 20;
+    } else if (12 * csr > c.pool_reserved) {
       size_t fr = 0, tot = 0;
       CK(cudaMemGetInfo(&fr, &tot));
-      c.reserve_pool(std::min<size_t>(12 * csr, c.pool_reserved + fr / 10 * 6));
+      size_t used = 0, resv = 0;
+      cudaMemPool_t pool = current_pool();
+      CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &resv));
+      CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+      const size_t avail = fr + (resv > used ? resv - used : 0);
+      const size_t work = (size_t)(3.3 * (double)csr) + (size_t)g0.n * 96 + ((size_t)1 << 30);
+      if (12 * csr > avail) {  // the hierarchy may not fit: budgeted
+        budget = avail > work + csr ? avail - work : csr;
+        c.reserve_pool(std::min<size_t>(avail / 20 * 19, c.pool_reserved + fr / 20 * 19));
+      } else {
+        c.reserve_pool(std::min<size_t>(12 * csr, c.pool_reserved + fr / 10 * 6));
+      }
     }
   }
   const double t_res = now_s();
   Hierarchy h;
   c.prof_tag = "coarsen:";
-  device_build_hierarchy(c, g0, target, h, cfg.deterministic == 0);
+  device_build_hierarchy(c, g0, target, h, cfg.deterministic == 0, budget);
+  if (budget) c.release_scratch();
   c.prof_tag.clear();
   const double t_hier = now_s();
   c.sync();
   const double t1 = now_s();
-  if (getenv("JET_SYNC_STATS"))
-    fprintf(stderr, "COARSEN_SPLIT pre %.2f ms hierarchy %.2f ms final sync %.2f ms\n",
-            (t_res - t0) * 1e3, (t_hier - t_res) * 1e3, (t1 - t_hier) * 1e3);
+  if (getenv("JET_SYNC_STATS") || getenv("JET_HIER_STATS"))
+    fprintf(stderr, "COARSEN_SPLIT pre %.2f ms hierarchy %.2f ms final sync %.2f ms budget %.2f GB "
+            "resident %.2f GB evictions %d\n",
+            (t_res - t0) * 1e3, (t_hier - t_res) * 1e3, (t1 - t_hier) * 1e3, budget / 1e9,
+            h.resident_bytes() / 1e9, h.evictions);
   S.t_coarsen = t1 - t0;
 
   const int top = h.size() - 1;
@@ -245,7 +268,18 @@ void run_partition(Ctx& c, const DGraph& g0, const jet_config& cfg, int32_t* par
   int32_t* nxt = pb.get();
   int li = 0;
   for (int level = top; level >= 0; --level) {
-    const DGraph& g = h.level(level);
+    if (level != top) h.release(level + 1);  // projected from: no longer needed
+    const int rb0 = h.rebuilds;
+    const double tr = now_s();
+    const DGraph& g = hier_acquire(c, h, level);
+    if (h.rebuilds != rb0) {
+      c.release_scratch();
+      if (getenv("JET_HIER_STATS")) {
+        c.sync();
+        fprintf(stderr, "HIER rebuilt L%d (%d contractions, %.2f s) resident %.2f GB\n", level,
+                h.rebuilds - rb0, now_s() - tr, h.resident_bytes() / 1e9);
+      }
+    }
     if (level != top) {
       device_project(c, h.maps[level].get(), cur, nxt, g.n);
       std::swap(cur, nxt);
