@@ -136,6 +136,21 @@ void refine_level(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, int64_t
               st.iterations - 1, is_lp ? 1 : (rebal_streak <= 2 ? 2 : 3), (long long)ar.n_moves,
               (long long)cut, (long long)worst(), no_improve, has_best ? 1 : 0);
     if (fixed_point) break;
+    // a strong pass that moved nothing repeats identically (no RNG, same
+    // state) until the loop ends: book those passes (level.cu lv_bookkeep)
+    if (strong_pass && ar.n_moves == 0 && !balanced()) {
+      while (no_improve < cfg.no_improve_limit && rebal_streak < 2 + k) {
+        st.strong_passes++;
+        rebal_streak++;
+        pass_index++;
+        st.iterations++;
+        no_improve++;
+        if (c.api_trace) {
+          const int64_t rec[4] = {3, cut, worst(), 0};
+          c.api_trace->insert(c.api_trace->end(), rec, rec + 4);
+        }
+      }
+    }
   }
   d2d(c, parts, keep.get(), g.n);
   cut = keep_cut;

@@ -381,6 +381,27 @@ __device__ void lv_bookkeep(const LevelArgs& A, LevelCtl* C, const unsigned long
       t[4] = C->no_improve;
       t[5] = C->has_best;
     }
+    // A strong pass that moved nothing left parts, part weights and cut as
+    // they were, and strong passes draw no random numbers: every following
+    // pass repeats it (still unbalanced, streak >= 2) until no_improve
+    // reaches the limit or the stuck guard fires (refine.py:229-263). Book
+    // those passes without running them; outputs and stats are unchanged.
+    if (kind == 3 && nm == 0 && worst > A.limit && !fixed_point) {
+      const int it0 = C->iterations;
+      while (C->no_improve < A.no_improve_limit && C->rebal_streak < 2 + k) {
+        C->strong++;
+        C->rebal_streak++;
+        C->pass_index++;
+        C->iterations++;
+        C->no_improve++;
+        if (A.trace && C->iterations <= A.trace_cap && it0 <= A.trace_cap) {
+          long long* t = A.trace + 10 * (C->iterations - 1);
+          const long long* t0 = A.trace + 10 * (it0 - 1);
+          for (int q = 0; q < 10; ++q) t[q] = t0[q];
+          t[4] = C->no_improve;
+        }
+      }
+    }
   }
   __syncthreads();
   if (s_copy)
