@@ -1529,6 +1529,7 @@ static void device_match_fast(Ctx& c, const DGraph& g, int32_t* partner) {
     dzero(c, cnt.get(), 2 * MAXR);
     const GView gv = view(g);
     int64_t matched = 0;
+    int low_rounds = 0;
     static const bool fstats = getenv("JET_MATCH_STATS") && getenv("JET_MATCH_STATS")[0] == '1';
     for (int r0 = 0; r0 < MAXR; r0 += RG) {
       for (int round = r0; round < r0 + RG; ++round) {
@@ -1570,10 +1571,18 @@ static void device_match_fast(Ctx& c, const DGraph& g, int32_t* partner) {
         if (fstats)
           fprintf(stderr, "FAST n=%lld round=%d proposers=%llu pairs=%llu matched=%lld\n",
                   (long long)n, r0 + q, h[2 * q], h[2 * q + 1], (long long)matched);
-        // rounds until no pair is added: stopping at a 1 % yield left many
-        // leftovers to the leaf pairing, whose non-adjacent pairs made the
-        // coarse levels refine 2x longer (128^3: 143 -> 72 ms, 3 % lower cut)
-        done = h[2 * q] == 0 || h[2 * q + 1] == 0;
+        // rounds until no pair is added: stopping at a 1 % yield (of n) left
+        // many leftovers to the leaf pairing, whose non-adjacent pairs made
+        // the coarse levels refine 2x longer (128^3: 143 -> 72 ms, 3 % lower
+        // cut). On dense power-law levels the proposals chain towards the
+        // hubs instead, and each round pairs a few hundred of 10^5 proposers
+        // for 40+ rounds that each rescan every live row (R-MAT 2^22: 0.3 s
+        // of matching): once a round pairs under 0.5 % of its proposers
+        // twice in a row, the rest goes to the leaf pairing, which pairs
+        // leftovers sharing their heaviest neighbour.
+        const bool low = h[2 * q + 1] * 200 < h[2 * q];
+        low_rounds = low ? low_rounds + 1 : 0;
+        done = h[2 * q] == 0 || h[2 * q + 1] == 0 || low_rounds >= 2;
       }
       if (done) break;
     }

@@ -1,7 +1,7 @@
 """BASELINE configs[4] shape on one GPU: R-MAT scale S (default 27), edge
 factor 16, k=1024, generated on the device; one partition per mode with
 per-level stats. python scripts/probe_rmat_big.py [scale] [modes]"""
-import sys, time
+import os, sys, time
 sys.path.insert(0, '.')
 import paper_2304_13194_b200 as J
 from paper_2304_13194_b200 import generators as gen, _lib
@@ -14,7 +14,8 @@ dg = gen.rmat_device(scale, 16, 0, ctx=ctx)
 n, nnz, W = dg.info()
 print(f"rmat {scale}: n={n} m={nnz // 2} gen {time.perf_counter() - t:.2f}s", flush=True)
 for mode in modes:
-    cfg = J.RefinerConfig(k=1024, imbalance=0.03, seed=0, deterministic=(mode == "det"))
+    cfg = J.RefinerConfig(k=int(os.environ.get("JET_K", "1024")), imbalance=0.03, seed=0,
+                          deterministic=(mode == "det"))
     for rep in range(2 if len(sys.argv) > 3 else 1):
         ctx.timer_start()
         t = time.perf_counter()
