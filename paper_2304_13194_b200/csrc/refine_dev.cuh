@@ -570,6 +570,8 @@ static __device__ void agg_warp(const typename Op::Args& a, const GView& g,
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t per = (size_t)k + (size_t)(tl_cap + 3) / 2;
   unsigned long long* tab = smem + wib * per;
+  unsigned* tab32 = reinterpret_cast<unsigned*>(tab);  // narrow weighted sums (lane atomics)
+  const bool lane_atomic = !UNIT && !wide;
   int* tl = reinterpret_cast<int*>(tab + k);
   int* tcnt = tl + tl_cap;
   for (int i = lane; i < k; i += 32) tab[i] = 0;
@@ -637,11 +639,17 @@ static __device__ void agg_warp(const typename Op::Args& a, const GView& g,
       for (int q = 0; q < U; ++q) {
         const int p = pp[q];
         if (p >= 0) ex += Op::extra(a, p, wv[q]);
-        const unsigned peers = __match_any_sync(0xffffffffu, p);
-        const long long sm = UNIT ? (long long)__popc(peers) : peer_sum(peers, wv[q], wide);
-        if (p >= 0 && (__ffs(peers) - 1) == lane) {
-          const unsigned long long old = atomicAdd(&tab[p], (unsigned long long)sm);
-          if (old == 0) tl[atomicAdd(tcnt, 1)] = p;
+        if (lane_atomic) {
+          // weighted, narrow: one 32-bit shared atomic per lane (a REDUX over
+          // each match_any group serialises over the groups of the warp)
+          if (p >= 0 && atomicAdd(&tab32[p], (unsigned)wv[q]) == 0u) tl[atomicAdd(tcnt, 1)] = p;
+        } else {
+          const unsigned peers = __match_any_sync(0xffffffffu, p);
+          const long long sm = UNIT ? (long long)__popc(peers) : peer_sum(peers, wv[q], wide);
+          if (p >= 0 && (__ffs(peers) - 1) == lane) {
+            const unsigned long long old = atomicAdd(&tab[p], (unsigned long long)sm);
+            if (old == 0) tl[atomicAdd(tcnt, 1)] = p;
+          }
         }
       }
       if (r != cur_r) {  // row cur_r complete: reduce its table
@@ -655,8 +663,14 @@ static __device__ void agg_warp(const typename Op::Args& a, const GView& g,
           unsigned usc = 0, bm = 0, bp = 0xffffffffu;
           for (int t = lane; t < nt; t += 32) {
             const int p = tl[t];
-            const unsigned cv = (unsigned)tab[p];
-            tab[p] = 0;
+            unsigned cv;
+            if (lane_atomic) {
+              cv = tab32[p];
+              tab32[p] = 0;
+            } else {
+              cv = (unsigned)tab[p];
+              tab[p] = 0;
+            }
             if (p == rown) usc = cv;
             else if (Op::competes(a, p, rown) && (cv > bm || (cv == bm && (unsigned)p < bp))) {
               bm = cv;
@@ -713,6 +727,8 @@ static __device__ void agg_block(const typename Op::Args& a, const GView& g,
                           unsigned long long* smem, long long& acc) {
   if (dcnt) cnt = (int64_t)*(const volatile unsigned long long*)dcnt;
   unsigned long long* tab = smem;
+  unsigned* tab32 = reinterpret_cast<unsigned*>(tab);
+  const bool lane_atomic = !UNIT && !wide;
   int* tl = reinterpret_cast<int*>(tab + k);
   __shared__ int tcnt;
   __shared__ long long r_self[32], r_ex[32];
@@ -745,11 +761,15 @@ static __device__ void agg_block(const typename Op::Args& a, const GView& g,
       for (int q = 0; q < U; ++q) {
         const int p = pp[q], w = ww[q];
         if (p >= 0) ex += Op::extra(a, p, w);
-        const unsigned peers = __match_any_sync(0xffffffffu, p);
-        const long long s = UNIT ? (long long)__popc(peers) : peer_sum(peers, w, wide);
-        if (p >= 0 && (__ffs(peers) - 1) == lane) {
-          unsigned long long old = atomicAdd(&tab[p], (unsigned long long)s);
-          if (old == 0) tl[atomicAdd(&tcnt, 1)] = p;
+        if (lane_atomic) {  // see agg_warp
+          if (p >= 0 && atomicAdd(&tab32[p], (unsigned)w) == 0u) tl[atomicAdd(&tcnt, 1)] = p;
+        } else {
+          const unsigned peers = __match_any_sync(0xffffffffu, p);
+          const long long s = UNIT ? (long long)__popc(peers) : peer_sum(peers, w, wide);
+          if (p >= 0 && (__ffs(peers) - 1) == lane) {
+            unsigned long long old = atomicAdd(&tab[p], (unsigned long long)s);
+            if (old == 0) tl[atomicAdd(&tcnt, 1)] = p;
+          }
         }
       }
     }
@@ -759,8 +779,14 @@ static __device__ void agg_block(const typename Op::Args& a, const GView& g,
     unsigned long long key = 0;
     for (int t = threadIdx.x; t < nt; t += blockDim.x) {
       const int p = tl[t];
-      const long long cv = (long long)tab[p];
-      tab[p] = 0;
+      long long cv;
+      if (lane_atomic) {
+        cv = (long long)tab32[p];
+        tab32[p] = 0;
+      } else {
+        cv = (long long)tab[p];
+        tab[p] = 0;
+      }
       if (p == own) self_c = cv;
       else if (Op::competes(a, p, own)) {
         unsigned long long kk = pack_best(cv, p);
@@ -882,6 +908,42 @@ static __device__ __forceinline__ void ab_group_rows(const AbArgs& a, const GVie
 // *nmove, and the apply phase walks the candidate lists skipping unmoved
 // rows -- one atomic per row on a hot counter serialises in L2.
 // wr/we (optional): += rows / entries visited, for the roofline accounting.
+// Afterburner sum of one long row over the entries j = j0, j0 + stride, ...
+// (a warp or block per row): RU strides are loaded per step, so each lane
+// has RU independent adjacency -> (part, dest) -> F chains in flight
+// (one at a time left the dense R-MAT levels latency-bound).
+template <bool UNIT, int RU = 4>
+static __device__ __forceinline__ long long ab_row_f2(const AbArgs& a, const GView& g, int v, int own,
+                                                      int dv, long long Fv, int64_t j0, int64_t e,
+                                                      int64_t stride) {
+  long long f2 = 0;
+  for (; j0 < e; j0 += stride * RU) {
+    int uu[RU], ww[RU], pu[RU], cu[RU];
+    long long Fu[RU];
+#pragma unroll
+    for (int q = 0; q < RU; ++q) {
+      const int64_t j = j0 + q * stride;
+      uu[q] = j < e ? g.adj[j] : -1;
+      ww[q] = j < e ? (UNIT ? 1 : g.ew[j]) : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < RU; ++q) {
+      pu[q] = uu[q] >= 0 ? a.parts[uu[q]] : -1;
+      cu[q] = uu[q] >= 0 ? a.cdest[uu[q]] : -1;
+    }
+#pragma unroll
+    for (int q = 0; q < RU; ++q) Fu[q] = cu[q] >= 0 ? a.F[uu[q]] : 0;
+#pragma unroll
+    for (int q = 0; q < RU; ++q) {
+      int eff = pu[q];
+      if (cu[q] >= 0 && (Fu[q] > Fv || (Fu[q] == Fv && uu[q] < v))) eff = cu[q];
+      const int w = ww[q];
+      f2 += uu[q] < 0 ? 0 : (eff == dv) ? w : (eff == own) ? -w : 0;
+    }
+  }
+  return f2;
+}
+
 template <bool UNIT>
 static __device__ void afterburner_rows(const AbArgs& a, const GView& g, const SegLists& sl,
                                  const RbSegsDev& mseg, int64_t w0, int64_t ws,
@@ -903,19 +965,8 @@ static __device__ void afterburner_rows(const AbArgs& a, const GView& g, const S
           *wr += 1;
           *we += (unsigned long long)(e - b);
         }
-        long long f2 = 0;
-        for (int64_t j = b + threadIdx.x; j < e; j += blockDim.x) {
-          const int u = g.adj[j];
-          int eff = a.parts[u];
-          const int cu = a.cdest[u];
-          if (cu >= 0) {
-            const long long Fu = a.F[u];
-            if (Fu > Fv || (Fu == Fv && u < v)) eff = cu;
-          }
-          const int w = UNIT ? 1 : g.ew[j];
-          f2 += (eff == dv) ? w : (eff == own) ? -w : 0;
-        }
-        f2 = block_sum_all(f2);
+        const long long f2 = block_sum_all(ab_row_f2<UNIT>(a, g, v, own, dv, Fv, b + threadIdx.x, e,
+                                                           (int64_t)blockDim.x));
         if (threadIdx.x == 0) {
           if (a.f2_out) a.f2_out[v] = f2;
           if (f2 >= 0) {
@@ -946,19 +997,7 @@ static __device__ void afterburner_rows(const AbArgs& a, const GView& g, const S
         *wr += 1;
         *we += (unsigned long long)(e - b);
       }
-      long long f2 = 0;
-      for (int64_t j = b + lane; j < e; j += 32) {
-        const int u = g.adj[j];
-        int eff = a.parts[u];
-        const int cu = a.cdest[u];
-        if (cu >= 0) {
-          const long long Fu = a.F[u];
-          if (Fu > Fv || (Fu == Fv && u < v)) eff = cu;
-        }
-        const int w = UNIT ? 1 : g.ew[j];
-        f2 += (eff == dv) ? w : (eff == own) ? -w : 0;
-      }
-      f2 = gsum<32>(f2, 0xffffffffu);
+      const long long f2 = gsum<32>(ab_row_f2<UNIT>(a, g, v, own, dv, Fv, b + lane, e, 32), 0xffffffffu);
       if (lane == 0) {
         if (a.f2_out) a.f2_out[v] = f2;
         if (f2 >= 0) {
@@ -1003,6 +1042,37 @@ static __device__ __forceinline__ void ext_entry(int32_t* ext, int u, int pu, in
 // moved appear twice and are halved, so we sum 2c / c and halve at the end.
 // Rows whose mv[v] < 0 are skipped (the level kernel applies Jetlp moves
 // straight from the candidate lists).
+// Cut delta / weight / external-degree upkeep of one long moved row over
+// j = j0, j0 + stride, ... with RU strides in flight per step (ab_row_f2).
+template <bool UNIT, int RU = 4>
+static __device__ __forceinline__ void ap_row(const ApArgs& a, const GView& g, int dst, int old,
+                                              int64_t j0, int64_t e, int64_t stride, long long& d,
+                                              long long& ev) {
+  for (; j0 < e; j0 += stride * RU) {
+    int uu[RU], ww[RU], pu[RU], mu[RU];
+#pragma unroll
+    for (int q = 0; q < RU; ++q) {
+      const int64_t j = j0 + q * stride;
+      uu[q] = j < e ? g.adj[j] : -1;
+      ww[q] = j < e ? (UNIT ? 1 : g.ew[j]) : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < RU; ++q) {
+      pu[q] = uu[q] >= 0 ? a.parts[uu[q]] : 0;
+      mu[q] = uu[q] >= 0 ? a.mv[uu[q]] : -1;
+    }
+#pragma unroll
+    for (int q = 0; q < RU; ++q) {
+      if (uu[q] < 0) continue;
+      const int nu = mu[q] >= 0 ? mu[q] : pu[q];
+      const long long w = ww[q];
+      const long long cc = w * ((long long)(nu != dst) - (long long)(pu[q] != old));
+      d += mu[q] >= 0 ? cc : 2 * cc;
+      if (a.ext) ext_entry(a.ext, uu[q], pu[q], mu[q], nu, dst, old, w, ev);
+    }
+  }
+}
+
 template <bool UNIT>
 static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const SegLists& sl,
                                  int64_t w0, int64_t ws, long long& acc,
@@ -1024,16 +1094,7 @@ static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const S
           *we += (unsigned long long)(e - b);
         }
         long long ev = 0;
-        for (int64_t j = b + threadIdx.x; j < e; j += blockDim.x) {
-          const int u = g.adj[j];
-          const int pu = a.parts[u];
-          const int mu = a.mv[u];
-          const int nu = mu >= 0 ? mu : pu;
-          const long long w = UNIT ? 1 : g.ew[j];
-          const long long cc = w * ((long long)(nu != dst) - (long long)(pu != old));
-          acc += mu >= 0 ? cc : 2 * cc;
-          if (a.ext) ext_entry(a.ext, u, pu, mu, nu, dst, old, w, ev);
-        }
+        ap_row<UNIT>(a, g, dst, old, b + threadIdx.x, e, (int64_t)blockDim.x, acc, ev);
         if (a.ext) {
           ev = block_sum_all(ev);
           if (threadIdx.x == 0) a.ext[v] = (int32_t)ev;
@@ -1102,16 +1163,7 @@ static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const S
         *we += (unsigned long long)(e - b);
       }
       long long d = 0, ev = 0;
-      for (int64_t j = b + lane; j < e; j += 32) {
-        const int u = g.adj[j];
-        const int pu = a.parts[u];
-        const int mu = a.mv[u];
-        const int nu = mu >= 0 ? mu : pu;
-        const long long w = UNIT ? 1 : g.ew[j];
-        const long long cc = w * ((long long)(nu != dst) - (long long)(pu != old));
-        d += mu >= 0 ? cc : 2 * cc;
-        if (a.ext) ext_entry(a.ext, u, pu, mu, nu, dst, old, w, ev);
-      }
+      ap_row<UNIT>(a, g, dst, old, b + lane, e, 32, d, ev);
       acc += d;  // per-lane partial sums: the caller reduces over the block
       if (a.ext) {
         ev = gsum<32>(ev, 0xffffffffu);
