@@ -21,6 +21,7 @@
 #include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <cub/block/block_scan.cuh>
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
 #include <algorithm>
 #include <chrono>
@@ -1788,15 +1789,76 @@ __global__ void __launch_bounds__(256) k_merge_rows(RowMerge m) {
 
 // long rows: gather keys into a segmented buffer for a library segmented sort
 __global__ void k_big_gather(RowMerge m, const int32_t* __restrict__ big, int64_t nbig,
-                             const int64_t* __restrict__ boff, unsigned long long* keys) {
+                             const int64_t* __restrict__ boff, unsigned long long* keys,
+                             int64_t min_len) {
   for (int64_t i = blockIdx.x; i < nbig; i += gridDim.x) {
     const int c = big[i];
+    const int64_t d = m.rowlen[c];
+    if (d <= min_len) continue;  // sorted on chip by k_big_sort_block
     const int a = m.mem_a[c], b = m.mem_b[c];
     const int64_t da = m.offs[a + 1] - m.offs[a];
-    const int64_t d = m.rowlen[c];
     const int64_t o = boff[i];
     for (int64_t idx = threadIdx.x; idx < d; idx += blockDim.x) keys[o + idx] = merged_key(m, c, idx, a, b, da);
   }
+}
+
+// Long rows of up to BIG_BLOCK_MAX entries (almost all of them on the dense
+// coarse levels of power-law graphs): one block gathers the merged row
+// straight from the fine rows into registers, radix-sorts it on chip over
+// the coarse-id bits only (+1 bit so contraction self loops, ~0, sort last)
+// and writes it sorted: no gather pass and no device-wide segmented sort.
+constexpr int BIG_BT = 256, BIG_IPT_S = 4, BIG_IPT_L = 16;
+constexpr int64_t BIG_BLOCK_MAX = (int64_t)BIG_BT * BIG_IPT_L;
+
+template <int IPT>
+__device__ __forceinline__ void big_sort_row(const RowMerge& m, int c, int64_t d, int64_t o,
+                                             int cbits, unsigned long long* out, void* ts_raw) {
+  typedef cub::BlockRadixSort<unsigned long long, BIG_BT, IPT> BRS;
+  auto& ts = *reinterpret_cast<typename BRS::TempStorage*>(ts_raw);
+  const int a = m.mem_a[c], b = m.mem_b[c];
+  const int64_t da = m.offs[a + 1] - m.offs[a];
+  unsigned long long k[IPT];
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    const int64_t idx = (int64_t)threadIdx.x * IPT + q;  // blocked arrangement
+    k[q] = idx < d ? merged_key(m, c, idx, a, b, da) : ~0ull;
+  }
+  BRS(ts).Sort(k, 32, 32 + cbits + 1);
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    const int64_t idx = (int64_t)threadIdx.x * IPT + q;
+    if (idx < d) out[o + idx] = k[q];
+  }
+}
+
+__global__ void __launch_bounds__(BIG_BT)
+    k_big_sort_block(RowMerge m, const int32_t* __restrict__ big, int64_t nbig,
+                     const int64_t* __restrict__ boff, int cbits, unsigned long long* out) {
+  typedef cub::BlockRadixSort<unsigned long long, BIG_BT, BIG_IPT_S> BS;
+  typedef cub::BlockRadixSort<unsigned long long, BIG_BT, BIG_IPT_L> BL;
+  __shared__ union {
+    typename BS::TempStorage s;
+    typename BL::TempStorage l;
+  } ts;
+  for (int64_t i = blockIdx.x; i < nbig; i += gridDim.x) {
+    const int c = big[i];
+    const int64_t d = m.rowlen[c];  // block-uniform
+    if (d > BIG_BLOCK_MAX) continue;
+    if (d <= (int64_t)BIG_BT * BIG_IPT_S)
+      big_sort_row<BIG_IPT_S>(m, c, d, boff[i], cbits, out, &ts);
+    else
+      big_sort_row<BIG_IPT_L>(m, c, d, boff[i], cbits, out, &ts);
+    __syncthreads();  // the temp storage is reused by the next row
+  }
+}
+
+// segment ends for the device-wide sort: rows sorted on chip get empty segments
+__global__ void k_big_ends(const int32_t* __restrict__ big, int64_t nbig,
+                           const int64_t* __restrict__ rowlen, const int64_t* __restrict__ off,
+                           int64_t* end) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nbig;
+       i += (int64_t)gridDim.x * blockDim.x)
+    end[i] = rowlen[big[i]] > BIG_BLOCK_MAX ? off[i + 1] : off[i];
 }
 
 __global__ void k_big_len(const int32_t* __restrict__ big, int64_t nbig,
@@ -1988,8 +2050,10 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
     int64_t maxcnt = 0;
     for (const Grp& q : groups) maxcnt = std::max(maxcnt, q.cnt);
     DBuf<unsigned long long> bk(maxcnt, c.stream), bk2(maxcnt, c.stream);
-    DBuf<int64_t> rel;
+    DBuf<int64_t> rel, bend(nb + 1, c.stream);
     if (groups.size() > 1) rel.alloc(nb + 1, c.stream);
+    int cbits = 1;
+    while ((1LL << cbits) < nc) ++cbits;
     for (const Grp& q : groups) {
       JET_REQUIRE(q.cnt < (int64_t)INT_MAX, JET_EUNSUPPORTED, "merged coarse row longer than 2^31 entries");
       const int64_t* off = boff.get();
@@ -2002,15 +2066,23 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
       }
       launch(c, "big_gather", 20.0 * q.cnt, [&] {
         k_big_gather<<<grid_for(c, q.ns * 256, 256), 256, 0, c.stream>>>(rm, big_p + q.s0, q.ns, off,
-                                                                         bk.get());
+                                                                         bk.get(), BIG_BLOCK_MAX);
+      });
+      launch(c, "big_ends", 16.0 * q.ns, [&] {
+        k_big_ends<<<grid_for(c, q.ns, 256), 256, 0, c.stream>>>(big_p + q.s0, q.ns, rowlen_p, off,
+                                                                 bend.get());
       });
       size_t tmp = 0;
       CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, bk.get(), bk2.get(), (int)q.cnt, (int)q.ns, off,
-                                            off + 1, c.stream));
+                                            bend.get(), c.stream));
       void* p = c.cub_scratch(tmp);
       launch(c, "big_sort", 32.0 * q.cnt, [&] {
         CK(cub::DeviceSegmentedSort::SortKeys(p, tmp, bk.get(), bk2.get(), (int)q.cnt, (int)q.ns, off,
-                                              off + 1, c.stream));
+                                              bend.get(), c.stream));
+      });
+      launch(c, "big_sort_block", 20.0 * q.cnt, [&] {
+        k_big_sort_block<<<grid_for(c, q.ns * BIG_BT, BIG_BT), BIG_BT, 0, c.stream>>>(
+            rm, big_p + q.s0, q.ns, off, cbits, bk2.get());
       });
       launch(c, "big_dedup", 16.0 * q.cnt, [&] {
         k_big_dedup<<<grid_for(c, q.ns * 256, 256), 256, 0, c.stream>>>(rm, big_p + q.s0, q.ns, off,
