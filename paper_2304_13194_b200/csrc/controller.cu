@@ -14,6 +14,15 @@
 
 namespace jet {
 
+// Jet loop patience of a level: the reference's no_improve_limit, shortened
+// on coarse levels in throughput mode (jet_config.coarse_patience).
+int level_patience(const jet_config& cfg, int level) {
+  if (cfg.deterministic || cfg.coarse_patience <= 0 || level < cfg.coarse_patience_from ||
+      cfg.k < cfg.coarse_patience_min_k)
+    return cfg.no_improve_limit;
+  return std::min(cfg.coarse_patience, cfg.no_improve_limit);
+}
+
 static double now_s() {
   using namespace std::chrono;
   return duration<double>(steady_clock::now().time_since_epoch()).count();
@@ -64,7 +73,8 @@ void refine_level(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, int64_t
   int no_improve = 0, rebal_streak = 0, pass_index = 0;
   int64_t locked = 0;
   int32_t epoch = ++c.lock_epoch;  // fresh table: no vertex locked
-  while (no_improve < cfg.no_improve_limit) {
+  const int patience = level_patience(cfg, level);
+  while (no_improve < patience) {
     bool is_lp = false, locks_all_clear = false, strong_pass = false;
     if (balanced()) {
       rebal_streak = 0;
@@ -139,7 +149,7 @@ void refine_level(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, int64_t
     // a strong pass that moved nothing repeats identically (no RNG, same
     // state) until the loop ends: book those passes (level.cu lv_bookkeep)
     if (strong_pass && ar.n_moves == 0 && !balanced()) {
-      while (no_improve < cfg.no_improve_limit && rebal_streak < 2 + k) {
+      while (no_improve < patience && rebal_streak < 2 + k) {
         st.strong_passes++;
         rebal_streak++;
         pass_index++;

@@ -16,6 +16,8 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
                          const jet_config& cfg, bool finest, int level, jet_level_stats& st,
                          DBuf<int32_t>& keep);
 void check_partition_args(const DGraph& g, const jet_config& cfg);
+// no_improve_limit of a level (shortened on coarse levels in throughput mode)
+int level_patience(const jet_config& cfg, int level);
 void run_partition(Ctx& c, const DGraph& g0, const jet_config& cfg, int32_t* parts_out,
                    int64_t* pw_out, jet_run_stats* st);
 

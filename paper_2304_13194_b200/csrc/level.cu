@@ -1190,7 +1190,7 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   A.afterburner = cfg.afterburner;
   A.locking = cfg.locking;
   A.phi = cfg.phi;
-  A.no_improve_limit = cfg.no_improve_limit;
+  A.no_improve_limit = level_patience(cfg, level);
   A.sub_buckets = cfg.sub_buckets;
   A.seed = cfg.seed;
   A.level = level;
