@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_throughput_mode.py tests/test_gpu_parity.py tests/test_configs.py tests/test_reference_big.py tests/test_hierarchy_budget.py -m gpu -x -q > gpurun_out/pytest_ab.log 2>&1; tail -3 gpurun_out/pytest_ab.log
+timeout 900 python -m pytest tests/test_throughput_mode.py tests/test_gpu_parity.py tests/test_configs.py tests/test_reference_big.py tests/test_hierarchy_budget.py tests/test_sharding.py -m gpu -x -q > gpurun_out/pytest_ab.log 2>&1; tail -3 gpurun_out/pytest_ab.log
 for v in cur ${VARIANTS:-build/libjet_base.so}; do
   if [ $v = cur ]; then unset JET_LIB; else export JET_LIB=$v; fi
   echo "$v grid128: $(timeout 300 python scripts/ab_time.py grid 128 64 5 2>&1 | tail -1)"

@@ -114,3 +114,17 @@ def test_nccl_transport_single_rank(monkeypatch):
     ctx.detach()
     assert st.cutsize == ref_st.cutsize
     assert np.array_equal(parts, ref_parts)
+
+
+def test_sharded_rmat24_equals_unsharded():
+    """Power-law input at scale (R-MAT 2^24 ef16, k=64, deterministic): two
+    local ranks over the sharded path (levels >= 2^20 vertices sharded)
+    return the unsharded partition bit for bit."""
+    g = gen.rmat_graph(24, 16, 0)
+    cfg = J.RefinerConfig(k=64, imbalance=0.03, seed=0, deterministic=True)
+    ref_parts, ref_pw, ref_st = partition_resident(_lib.DeviceGraph.upload(g), g, cfg)
+    res = _run_sharded(g, cfg, 2, shard_min=1 << 20)
+    for parts, pw, st in res:
+        assert st.cutsize == ref_st.cutsize
+        assert np.array_equal(pw, ref_pw)
+        assert np.array_equal(parts, ref_parts)

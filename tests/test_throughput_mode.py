@@ -55,18 +55,25 @@ def test_throughput_matching_is_a_matching():
 @pytest.mark.parametrize("name", ["rmat22", "rgg16m"])
 def test_large_configs_gate(name):
     """BASELINE configs 3-4 (device-generated, identical to the reference's
-    generators) in throughput mode: balanced, cut <= 1.02x the reference's."""
+    generators) in throughput mode, partition seeds 0-4 where the reference's
+    cuts are recorded (make_quality_big.py): every run balanced, cut geomean
+    <= 1.02x the reference's."""
     from paper_2304_13194_b200.driver import partition_resident
     case = QUALITY[name]
     spec = case["spec"]
     dg = gen.rmat_device(spec[1], spec[2], spec[3]) if spec[0] == "rmat" else \
         gen.geometric_device(spec[1], spec[2], spec[3])
     try:
-        cfg = J.RefinerConfig(k=case["k"], imbalance=case["imbalance"], seed=0, deterministic=False)
-        _, pw, st = partition_resident(dg, None, cfg, want_parts=False)
         n, _, W = dg.info()
-        assert st.balanced
-        assert int(pw.max()) <= J.part_weight_limit(W, case["k"], case["imbalance"])
-        assert st.cutsize <= 1.02 * case["cuts"]["0"], (st.cutsize, case["cuts"]["0"])
+        ratios = []
+        for seed_s, ref_cut in sorted(case["cuts"].items()):
+            cfg = J.RefinerConfig(k=case["k"], imbalance=case["imbalance"], seed=int(seed_s),
+                                  deterministic=False)
+            _, pw, st = partition_resident(dg, None, cfg, want_parts=False)
+            assert st.balanced, (name, seed_s)
+            assert int(pw.max()) <= J.part_weight_limit(W, case["k"], case["imbalance"])
+            ratios.append(st.cutsize / ref_cut)
+        geo = math.exp(sum(math.log(r) for r in ratios) / len(ratios))
+        assert geo <= 1.02, (name, geo, ratios)
     finally:
         dg.free()
