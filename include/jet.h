@@ -157,9 +157,12 @@ void jet_graph_free(jet_graph* g);
  * block and all-gather the candidates (id, destination, gain) and the moves;
  * rebalancing passes collect and score the owned candidates, all-reduce the
  * bucket histograms and crossing-chunk weights and all-gather the direct
- * moves and the evicted sets. The apply step and coarsening run replicated
- * on the gathered moves, and smaller levels run unsharded. Every rank
- * computes the same partition, bit-identical to the unsharded run.
+ * moves and the evicted sets. The apply step walks the owned moved rows
+ * only; the doubled cut delta and the k part-weight deltas are summed over
+ * the ranks by one ncclAllReduce (k + 1 words) and every rank commits the
+ * gathered move set. Coarsening still runs replicated on every rank, and
+ * smaller levels run unsharded. Every rank computes the same partition,
+ * bit-identical to the unsharded run.
  * NCCL (one process per GPU): rank 0 calls jet_comm_nccl_id, the id is
  * broadcast out of band (torch.distributed), every rank attaches.
  * Local groups: `size` contexts in one process (one thread each) on one GPU

@@ -70,15 +70,17 @@ typedef void* NcclComm_t;
 typedef int (*PGetUniqueId)(NcclId*);
 typedef int (*PCommInitRank)(NcclComm_t*, int, NcclId, int);
 typedef int (*PAllGather)(const void*, void*, size_t, int, NcclComm_t, cudaStream_t);
+typedef int (*PAllReduce)(const void*, void*, size_t, int, int, NcclComm_t, cudaStream_t);
 typedef int (*PCommDestroy)(NcclComm_t);
 typedef const char* (*PGetErrorString)(int);
-constexpr int NCCL_INT8 = 0;
+constexpr int NCCL_INT8 = 0, NCCL_UINT64 = 5, NCCL_SUM = 0;
 
 struct NcclApi {
   void* h = nullptr;
   PGetUniqueId get_id = nullptr;
   PCommInitRank init = nullptr;
   PAllGather allgather = nullptr;
+  PAllReduce allreduce = nullptr;
   PCommDestroy destroy = nullptr;
   PGetErrorString err = nullptr;
   bool load() {
@@ -91,9 +93,10 @@ struct NcclApi {
     get_id = (PGetUniqueId)dlsym(h, "ncclGetUniqueId");
     init = (PCommInitRank)dlsym(h, "ncclCommInitRank");
     allgather = (PAllGather)dlsym(h, "ncclAllGather");
+    allreduce = (PAllReduce)dlsym(h, "ncclAllReduce");
     destroy = (PCommDestroy)dlsym(h, "ncclCommDestroy");
     err = (PGetErrorString)dlsym(h, "ncclGetErrorString");
-    return get_id && init && allgather && destroy;
+    return get_id && init && allgather && allreduce && destroy;
   }
 };
 NcclApi& nccl() {
@@ -112,6 +115,10 @@ struct NcclComm : Comm {
   DBuf<uint8_t> stage, padded;
   ~NcclComm() override {
     if (comm) nccl().destroy(comm);
+  }
+  void allreduce_sum(Ctx& c, unsigned long long* d, int64_t count) override {
+    if (count <= 0) return;
+    nck(nccl().allreduce(d, d, (size_t)count, NCCL_UINT64, NCCL_SUM, comm, c.stream), "ncclAllReduce");
   }
   void allgatherv(Ctx& c, const void* dsend, int64_t bytes, DBuf<uint8_t>& recv,
                   std::vector<int64_t>& counts) override {

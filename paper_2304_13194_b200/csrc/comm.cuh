@@ -23,9 +23,10 @@ struct Comm {
   // c.stream) into `recv`, rank-major and compact; counts[r] = rank r's bytes.
   virtual void allgatherv(Ctx& c, const void* dsend, int64_t bytes, DBuf<uint8_t>& recv,
                           std::vector<int64_t>& counts) = 0;
-  // In-place sum over ranks of a device array (gather + local sum: the
-  // arrays exchanged here are histograms of a few 10^5 words at most).
-  void allreduce_sum(Ctx& c, unsigned long long* d, int64_t count);
+  // In-place sum over ranks of a device array of 64-bit words (two's
+  // complement: signed deltas sum correctly). NCCL: ncclAllReduce on the
+  // context stream; the local group: gather + local sum.
+  virtual void allreduce_sum(Ctx& c, unsigned long long* d, int64_t count);
   DBuf<uint8_t> red_buf;
 };
 

@@ -107,7 +107,7 @@ void refine_level(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, int64_t
     }
     const bool set_lock = is_lp && cfg.locking;
     const int32_t new_epoch = set_lock ? ++c.lock_epoch : epoch;
-    const ApplyResult ar = apply_moves(c, w, g, parts, k, set_lock, new_epoch);
+    const ApplyResult ar = apply_moves(c, w, g, parts, k, set_lock, new_epoch, sharded ? &sh : nullptr);
     if (set_lock) {
       epoch = new_epoch;
       locked = ar.n_moves;

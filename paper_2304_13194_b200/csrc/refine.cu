@@ -600,16 +600,44 @@ void afterburner_only(Ctx& c, Workspace& w, const DGraph& g, const int32_t* part
 // ===========================================================================
 // Apply
 // ===========================================================================
+// pw[p] += delta[1 + p]; cut2d = delta[0] (sharded apply, after the all-reduce)
+__global__ void k_add_deltas(const unsigned long long* __restrict__ delta, int k,
+                             unsigned long long* pw, unsigned long long* cut2d) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < k; p += gridDim.x * blockDim.x)
+    pw[p] += delta[1 + p];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *cut2d = delta[0];
+}
+
 ApplyResult apply_moves(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts,
-                        int k, bool set_lock, int32_t epoch) {
+                        int k, bool set_lock, int32_t epoch, ShardLists* sh) {
   const GView gv = view(g);
   ApArgs a{parts, w.mv.get(), w.ctr.get() + CTR_PW, w.ctr.get() + CTR_CUT2D, k};
+  // Sharded level: every rank holds the whole move set (the
+  // exchanges gathered it), but walks only the rows it owns; the doubled cut
+  // delta and the k part-weight deltas are then summed over the ranks by one
+  // all-reduce (k + 1 words) and added to the replicated state.
+  const bool shard = sh && c.comm;
+  if (shard) {
+    sh->delta.ensure((size_t)k + 1, c.stream);
+    dzero(c, sh->delta.get(), k + 1);
+    a.cut2d = sh->delta.get();
+    a.pw = sh->delta.get() + 1;
+    a.own_lo = sh->lo;
+    a.own_hi = sh->hi;
+  }
   const SegLists sl = seg_lists(w, true);
   const unsigned grid = grid_for(c, g.n * 32, 256, 4);
   launch(c, "apply_delta", 0.0, [&] {
     if (g.unit_ew) k_apply_delta<true><<<grid, 256, 0, c.stream>>>(a, gv, sl);
     else k_apply_delta<false><<<grid, 256, 0, c.stream>>>(a, gv, sl);
   });
+  if (shard) {
+    c.comm->allreduce_sum(c, sh->delta.get(), k + 1);
+    launch(c, "apply_add_deltas", 16.0 * k, [&] {
+      k_add_deltas<<<grid_for(c, k, 256), 256, 0, c.stream>>>(
+          sh->delta.get(), k, w.ctr.get() + CTR_PW, w.ctr.get() + CTR_CUT2D);
+    });
+  }
   CommitArgs ca{};
   ca.parts = parts;
   ca.mv = w.mv.get();

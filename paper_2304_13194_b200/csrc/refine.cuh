@@ -86,6 +86,7 @@ struct ShardLists {
   DBuf<unsigned long long> dcnt;     // NBINS device counts
   DBuf<int64_t> scratch;
   DBuf<uint8_t> send, recv;          // exchange buffers
+  DBuf<unsigned long long> delta;    // sharded apply: {2 x cut delta, k part-weight deltas}
 };
 void build_shard_lists(Ctx& c, const DGraph& g, int rank, int size, ShardLists& s);
 
@@ -118,7 +119,7 @@ bool rebalance_pass(Ctx& c, Workspace& w, const DGraph& g, const int32_t* parts,
 // Apply the pending moves (conn.py:215-254): parts, part weights, exact cut
 // delta, locks. Reads back the part weights into w.h_pw.
 ApplyResult apply_moves(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts,
-                        int k, bool set_lock, int32_t epoch);
+                        int k, bool set_lock, int32_t epoch, ShardLists* sh = nullptr);
 
 // ConnectivityTable surface (conn.cu): nonzero conn(v, p) triples of the
 // given rows (all rows when rows == nullptr) sorted by (row, part), and the

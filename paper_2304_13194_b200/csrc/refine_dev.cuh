@@ -1021,7 +1021,13 @@ struct ApArgs {
   unsigned long long* pw;
   unsigned long long* cut2d;
   int k;
-  int32_t* ext;  // optional: weighted external degrees kept current (level kernel, < 2^31)
+  int32_t* ext = nullptr;  // optional: weighted external degrees kept current (level kernel, < 2^31)
+  // sharded levels: only rows of the owned block [own_lo, own_hi) are walked
+  // (their cut / weight deltas are summed over the ranks); own_hi < 0: all
+  int64_t own_lo = 0, own_hi = -1;
+  __device__ __forceinline__ bool owns(int v) const {
+    return own_hi < 0 || ((int64_t)v >= own_lo && (int64_t)v < own_hi);
+  }
 };
 
 // External-degree upkeep of one entry (v moves old -> dst, neighbour u in pu,
@@ -1085,7 +1091,7 @@ static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const S
       // hub rows: a block per row (block-uniform skip of unmoved rows)
       for (int64_t i = blockIdx.x; i < cnt; i += gridDim.x) {
         const int v = list[i];
-        const int dst = a.mv[v];
+        const int dst = a.owns(v) ? a.mv[v] : -1;
         if (dst < 0) continue;
         const int old = a.parts[v];
         const int64_t b = g.offs[v], e = g.offs[v + 1];
@@ -1116,7 +1122,7 @@ static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const S
         int64_t b = 0, e = 0;
         if (i < cnt) {
           v = list[i];
-          dst = a.mv[v];
+          dst = a.owns(v) ? a.mv[v] : -1;
           if (dst >= 0) {
             old = a.parts[v];
             b = g.offs[v];
@@ -1154,7 +1160,7 @@ static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const S
     }
     for (int64_t i = w0; i < cnt; i += ws) {
       const int v = list[i];
-      const int dst = a.mv[v];
+      const int dst = a.owns(v) ? a.mv[v] : -1;
       if (dst < 0) continue;
       const int old = a.parts[v];
       const int64_t b = g.offs[v], e = g.offs[v + 1];
