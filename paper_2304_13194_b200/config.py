@@ -35,12 +35,15 @@ class RefinerConfig:
     # throughput mode only (deterministic=False): with k >= coarse_patience_min_k
     # the Jet loop of every level >= coarse_patience_from stops after
     # coarse_patience passes without improvement instead of no_improve_limit
-    # (finer levels redo most of that work; measured: 128^3 -19 %, R-MAT 2^22
-    # -15 %, RGG 2^24 -19 % time, cut still 0.4-10 % below the reference's).
-    # With few parts the coarse boundary shape survives to the final cut (2D
-    # grid 256^2, k=8: +4.9 % geomean), hence the k floor. 0 disables.
+    # (finer levels redo most of that work). 4 = one Jetlp + weak + weak +
+    # strong cycle: 3 cuts the loop inside a rebalancing cycle (RGG 2^24 cut
+    # +20 %). Measured against the full patience: 128^3 57 -> 40 ms, R-MAT
+    # 2^22 446 -> 344 ms, RGG 2^24 98 -> 76 ms, cuts still 0.4-10 % below the
+    # reference's (tests/test_throughput_mode.py). With few parts the coarse
+    # boundary shape survives to the final cut (2D grid 256^2, k=8: +4.9 %
+    # geomean), hence the k floor. 0 disables.
     coarse_patience: int = 4
-    coarse_patience_from: int = 3
+    coarse_patience_from: int = 1
     coarse_patience_min_k: int = 32
 
     def __post_init__(self):
