@@ -1712,6 +1712,7 @@ struct RowMerge {
   unsigned long long* big_cnt;
   unsigned* overflow;
   int64_t nc;
+  int collect_big;  // append long rows to `big` (0: the list is already built)
 };
 
 // gather row entries of member x of coarse vertex c as sort keys
@@ -1756,9 +1757,11 @@ __device__ void merge_row_warp(const RowMerge& m, int c, unsigned long long* sbu
     const unsigned hm = __ballot_sync(0xffffffffu, head);
     if (head) {
       const int pos = outn + __popc(hm & lanemask_lt());
-      m.tadj[base + pos] = (int32_t)cv;
       if (sum > 2147483647LL) atomicOr(m.overflow, 2u);
-      m.tew[base + pos] = (int32_t)sum;
+      if (m.tadj) {  // nullptr: counting pass of a two-pass contraction
+        m.tadj[base + pos] = (int32_t)cv;
+        m.tew[base + pos] = (int32_t)sum;
+      }
     }
     outn += __popc(hm);
   }
@@ -1778,7 +1781,7 @@ __global__ void __launch_bounds__(256) k_merge_rows(RowMerge m) {
     else if (d <= 64) merge_row_warp<2>(m, (int)c, sbuf[wib]);
     else if (d <= 128) merge_row_warp<4>(m, (int)c, sbuf[wib]);
     else if (d <= 256) merge_row_warp<8>(m, (int)c, sbuf[wib]);
-    else {
+    else if (m.collect_big) {
       if (lane == 0) {
         const unsigned long long i = atomicAdd(m.big_cnt, 1ull);
         m.big[i] = (int32_t)c;
@@ -1897,9 +1900,11 @@ __global__ void __launch_bounds__(256)
       BS(ts).ExclusiveSum(head ? 1 : 0, rank, total);
       const int run = s_out;
       if (head) {
-        m.tadj[base + run + rank] = (int32_t)cv;
         if (sum > 2147483647LL) atomicOr(m.overflow, 2u);
-        m.tew[base + run + rank] = (int32_t)sum;
+        if (m.tadj) {
+          m.tadj[base + run + rank] = (int32_t)cv;
+          m.tew[base + run + rank] = (int32_t)sum;
+        }
       }
       __syncthreads();
       if (threadIdx.x == 0) s_out = run + total;
@@ -1935,7 +1940,7 @@ static double wall_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* partner,
-                                        int32_t* vmap) {
+                                        int32_t* vmap, bool two_pass) {
   static const bool dbg = getenv("JET_COARSEN_TIMES") && getenv("JET_COARSEN_TIMES")[0] == '2';
   double tm = dbg ? wall_s() : 0;
   auto mark = [&](const char* what) {
@@ -1991,16 +1996,20 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
     });
   }
   // the merged rows concatenate both members' rows: their lengths sum to the
-  // fine graph's entry count (no need to read the scan's total back)
+  // fine graph's entry count (no need to read the scan's total back).
+  // Two-pass (memory-tight hierarchies): the first pass only counts each
+  // coarse row's distinct entries, the second merges straight into the
+  // exact-size coarse arrays -- no fine-sized staging copy (34 GB on R-MAT
+  // 2^27) at the price of merging every row twice.
   const int64_t T = g.nnz;
   mark("map+scan");
-  int32_t* tadj_p = c.scratch<int32_t>(7, T);
-  int32_t* tew_p = c.scratch<int32_t>(8, T);
+  int32_t* tadj_p = two_pass ? nullptr : c.scratch<int32_t>(7, T);
+  int32_t* tew_p = two_pass ? nullptr : c.scratch<int32_t>(8, T);
   int32_t* big_p = c.scratch<int32_t>(9, nc);
   DBuf<unsigned long long> big_cnt(1, c.stream);
   dzero(c, big_cnt.get(), 1);
   RowMerge rm{g.offs.get(), g.adj.get(), g.ew.get(), vmap, mem_a_p, mem_b_p, toff_p,
-              rowlen_p, tadj_p, tew_p, cdeg_p, big_p, big_cnt.get(), ovf.get(), nc};
+              rowlen_p, tadj_p, tew_p, cdeg_p, big_p, big_cnt.get(), ovf.get(), nc, 1};
   launch(c, "contract_rows", 12.0 * g.nnz + 8.0 * T + 16.0 * nc, [&] {
     k_merge_rows<<<grid_for(c, nc * 32, 256), 256, 0, c.stream>>>(rm);
   });
@@ -2008,9 +2017,21 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
   d2h(c, &nbig, big_cnt.get(), 1);
   c.sync();
   mark("alloc+rows");
-  if (nbig > 0) {
-    const int64_t nb = (int64_t)nbig;
-    DBuf<int64_t> blen(nb + 1, c.stream), boff(nb + 1, c.stream);
+  // Long rows are gathered, sorted and deduplicated in groups of rows of at
+  // most CH entries (one row may exceed it alone): the key buffers stay a
+  // few GB however dense the level (the dense coarse levels of R-MAT 2^27
+  // route ~4 G entries through here), and CUB's 32-bit item counts hold.
+  const int64_t nb = (int64_t)nbig;
+  const int64_t CH = (int64_t)1 << 28;
+  struct Grp { int64_t s0, ns, base, cnt; };
+  std::vector<Grp> groups;
+  DBuf<int64_t> boff, rel, bend;
+  DBuf<unsigned long long> bk, bk2;
+  int cbits = 1;
+  while ((1LL << cbits) < nc) ++cbits;
+  if (nb > 0) {
+    DBuf<int64_t> blen(nb + 1, c.stream);
+    boff.alloc(nb + 1, c.stream);
     dzero(c, blen.get() + nb, 1);
     launch(c, "big_len", 16.0 * nb, [&] {
       k_big_len<<<grid_for(c, nb, 256), 256, 0, c.stream>>>(big_p, nb, rowlen_p, blen.get());
@@ -2026,13 +2047,6 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
     int64_t BT = 0;
     d2h(c, &BT, boff.get() + nb, 1);
     c.sync();
-    // Long rows are gathered, sorted and deduplicated in groups of rows of at
-    // most CH entries (one row may exceed it alone): the key buffers stay a
-    // few GB however dense the level (the dense coarse levels of R-MAT 2^27
-    // route ~4 G entries through here), and CUB's 32-bit item counts hold.
-    const int64_t CH = (int64_t)1 << 28;
-    struct Grp { int64_t s0, ns, base, cnt; };
-    std::vector<Grp> groups;
     if (BT <= CH) {
       groups.push_back({0, nb, 0, BT});
     } else {
@@ -2049,11 +2063,12 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
     }
     int64_t maxcnt = 0;
     for (const Grp& q : groups) maxcnt = std::max(maxcnt, q.cnt);
-    DBuf<unsigned long long> bk(maxcnt, c.stream), bk2(maxcnt, c.stream);
-    DBuf<int64_t> rel, bend(nb + 1, c.stream);
+    bk.alloc(maxcnt, c.stream);
+    bk2.alloc(maxcnt, c.stream);
+    bend.alloc(nb + 1, c.stream);
     if (groups.size() > 1) rel.alloc(nb + 1, c.stream);
-    int cbits = 1;
-    while ((1LL << cbits) < nc) ++cbits;
+  }
+  auto run_big = [&](const RowMerge& r) {
     for (const Grp& q : groups) {
       JET_REQUIRE(q.cnt < (int64_t)INT_MAX, JET_EUNSUPPORTED, "merged coarse row longer than 2^31 entries");
       const int64_t* off = boff.get();
@@ -2065,7 +2080,7 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
         off = rel.get();
       }
       launch(c, "big_gather", 20.0 * q.cnt, [&] {
-        k_big_gather<<<grid_for(c, q.ns * 256, 256), 256, 0, c.stream>>>(rm, big_p + q.s0, q.ns, off,
+        k_big_gather<<<grid_for(c, q.ns * 256, 256), 256, 0, c.stream>>>(r, big_p + q.s0, q.ns, off,
                                                                          bk.get(), BIG_BLOCK_MAX);
       });
       launch(c, "big_ends", 16.0 * q.ns, [&] {
@@ -2082,14 +2097,15 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
       });
       launch(c, "big_sort_block", 20.0 * q.cnt, [&] {
         k_big_sort_block<<<grid_for(c, q.ns * BIG_BT, BIG_BT), BIG_BT, 0, c.stream>>>(
-            rm, big_p + q.s0, q.ns, off, cbits, bk2.get());
+            r, big_p + q.s0, q.ns, off, cbits, bk2.get());
       });
       launch(c, "big_dedup", 16.0 * q.cnt, [&] {
-        k_big_dedup<<<grid_for(c, q.ns * 256, 256), 256, 0, c.stream>>>(rm, big_p + q.s0, q.ns, off,
+        k_big_dedup<<<grid_for(c, q.ns * 256, 256), 256, 0, c.stream>>>(r, big_p + q.s0, q.ns, off,
                                                                         bk2.get());
       });
     }
-  }
+  };
+  run_big(rm);
   // final offsets
   cg_->offs.alloc(nc + 1, c.stream);
   {
@@ -2111,10 +2127,22 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
   cg_->adj.alloc(cnnz > 0 ? cnnz : 1, c.stream);
   cg_->ew.alloc(cnnz > 0 ? cnnz : 1, c.stream);
   mark("big+offs");
-  launch(c, "copy_rows", 16.0 * cnnz + 16.0 * nc, [&] {
-    k_copy_rows<<<grid_for(c, nc * 32, 256), 256, 0, c.stream>>>(toff_p, cg_->offs.get(), tadj_p,
-                                                                tew_p, cg_->adj.get(), cg_->ew.get(), nc);
-  });
+  if (two_pass) {
+    RowMerge r2 = rm;  // merge again, straight into the coarse arrays
+    r2.toff = cg_->offs.get();
+    r2.tadj = cg_->adj.get();
+    r2.tew = cg_->ew.get();
+    r2.collect_big = 0;
+    launch(c, "contract_rows", 12.0 * g.nnz + 8.0 * cnnz + 16.0 * nc, [&] {
+      k_merge_rows<<<grid_for(c, nc * 32, 256), 256, 0, c.stream>>>(r2);
+    });
+    run_big(r2);
+  } else {
+    launch(c, "copy_rows", 16.0 * cnnz + 16.0 * nc, [&] {
+      k_copy_rows<<<grid_for(c, nc * 32, 256), 256, 0, c.stream>>>(toff_p, cg_->offs.get(), tadj_p,
+                                                                  tew_p, cg_->adj.get(), cg_->ew.get(), nc);
+    });
+  }
   mark("copy");
   finalize_graph(c, *cg_);
   mark("finalize");
@@ -2155,7 +2183,7 @@ void Hierarchy::release(int i) {
 static std::unique_ptr<DGraph> contract_level(Ctx& c, Hierarchy& h, int i, const DGraph& fine,
                                               const int32_t* partner, int32_t* vmap) {
   try {
-    return device_contract(c, fine, partner, vmap);
+    return device_contract(c, fine, partner, vmap, h.budget != 0);
   } catch (const Error& e) {
     if (e.code != JET_ENOMEM || h.budget == 0) throw;
     c.sync();
@@ -2164,14 +2192,20 @@ static std::unique_ptr<DGraph> contract_level(Ctx& c, Hierarchy& h, int i, const
     CK(cudaStreamSynchronize(c.stream));
     CK(cudaMemPoolTrimTo(current_pool(), 0));
     c.pool_reserved = 0;
-    return device_contract(c, fine, partner, vmap);
+    return device_contract(c, fine, partner, vmap, true);
   }
 }
 
+// Rebuild chain j -> i (j the highest resident level below i). Uncoarsening
+// then needs i-1, i-2, ..., j+1 in turn, so the chain keeps its midpoint as a
+// checkpoint when the budget holds it next to level i (recursive halving:
+// each later rebuild starts from the nearest checkpoint below it); every other
+// intermediate level is dropped as soon as the next one is built.
 const DGraph& hier_acquire(Ctx& c, Hierarchy& h, int i) {
   if (h.resident(i)) return h.level(i);
   int j = i - 1;
   while (!h.resident(j)) --j;
+  const int mid = (j + i + 1) / 2;
   for (int t = j + 1; t <= i; ++t) {
     JET_REQUIRE(h.partners[t - 1].get() != nullptr, JET_EINTERNAL, "evicted level without its matching");
     // rebuilds overwrite maps[t-1] with identical values
@@ -2180,10 +2214,12 @@ const DGraph& hier_acquire(Ctx& c, Hierarchy& h, int i) {
     JET_REQUIRE(h.owned[t - 1]->n == h.lv_n[t] && h.owned[t - 1]->nnz == h.lv_nnz[t], JET_EINTERNAL,
                 "rebuilt level differs from the original");
     ++h.rebuilds;
-    // keep the newest levels (the next ones uncoarsening needs): evict from
-    // the bottom of the chain
-    if (h.budget) h.shrink_to(h.budget, t, i);
+    if (t - 1 > j && t - 1 != mid) h.release(t - 1);  // a plain intermediate
+    // keep the checkpoint only if it fits next to the target level (level
+    // sizes along a chain are close: level t stands in for level i)
+    if (t - 1 == mid && h.budget && h.resident_bytes() > h.budget) h.release(t - 1);
   }
+  if (h.budget) h.shrink_to(h.budget, i, mid);
   return h.level(i);
 }
 

@@ -40,8 +40,10 @@ const DGraph& hier_acquire(Ctx& c, Hierarchy& h, int i);
 void device_match(Ctx& c, const DGraph& g, int32_t* partner);
 // partner[partner[v]] == v for all v (ids already range-checked)
 bool device_is_involution(Ctx& c, const int32_t* partner, int64_t n);
+// two_pass: count, then merge straight into the exact-size coarse arrays (no
+// fine-sized staging buffers; memory-tight hierarchies)
 std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* partner,
-                                        int32_t* vmap);
+                                        int32_t* vmap, bool two_pass = false);
 // fast: throughput-mode matching (device_match_fast), else the reference's
 // exact matching semantics.
 void device_build_hierarchy(Ctx& c, const DGraph& g0, int64_t target, Hierarchy& h,

@@ -227,9 +227,9 @@ void run_partition(Ctx& c, const DGraph& g0, const jet_config& cfg, int32_t* par
   // the host for 50-90 ms in ~1 of 8 calls).
   // When the whole hierarchy cannot fit (R-MAT 2^26+: every level keeps ~m
   // edges), the owned levels get a byte budget: what is left after the input,
-  // the contraction's working set (fine level, merged-row scratch, coarse
-  // level, sort groups ~3.3x the input CSR) and the refinement workspace;
-  // evicted levels are rebuilt on demand (coarsen.cuh Hierarchy).
+  // the contraction's working set (two-pass: the coarse level being built +
+  // the long-row sort groups, ~1.3x the input CSR) and the refinement
+  // workspace; evicted levels are rebuilt on demand (coarsen.cuh Hierarchy).
   size_t budget = 0;
   {
     const size_t csr = graph_bytes(g0);
@@ -244,7 +244,7 @@ void run_partition(Ctx& c, const DGraph& g0, const jet_config& cfg, int32_t* par
       CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &resv));
       CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
       const size_t avail = fr + (resv > used ? resv - used : 0);
-      const size_t work = (size_t)(3.3 * (double)csr) + (size_t)g0.n * 96 + ((size_t)1 << 30);
+      const size_t work = (size_t)(1.3 * (double)csr) + (size_t)g0.n * 96 + ((size_t)3 << 30);
       if (12 * csr > avail) {  // the hierarchy may not fit: budgeted
         budget = avail > work + csr ? avail - work : csr;
         c.reserve_pool(std::min<size_t>(avail / 20 * 19, c.pool_reserved + fr / 20 * 19));
