@@ -1855,6 +1855,52 @@ __global__ void __launch_bounds__(BIG_BT)
   }
 }
 
+// Counting pass of a two-pass contraction, rows of up to BIG_BLOCK_MAX
+// entries: the number of distinct coarse neighbours (self loops excluded) by
+// one insertion pass into a shared-memory hash set (load factor <= 1/2)
+// instead of a radix sort -- the second pass sorts.
+constexpr int BIG_HASH_BITS = 13;
+constexpr int BIG_HASH = 1 << BIG_HASH_BITS;
+static_assert(BIG_HASH >= 2 * BIG_BLOCK_MAX, "hash set load factor");
+
+__global__ void __launch_bounds__(BIG_BT)
+    k_big_count_block(RowMerge m, const int32_t* __restrict__ big, int64_t nbig) {
+  __shared__ unsigned tab[BIG_HASH];
+  __shared__ int s_cnt;
+  for (int i = threadIdx.x; i < BIG_HASH; i += BIG_BT) tab[i] = 0xffffffffu;
+  for (int64_t i = blockIdx.x; i < nbig; i += gridDim.x) {
+    const int c = big[i];
+    const int64_t d = m.rowlen[c];  // block-uniform
+    if (d > BIG_BLOCK_MAX) continue;
+    const int a = m.mem_a[c], b = m.mem_b[c];
+    const int64_t da = m.offs[a + 1] - m.offs[a];
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    int mine = 0;
+    for (int64_t idx = threadIdx.x; idx < d; idx += BIG_BT) {
+      const unsigned long long k = merged_key(m, c, idx, a, b, da);
+      if (k == ~0ull) continue;  // self loop
+      const unsigned cv = (unsigned)(k >> 32);
+      unsigned h = (cv * 0x9e3779b1u) >> (32 - BIG_HASH_BITS);  // Fibonacci hashing: top bits
+      while (true) {
+        const unsigned old = atomicCAS(&tab[h], 0xffffffffu, cv);
+        if (old == 0xffffffffu) {
+          ++mine;
+          break;
+        }
+        if (old == cv) break;
+        h = (h + 1) & (BIG_HASH - 1);
+      }
+    }
+    mine = __reduce_add_sync(0xffffffffu, mine);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&s_cnt, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) m.cdeg[c] = s_cnt;
+    for (int q = threadIdx.x; q < BIG_HASH; q += BIG_BT) tab[q] = 0xffffffffu;
+    __syncthreads();
+  }
+}
+
 // segment ends for the device-wide sort: rows sorted on chip get empty segments
 __global__ void k_big_ends(const int32_t* __restrict__ big, int64_t nbig,
                            const int64_t* __restrict__ rowlen, const int64_t* __restrict__ off,
@@ -1873,13 +1919,15 @@ __global__ void k_big_len(const int32_t* __restrict__ big, int64_t nbig,
 
 __global__ void __launch_bounds__(256)
     k_big_dedup(RowMerge m, const int32_t* __restrict__ big, int64_t nbig,
-                const int64_t* __restrict__ boff, const unsigned long long* __restrict__ keys) {
+                const int64_t* __restrict__ boff, const unsigned long long* __restrict__ keys,
+                int64_t min_len) {
   typedef cub::BlockScan<int, 256> BS;
   __shared__ typename BS::TempStorage ts;
   __shared__ int s_out;
   for (int64_t i = blockIdx.x; i < nbig; i += gridDim.x) {
     const int c = big[i];
     const int64_t o = boff[i], d = m.rowlen[c];
+    if (d <= min_len) continue;  // counted by k_big_count_block
     const int64_t base = m.toff[c];
     if (threadIdx.x == 0) s_out = 0;
     __syncthreads();
@@ -2095,13 +2143,21 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
         CK(cub::DeviceSegmentedSort::SortKeys(p, tmp, bk.get(), bk2.get(), (int)q.cnt, (int)q.ns, off,
                                               bend.get(), c.stream));
       });
-      launch(c, "big_sort_block", 20.0 * q.cnt, [&] {
-        k_big_sort_block<<<grid_for(c, q.ns * BIG_BT, BIG_BT), BIG_BT, 0, c.stream>>>(
-            r, big_p + q.s0, q.ns, off, cbits, bk2.get());
-      });
+      const bool counting = r.tadj == nullptr;  // first pass of a two-pass contraction
+      if (counting) {
+        launch(c, "big_count_block", 12.0 * q.cnt, [&] {
+          k_big_count_block<<<grid_for(c, q.ns * BIG_BT, BIG_BT), BIG_BT, 0, c.stream>>>(r, big_p + q.s0,
+                                                                                        q.ns);
+        });
+      } else {
+        launch(c, "big_sort_block", 20.0 * q.cnt, [&] {
+          k_big_sort_block<<<grid_for(c, q.ns * BIG_BT, BIG_BT), BIG_BT, 0, c.stream>>>(
+              r, big_p + q.s0, q.ns, off, cbits, bk2.get());
+        });
+      }
       launch(c, "big_dedup", 16.0 * q.cnt, [&] {
-        k_big_dedup<<<grid_for(c, q.ns * 256, 256), 256, 0, c.stream>>>(r, big_p + q.s0, q.ns, off,
-                                                                        bk2.get());
+        k_big_dedup<<<grid_for(c, q.ns * 256, 256), 256, 0, c.stream>>>(
+            r, big_p + q.s0, q.ns, off, bk2.get(), counting ? BIG_BLOCK_MAX : 0);
       });
     }
   };
