@@ -155,9 +155,11 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def load_traffic(kernel: str):
-    """dram bytes per launch of `kernel` from the committed ncu capture."""
-    f = ROOT / "profiles" / "ncu_traffic.json"
+def load_traffic(kernel: str, det: bool = False):
+    """dram bytes per launch of `kernel` from the committed ncu launch list of
+    the same mode (profiles/ncu_traffic.json: throughput, ncu_traffic_det.json:
+    deterministic; scripts/ncu_traffic.py)."""
+    f = ROOT / "profiles" / ("ncu_traffic_det.json" if det else "ncu_traffic.json")
     try:
         d = json.loads(f.read_text())
         return d.get(kernel, {}).get("dram_bytes_per_launch")
@@ -459,7 +461,7 @@ def run_ours(args, world, rank, local):
             "roofline": {"bound": "hbm", "kernel": dominant,
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
-                         "traffic": load_traffic(dominant),
+                         "traffic": load_traffic(dominant, det),
                          "algorithmic_bytes_per_launch": per_launch_bytes,
                          "launches": dom["launches"], "share_of_step": dominant_share},
             "cpu_baseline": cpu,
