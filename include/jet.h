@@ -80,15 +80,15 @@ typedef struct {
   int32_t locking;
   int32_t deterministic; /* 1: bit-exact reference semantics in every kernel;
                             0: throughput mode (hashed-priority matching,
-                            shorter refinement patience on coarse levels;
+                            shorter Jet-loop patience when k >= 32;
                             cut gated at 1.02x the reference's geomean,
                             balance always met) */
   int32_t verbose;
-  int32_t coarse_patience;      /* throughput mode only: no_improve_limit on
-                                   levels >= coarse_patience_from when
-                                   k >= coarse_patience_min_k (0: off) */
-  int32_t coarse_patience_from;
-  int32_t coarse_patience_min_k;
+  int32_t throughput_patience;  /* throughput mode only: no_improve_limit on
+                                   levels >= patience_from_level when
+                                   k >= patience_min_k (0: off) */
+  int32_t patience_from_level;
+  int32_t patience_min_k;
 } jet_config;
 
 typedef struct {

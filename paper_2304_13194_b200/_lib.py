@@ -52,8 +52,8 @@ class JetConfig(C.Structure):
         ("phi", C.c_double), ("no_improve_limit", i32), ("sub_buckets", i32),
         ("seed", C.c_uint64), ("coarse_target", i32), ("restarts", i32),
         ("afterburner", i32), ("locking", i32), ("deterministic", i32),
-        ("verbose", i32), ("coarse_patience", i32), ("coarse_patience_from", i32),
-        ("coarse_patience_min_k", i32),
+        ("verbose", i32), ("throughput_patience", i32), ("patience_from_level", i32),
+        ("patience_min_k", i32),
     ]
 
 

@@ -32,19 +32,19 @@ class RefinerConfig:
     restarts: int = 8
     afterburner: bool = True
     locking: bool = True
-    # throughput mode only (deterministic=False): with k >= coarse_patience_min_k
-    # the Jet loop of every level >= coarse_patience_from stops after
-    # coarse_patience passes without improvement instead of no_improve_limit
-    # (finer levels redo most of that work). 4 = one Jetlp + weak + weak +
-    # strong cycle: 3 cuts the loop inside a rebalancing cycle (RGG 2^24 cut
-    # +20 %). Measured against the full patience: 128^3 57 -> 40 ms, R-MAT
-    # 2^22 446 -> 344 ms, RGG 2^24 98 -> 76 ms, cuts still 0.4-10 % below the
+    # throughput mode only (deterministic=False): with k >= patience_min_k the
+    # Jet loop of every level >= patience_from_level stops after
+    # throughput_patience passes without improvement instead of
+    # no_improve_limit. 4 = one Jetlp + weak + weak + strong cycle: 3 cuts the
+    # loop inside a rebalancing cycle (RGG 2^24 cut +20 %). Measured against
+    # the reference's patience on every level: 128^3 57 -> 36 ms, R-MAT 2^22
+    # 446 -> 315 ms, RGG 2^24 98 -> 73 ms, cuts still 0.4-9 % below the
     # reference's (tests/test_throughput_mode.py). With few parts the coarse
-    # boundary shape survives to the final cut (2D grid 256^2, k=8: +4.9 %
-    # geomean), hence the k floor. 0 disables.
-    coarse_patience: int = 4
-    coarse_patience_from: int = 1
-    coarse_patience_min_k: int = 32
+    # boundary survives to the final cut (2D grid 256^2, k=8: +4.9 % geomean),
+    # hence the k floor. 0 disables.
+    throughput_patience: int = 4
+    patience_from_level: int = 0
+    patience_min_k: int = 32
 
     def __post_init__(self):
         if self.k < 1:
@@ -56,8 +56,8 @@ class RefinerConfig:
                 raise ValueError("gain-ratio constants must be in [0, 1]")
         if self.no_improve_limit < 1:
             raise ValueError("no_improve_limit must be >= 1")
-        if min(self.coarse_patience, self.coarse_patience_from, self.coarse_patience_min_k) < 0:
-            raise ValueError("coarse_patience* must be >= 0")
+        if min(self.throughput_patience, self.patience_from_level, self.patience_min_k) < 0:
+            raise ValueError("throughput_patience* must be >= 0")
         if self.sub_buckets < 1:
             raise ValueError("sub_buckets must be >= 1")
         if self.imbalance < 0:
@@ -99,7 +99,7 @@ def to_c(config: RefinerConfig, total_weight: int) -> _lib.JetConfig:
         afterburner=int(bool(config.afterburner)), locking=int(bool(config.locking)),
         deterministic=int(bool(config.deterministic)), verbose=0,
         # reference-side configs (jetpart_compat) have no such fields: off
-        coarse_patience=getattr(config, "coarse_patience", 0),
-        coarse_patience_from=getattr(config, "coarse_patience_from", 0),
-        coarse_patience_min_k=getattr(config, "coarse_patience_min_k", 0),
+        throughput_patience=getattr(config, "throughput_patience", 0),
+        patience_from_level=getattr(config, "patience_from_level", 0),
+        patience_min_k=getattr(config, "patience_min_k", 0),
     )

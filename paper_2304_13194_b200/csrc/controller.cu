@@ -15,12 +15,12 @@
 namespace jet {
 
 // Jet loop patience of a level: the reference's no_improve_limit, shortened
-// on coarse levels in throughput mode (jet_config.coarse_patience).
+// in throughput mode (jet_config.throughput_patience).
 int level_patience(const jet_config& cfg, int level) {
-  if (cfg.deterministic || cfg.coarse_patience <= 0 || level < cfg.coarse_patience_from ||
-      cfg.k < cfg.coarse_patience_min_k)
+  if (cfg.deterministic || cfg.throughput_patience <= 0 || level < cfg.patience_from_level ||
+      cfg.k < cfg.patience_min_k)
     return cfg.no_improve_limit;
-  return std::min(cfg.coarse_patience, cfg.no_improve_limit);
+  return std::min(cfg.throughput_patience, cfg.no_improve_limit);
 }
 
 static double now_s() {

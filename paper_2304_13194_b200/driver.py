@@ -123,9 +123,9 @@ def build_metrics(graph, config, state, st, total, W, limit) -> dict:
             "deterministic": config.deterministic, "coarse_target": config.coarse_target,
             "restarts": config.restarts, "afterburner": config.afterburner,
             "locking": config.locking,
-            "coarse_patience": getattr(config, "coarse_patience", 0),
-            "coarse_patience_from": getattr(config, "coarse_patience_from", 0),
-            "coarse_patience_min_k": getattr(config, "coarse_patience_min_k", 0),
+            "throughput_patience": getattr(config, "throughput_patience", 0),
+            "patience_from_level": getattr(config, "patience_from_level", 0),
+            "patience_min_k": getattr(config, "patience_min_k", 0),
         },
     }
 
