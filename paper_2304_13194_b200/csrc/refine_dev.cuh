@@ -843,71 +843,6 @@ struct SegLists {
   const unsigned long long* cnt;  // NBINS consecutive counters
 };
 
-// Afterburner over the short-row tiers: a G-lane group per row, so a warp
-// keeps 32/G rows in flight (a warp per ~10-entry row left the coarse levels
-// latency-bound).
-template <int G, bool UNIT>
-static __device__ __forceinline__ void ab_group_rows(const AbArgs& a, const GView& g,
-                                                     const int32_t* __restrict__ list, int64_t cnt,
-                                                     int t, const RbSegsDev& mseg, int64_t w0,
-                                                     int64_t ws, unsigned long long* wr,
-                                                     unsigned long long* we, long long* nmove) {
-  constexpr int RPS = 32 / G;
-  const int lane = threadIdx.x & 31, gl = lane & (G - 1), grp = lane / G;
-  const unsigned gm = group_mask<G>();
-  for (int64_t base = w0 * RPS; base < cnt; base += ws * RPS) {
-    const int64_t i = base + grp;
-    const bool has = i < cnt;
-    int v = 0, own = -1, dv = -1;
-    long long Fv = 0;
-    int64_t b = 0, e = 0;
-    if (has) {
-      v = list[i];
-      own = a.parts[v];
-      dv = a.cdest[v];
-      Fv = a.F[v];
-      b = g.offs[v];
-      e = g.offs[v + 1];
-      if (wr && gl == 0) {
-        *wr += 1;
-        *we += (unsigned long long)(e - b);
-      }
-    }
-    long long f2 = 0;
-    for (int64_t j = b + gl; j < e; j += G) {
-      const int u = g.adj[j];
-      int eff = a.parts[u];
-      const int cu = a.cdest[u];
-      if (cu >= 0) {
-        const long long Fu = a.F[u];
-        if (Fu > Fv || (Fu == Fv && u < v)) eff = cu;
-      }
-      const int w = UNIT ? 1 : g.ew[j];
-      f2 += (eff == dv) ? w : (eff == own) ? -w : 0;
-    }
-    f2 = gsum<G>(f2, gm);
-    if (has && gl == 0) {
-      if (a.f2_out) a.f2_out[v] = f2;
-      if (f2 >= 0) {
-        if (a.move_list) {
-          a.mv[v] = dv;
-          const unsigned long long q = atomicAdd(a.move_cnt + t, 1ull);
-          a.move_list[mseg.b[t] + q] = v;
-        } else if (nmove) {
-          a.mv[v] = dv;
-          *nmove += 1;
-        }
-      }
-    }
-  }
-}
-
-// One warp per candidate over all tiers (candidate sets are small).
-// With a move list, moves are appended per row (host-driven path); without
-// one (level kernel) only mv[v] is set and the moves are counted into
-// *nmove, and the apply phase walks the candidate lists skipping unmoved
-// rows -- one atomic per row on a hot counter serialises in L2.
-// wr/we (optional): += rows / entries visited, for the roofline accounting.
 // Afterburner sum of one long row over the entries j = j0, j0 + stride, ...
 // (a warp or block per row): RU strides are loaded per step, so each lane
 // has RU independent adjacency -> (part, dest) -> F chains in flight
@@ -944,6 +879,60 @@ static __device__ __forceinline__ long long ab_row_f2(const AbArgs& a, const GVi
   return f2;
 }
 
+// Afterburner over the short-row tiers: a G-lane group per row, so a warp
+// keeps 32/G rows in flight (a warp per ~10-entry row left the coarse levels
+// latency-bound).
+template <int G, bool UNIT>
+static __device__ __forceinline__ void ab_group_rows(const AbArgs& a, const GView& g,
+                                                     const int32_t* __restrict__ list, int64_t cnt,
+                                                     int t, const RbSegsDev& mseg, int64_t w0,
+                                                     int64_t ws, unsigned long long* wr,
+                                                     unsigned long long* we, long long* nmove) {
+  constexpr int RPS = 32 / G;
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1), grp = lane / G;
+  const unsigned gm = group_mask<G>();
+  for (int64_t base = w0 * RPS; base < cnt; base += ws * RPS) {
+    const int64_t i = base + grp;
+    const bool has = i < cnt;
+    int v = 0, own = -1, dv = -1;
+    long long Fv = 0;
+    int64_t b = 0, e = 0;
+    if (has) {
+      v = list[i];
+      own = a.parts[v];
+      dv = a.cdest[v];
+      Fv = a.F[v];
+      b = g.offs[v];
+      e = g.offs[v + 1];
+      if (wr && gl == 0) {
+        *wr += 1;
+        *we += (unsigned long long)(e - b);
+      }
+    }
+    long long f2 = ab_row_f2<UNIT>(a, g, v, own, dv, Fv, b + gl, e, G);
+    f2 = gsum<G>(f2, gm);
+    if (has && gl == 0) {
+      if (a.f2_out) a.f2_out[v] = f2;
+      if (f2 >= 0) {
+        if (a.move_list) {
+          a.mv[v] = dv;
+          const unsigned long long q = atomicAdd(a.move_cnt + t, 1ull);
+          a.move_list[mseg.b[t] + q] = v;
+        } else if (nmove) {
+          a.mv[v] = dv;
+          *nmove += 1;
+        }
+      }
+    }
+  }
+}
+
+// One warp per candidate over all tiers (candidate sets are small).
+// With a move list, moves are appended per row (host-driven path); without
+// one (level kernel) only mv[v] is set and the moves are counted into
+// *nmove, and the apply phase walks the candidate lists skipping unmoved
+// rows -- one atomic per row on a hot counter serialises in L2.
+// wr/we (optional): += rows / entries visited, for the roofline accounting.
 template <bool UNIT>
 static __device__ void afterburner_rows(const AbArgs& a, const GView& g, const SegLists& sl,
                                  const RbSegsDev& mseg, int64_t w0, int64_t ws,
@@ -1134,16 +1123,7 @@ static __device__ void apply_delta_rows(const ApArgs& a, const GView& g, const S
           }
         }
         long long d = 0, ev = 0;
-        for (int64_t j = b + gl; j < e; j += G) {
-          const int u = g.adj[j];
-          const int pu = a.parts[u];
-          const int mu = a.mv[u];
-          const int nu = mu >= 0 ? mu : pu;
-          const long long w = UNIT ? 1 : g.ew[j];
-          const long long cc = w * ((long long)(nu != dst) - (long long)(pu != old));
-          d += mu >= 0 ? cc : 2 * cc;
-          if (a.ext) ext_entry(a.ext, u, pu, mu, nu, dst, old, w, ev);
-        }
+        ap_row<UNIT>(a, g, dst, old, b + gl, e, G, d, ev);
         acc += d;
         if (a.ext) {
 #pragma unroll
