@@ -20,6 +20,13 @@ CASES = {
 }
 
 _G = None
+_K = None
+
+
+def _init(g, k):
+    global _G, _K
+    sys.path.insert(0, str(ROOT / "oracle"))
+    _G, _K = g, k
 
 
 def _one(seed):
@@ -45,9 +52,13 @@ if __name__ == "__main__":
         g = generators.rmat_graph(spec[1], spec[2], spec[3]) if spec[0] == "rmat" else \
             generators.geometric_graph(spec[1], spec[2], spec[3])
         tg = time.time() - t
-        _G, _K = g, k
-        with mp.get_context("fork").Pool(min(len(seeds), 4)) as pool:
-            res = pool.map(_one, seeds)
+        globals()["_G"], globals()["_K"] = g, k
+        if len(seeds) == 1:
+            res = [_one(seeds[0])]
+        else:  # spawn, not fork: the oracle's OpenMP runtime does not survive a fork
+            with mp.get_context("spawn").Pool(min(len(seeds), 4), initializer=_init,
+                                              initargs=(g, k)) as pool:
+                res = pool.map(_one, seeds)
         for seed, cut, tp in res:
             print(name, g.n, g.m, "gen", round(tg, 1), "s seed", seed, "partition", tp, "s cut", cut,
                   flush=True)

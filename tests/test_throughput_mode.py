@@ -22,10 +22,18 @@ QUALITY = json.loads((Path(__file__).parent / "golden" / "quality.json").read_te
 def _graph(spec):
     if spec[0] == "grid":
         return gen.grid_graph(spec[1], spec[2])
+    if spec[0] == "rmat":  # device generator, bit-identical to the reference's
+        return gen.rmat_graph(spec[1], spec[2], spec[3])
+    if spec[0] == "rgg":
+        return gen.geometric_graph(spec[1], spec[2], spec[3])
     return gen.grid27_graph(spec[1])
 
 
-@pytest.mark.parametrize("name", ["grid2d_256x256", "grid27_64", "grid27_128"])
+GATED = [n for n in ("grid2d_256x256", "grid27_64", "grid27_128", "grid2d_512x512_k64",
+                     "grid27_64_k256", "rmat18_k64", "rgg18_k128") if n in QUALITY]
+
+
+@pytest.mark.parametrize("name", GATED)
 def test_cut_within_2pct_geomean(name):
     case = QUALITY[name]
     g = _graph(case["spec"])
