@@ -143,6 +143,22 @@ int jet_graph_upload(jet_ctx* ctx, int64_t n, const int64_t* row_offsets,
                      const void* edge_weights, int ew_dtype,
                      const void* vertex_weights, int vw_dtype,
                      jet_graph** out);
+/* A 1D-distributed level: this rank's block of rows
+ * [row_lo, row_hi). row_offsets and vertex_weights are complete (n+1 / n);
+ * adjacency and edge_weights hold only the block's entries
+ * [row_offsets[row_lo], row_offsets[row_hi]). Attach the communicator first
+ * (the ranks agree on the level's weight statistics). Partition such graphs in
+ * throughput mode: the finest level's matching, contraction and refinement
+ * run distributed; the coarser levels are assembled on every rank. */
+int jet_graph_upload_block(jet_ctx* ctx, int64_t n, const int64_t* row_offsets,
+                           const void* adjacency_block, int adj_dtype,
+                           const void* edge_weights_block, int ew_dtype,
+                           const void* vertex_weights, int vw_dtype, int64_t row_lo,
+                           int64_t row_hi, jet_graph** out);
+/* The rows this rank stores: [row_lo, row_hi) and their entry count (the
+ * whole graph for an ordinary upload). */
+int jet_graph_block(const jet_graph* g, int64_t* row_lo, int64_t* row_hi,
+                    int64_t* local_entries);
 int jet_graph_info(const jet_graph* g, int64_t* n, int64_t* nnz,
                    int64_t* total_vertex_weight);
 int jet_graph_download(jet_ctx* ctx, const jet_graph* g, int64_t* row_offsets,

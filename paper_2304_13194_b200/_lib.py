@@ -90,6 +90,9 @@ _SIGS = {
     "jet_timer_stop": (C.c_int, [P, C.POINTER(C.c_double)]),
     "jet_flush_l2": (C.c_int, [P]),
     "jet_graph_upload": (C.c_int, [P, i64, P, P, C.c_int, P, C.c_int, P, C.c_int, C.POINTER(P)]),
+    "jet_graph_upload_block": (C.c_int, [P, i64, P, P, C.c_int, P, C.c_int, P, C.c_int, i64, i64,
+                                         C.POINTER(P)]),
+    "jet_graph_block": (C.c_int, [P, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
     "jet_graph_info": (C.c_int, [P, P, P, P]),
     "jet_graph_download": (C.c_int, [P, P, P, P, P, P]),
     "jet_graph_free": (None, [P]),
@@ -339,6 +342,29 @@ class DeviceGraph:
             ctx.handle, n, ptr(offs), ptr(arrays[0]), codes[0], ptr(arrays[1]), codes[1],
             ptr(arrays[2]), codes[2], C.byref(h)))
         return cls(ctx, h)
+
+    @classmethod
+    def upload_block(cls, graph, lo: int, hi: int, ctx: Context | None = None) -> "DeviceGraph":
+        """This rank's block [lo, hi) of a 1D-distributed graph: complete
+        row offsets and vertex weights, only the block's adjacency/weights
+        (include/jet.h jet_graph_upload_block). Attach the communicator first."""
+        ctx = ctx or Context.default()
+        (offs, *arrays), codes = csr_arrays(graph)
+        n = len(offs) - 1
+        e0, e1 = int(offs[lo]), int(offs[hi])
+        adj = np.ascontiguousarray(arrays[0][e0:e1])
+        ew = np.ascontiguousarray(arrays[1][e0:e1])
+        h = P()
+        check(lib().jet_graph_upload_block(
+            ctx.handle, n, ptr(offs), ptr(adj), codes[0], ptr(ew), codes[1],
+            ptr(arrays[2]), codes[2], int(lo), int(hi), C.byref(h)))
+        return cls(ctx, h)
+
+    def block(self):
+        """(row_lo, row_hi, entries stored on this rank)."""
+        lo, hi, e = i64(), i64(), i64()
+        check(lib().jet_graph_block(self.handle, C.byref(lo), C.byref(hi), C.byref(e)))
+        return lo.value, hi.value, e.value
 
     def info(self):
         n, nnz, w = i64(), i64(), i64()

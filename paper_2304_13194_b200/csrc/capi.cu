@@ -92,6 +92,37 @@ int jet_graph_upload(jet_ctx* ctx, int64_t n, const int64_t* row_offsets, const 
   API_END
 }
 
+int jet_graph_upload_block(jet_ctx* ctx, int64_t n, const int64_t* row_offsets,
+                           const void* adjacency_block, int adj_dtype,
+                           const void* edge_weights_block, int ew_dtype,
+                           const void* vertex_weights, int vw_dtype, int64_t row_lo,
+                           int64_t row_hi, jet_graph** out) {
+  API_BEGIN
+  Ctx& c = C(ctx);
+  JET_REQUIRE(out, JET_EINVAL, "out is NULL");
+  JET_REQUIRE(row_hi >= 0, JET_EINVAL, "row_hi must be >= 0");
+  auto g = upload_graph(c, n, row_offsets, adjacency_block, adj_dtype, edge_weights_block, ew_dtype,
+                        vertex_weights, vw_dtype, row_lo, row_hi);
+  jet_graph* jg = new jet_graph();
+  jg->g = std::move(g);
+  jg->device = c.device;
+  jg->ctx = &c;
+  ctx_retain(&c);
+  *out = jg;
+  API_END
+}
+
+int jet_graph_block(const jet_graph* g, int64_t* row_lo, int64_t* row_hi,
+                    int64_t* local_entries) {
+  API_BEGIN
+  JET_REQUIRE(g && g->g, JET_EINVAL, "graph is NULL");
+  const DGraph& d = *g->g;
+  if (row_lo) *row_lo = d.partial() ? d.row_lo : 0;
+  if (row_hi) *row_hi = d.partial() ? d.row_hi : d.n;
+  if (local_entries) *local_entries = d.local_nnz();
+  API_END
+}
+
 struct jet_group {
   jet::LocalGroup g;
   explicit jet_group(int n) : g(n) {}

@@ -15,6 +15,7 @@
 // rows merged per coarse vertex, sorted by neighbour and de-duplicated with
 // summed weights, self loops dropped.
 #include "coarsen.cuh"
+#include "comm.cuh"
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <cub/device/device_radix_sort.cuh>
@@ -1302,12 +1303,13 @@ template <bool UNIT>
 __global__ void __launch_bounds__(256)
     k_propose_fast(GView g, int64_t n, const int32_t* __restrict__ partner, int32_t* prop,
                    int32_t* elist, unsigned long long* ecnt, unsigned salt,
-                   const unsigned long long* prev) {
+                   const unsigned long long* prev, int64_t v_lo = 0) {
+  // vertices [v_lo, n): a distributed level proposes for its own rows only
   if (fast_round_dead(prev)) return;
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t base = w0 * 32; base < n; base += nw * 32) {
+  for (int64_t base = v_lo + w0 * 32; base < n; base += nw * 32) {
     const int64_t idx = base + lane;
     int v = (int)idx, deg = 0;
     int64_t beg = 0;
@@ -1720,16 +1722,34 @@ struct RowMerge {
   unsigned* overflow;
   int64_t nc;
   int collect_big;  // append long rows to `big` (0: the list is already built)
+  // distributed finest level: coarse rows [c_lo, c_hi) are merged here; fine
+  // rows of [row_lo, row_hi) are local (adj/ew from ent_lo), the others come
+  // from the import buffer at imp_pos[x]
+  int64_t c_lo = 0, c_hi = -1;
+  int64_t row_lo = 0, row_hi = INT64_MAX, ent_lo = 0;
+  const int64_t* imp_pos = nullptr;
+  const int32_t* imp_adj = nullptr;
+  const int32_t* imp_ew = nullptr;
 };
 
 // gather row entries of member x of coarse vertex c as sort keys
 __device__ __forceinline__ unsigned long long merged_key(const RowMerge& m, int c, int64_t idx,
                                                          int a, int b, int64_t da) {
   const int x = idx < da ? a : b;
-  const int64_t j = m.offs[x] + (idx < da ? idx : idx - da);
-  const int cv = m.vmap[m.adj[j]];
+  const int64_t k = idx < da ? idx : idx - da;
+  int u, w;
+  if (x >= m.row_lo && x < m.row_hi) {
+    const int64_t j = m.offs[x] - m.ent_lo + k;
+    u = m.adj[j];
+    w = m.ew[j];
+  } else {  // a member row owned by another rank (distributed finest level)
+    const int64_t j = m.imp_pos[x] + k;
+    u = m.imp_adj[j];
+    w = m.imp_ew[j];
+  }
+  const int cv = m.vmap[u];
   if (cv == c) return ~0ull;  // contraction self loop (coarsen.py:133)
-  return ((unsigned long long)(unsigned)cv << 32) | (unsigned)m.ew[j];
+  return ((unsigned long long)(unsigned)cv << 32) | (unsigned)w;
 }
 
 template <int E>
@@ -1782,7 +1802,8 @@ __global__ void __launch_bounds__(256) k_merge_rows(RowMerge m) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t c = w0; c < m.nc; c += ws) {
+  const int64_t c_hi = m.c_hi < 0 ? m.nc : m.c_hi;
+  for (int64_t c = m.c_lo + w0; c < c_hi; c += ws) {
     const int64_t d = m.rowlen[c];
     if (d <= 32) merge_row_warp<1>(m, (int)c, sbuf[wib]);
     else if (d <= 64) merge_row_warp<2>(m, (int)c, sbuf[wib]);
@@ -1994,6 +2015,114 @@ __global__ void k_copy_rows(const int64_t* __restrict__ toff, const int64_t* __r
 static double wall_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
+// Long merged rows (> 256 entries): grouped gather / sort / dedup (see
+// device_contract). setup() sizes the groups once; run() merges them for a
+// RowMerge (counting pass, merging pass, or single pass).
+struct LongRows {
+  Ctx& c;
+  int32_t* big_p;
+  int64_t nb;
+  const int64_t* rowlen_p;
+  int64_t nc;
+  struct Grp { int64_t s0, ns, base, cnt; };
+  std::vector<Grp> groups;
+  DBuf<int64_t> boff, rel, bend;
+  DBuf<unsigned long long> bk, bk2;
+  int cbits = 1;
+  LongRows(Ctx& cc, int32_t* bp, int64_t n_big, const int64_t* rl, int64_t ncoarse)
+      : c(cc), big_p(bp), nb(n_big), rowlen_p(rl), nc(ncoarse) {
+    // Long rows are gathered, sorted and deduplicated in groups of rows of at
+    // most CH entries (one row may exceed it alone): the key buffers stay a
+    // few GB however dense the level (the dense coarse levels of R-MAT 2^27
+    // route ~4 G entries through here), and CUB's 32-bit item counts hold.
+    const int64_t CH = (int64_t)1 << 28;
+    while ((1LL << cbits) < nc) ++cbits;
+    if (nb <= 0) return;
+    DBuf<int64_t> blen(nb + 1, c.stream);
+    boff.alloc(nb + 1, c.stream);
+    dzero(c, blen.get() + nb, 1);
+    launch(c, "big_len", 16.0 * nb, [&] {
+      k_big_len<<<grid_for(c, nb, 256), 256, 0, c.stream>>>(big_p, nb, rowlen_p, blen.get());
+    });
+    {
+      size_t tmp = 0;
+      CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, blen.get(), boff.get(), (int)(nb + 1), c.stream));
+      void* p = c.cub_scratch(tmp);
+      launch(c, "big_scan", 16.0 * nb, [&] {
+        CK(cub::DeviceScan::ExclusiveSum(p, tmp, blen.get(), boff.get(), (int)(nb + 1), c.stream));
+      });
+    }
+    int64_t BT = 0;
+    d2h(c, &BT, boff.get() + nb, 1);
+    c.sync();
+    if (BT <= CH) {
+      groups.push_back({0, nb, 0, BT});
+    } else {
+      std::vector<int64_t> hb(nb + 1);
+      d2h(c, hb.data(), boff.get(), nb + 1);
+      c.sync();
+      int64_t s0 = 0;
+      while (s0 < nb) {
+        int64_t s1 = s0 + 1;
+        while (s1 < nb && hb[s1 + 1] - hb[s0] <= CH) ++s1;
+        groups.push_back({s0, s1 - s0, hb[s0], hb[s1] - hb[s0]});
+        s0 = s1;
+      }
+    }
+    int64_t maxcnt = 0;
+    for (const Grp& q : groups) maxcnt = std::max(maxcnt, q.cnt);
+    bk.alloc(maxcnt, c.stream);
+    bk2.alloc(maxcnt, c.stream);
+    bend.alloc(nb + 1, c.stream);
+    if (groups.size() > 1) rel.alloc(nb + 1, c.stream);
+  }
+  void run(const RowMerge& r) {
+    for (const Grp& q : groups) {
+      JET_REQUIRE(q.cnt < (int64_t)INT_MAX, JET_EUNSUPPORTED, "merged coarse row longer than 2^31 entries");
+      const int64_t* off = boff.get();
+      if (groups.size() > 1) {
+        launch(c, "big_rebase", 16.0 * q.ns, [&] {
+          k_rebase<<<grid_for(c, q.ns + 1, 256), 256, 0, c.stream>>>(boff.get() + q.s0, q.ns + 1, q.base,
+                                                                     rel.get());
+        });
+        off = rel.get();
+      }
+      launch(c, "big_gather", 20.0 * q.cnt, [&] {
+        k_big_gather<<<grid_for(c, q.ns * 256, 256), 256, 0, c.stream>>>(r, big_p + q.s0, q.ns, off,
+                                                                         bk.get(), BIG_BLOCK_MAX);
+      });
+      launch(c, "big_ends", 16.0 * q.ns, [&] {
+        k_big_ends<<<grid_for(c, q.ns, 256), 256, 0, c.stream>>>(big_p + q.s0, q.ns, rowlen_p, off,
+                                                                 bend.get());
+      });
+      size_t tmp = 0;
+      CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, bk.get(), bk2.get(), (int)q.cnt, (int)q.ns, off,
+                                            bend.get(), c.stream));
+      void* p = c.cub_scratch(tmp);
+      launch(c, "big_sort", 32.0 * q.cnt, [&] {
+        CK(cub::DeviceSegmentedSort::SortKeys(p, tmp, bk.get(), bk2.get(), (int)q.cnt, (int)q.ns, off,
+                                              bend.get(), c.stream));
+      });
+      const bool counting = r.tadj == nullptr;  // first pass of a two-pass contraction
+      if (counting) {
+        launch(c, "big_count_block", 12.0 * q.cnt, [&] {
+          k_big_count_block<<<grid_for(c, q.ns * BIG_BT, BIG_BT), BIG_BT, 0, c.stream>>>(r, big_p + q.s0,
+                                                                                        q.ns);
+        });
+      } else {
+        launch(c, "big_sort_block", 20.0 * q.cnt, [&] {
+          k_big_sort_block<<<grid_for(c, q.ns * BIG_BT, BIG_BT), BIG_BT, 0, c.stream>>>(
+              r, big_p + q.s0, q.ns, off, cbits, bk2.get());
+        });
+      }
+      launch(c, "big_dedup", 16.0 * q.cnt, [&] {
+        k_big_dedup<<<grid_for(c, q.ns * 256, 256), 256, 0, c.stream>>>(
+            r, big_p + q.s0, q.ns, off, bk2.get(), counting ? BIG_BLOCK_MAX : 0);
+      });
+    }
+  }
+};
+
 std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* partner,
                                         int32_t* vmap, bool two_pass) {
   static const bool dbg = getenv("JET_COARSEN_TIMES") && getenv("JET_COARSEN_TIMES")[0] == '2';
@@ -2072,103 +2201,8 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
   d2h(c, &nbig, big_cnt.get(), 1);
   c.sync();
   mark("alloc+rows");
-  // Long rows are gathered, sorted and deduplicated in groups of rows of at
-  // most CH entries (one row may exceed it alone): the key buffers stay a
-  // few GB however dense the level (the dense coarse levels of R-MAT 2^27
-  // route ~4 G entries through here), and CUB's 32-bit item counts hold.
-  const int64_t nb = (int64_t)nbig;
-  const int64_t CH = (int64_t)1 << 28;
-  struct Grp { int64_t s0, ns, base, cnt; };
-  std::vector<Grp> groups;
-  DBuf<int64_t> boff, rel, bend;
-  DBuf<unsigned long long> bk, bk2;
-  int cbits = 1;
-  while ((1LL << cbits) < nc) ++cbits;
-  if (nb > 0) {
-    DBuf<int64_t> blen(nb + 1, c.stream);
-    boff.alloc(nb + 1, c.stream);
-    dzero(c, blen.get() + nb, 1);
-    launch(c, "big_len", 16.0 * nb, [&] {
-      k_big_len<<<grid_for(c, nb, 256), 256, 0, c.stream>>>(big_p, nb, rowlen_p, blen.get());
-    });
-    {
-      size_t tmp = 0;
-      CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, blen.get(), boff.get(), (int)(nb + 1), c.stream));
-      void* p = c.cub_scratch(tmp);
-      launch(c, "big_scan", 16.0 * nb, [&] {
-        CK(cub::DeviceScan::ExclusiveSum(p, tmp, blen.get(), boff.get(), (int)(nb + 1), c.stream));
-      });
-    }
-    int64_t BT = 0;
-    d2h(c, &BT, boff.get() + nb, 1);
-    c.sync();
-    if (BT <= CH) {
-      groups.push_back({0, nb, 0, BT});
-    } else {
-      std::vector<int64_t> hb(nb + 1);
-      d2h(c, hb.data(), boff.get(), nb + 1);
-      c.sync();
-      int64_t s0 = 0;
-      while (s0 < nb) {
-        int64_t s1 = s0 + 1;
-        while (s1 < nb && hb[s1 + 1] - hb[s0] <= CH) ++s1;
-        groups.push_back({s0, s1 - s0, hb[s0], hb[s1] - hb[s0]});
-        s0 = s1;
-      }
-    }
-    int64_t maxcnt = 0;
-    for (const Grp& q : groups) maxcnt = std::max(maxcnt, q.cnt);
-    bk.alloc(maxcnt, c.stream);
-    bk2.alloc(maxcnt, c.stream);
-    bend.alloc(nb + 1, c.stream);
-    if (groups.size() > 1) rel.alloc(nb + 1, c.stream);
-  }
-  auto run_big = [&](const RowMerge& r) {
-    for (const Grp& q : groups) {
-      JET_REQUIRE(q.cnt < (int64_t)INT_MAX, JET_EUNSUPPORTED, "merged coarse row longer than 2^31 entries");
-      const int64_t* off = boff.get();
-      if (groups.size() > 1) {
-        launch(c, "big_rebase", 16.0 * q.ns, [&] {
-          k_rebase<<<grid_for(c, q.ns + 1, 256), 256, 0, c.stream>>>(boff.get() + q.s0, q.ns + 1, q.base,
-                                                                     rel.get());
-        });
-        off = rel.get();
-      }
-      launch(c, "big_gather", 20.0 * q.cnt, [&] {
-        k_big_gather<<<grid_for(c, q.ns * 256, 256), 256, 0, c.stream>>>(r, big_p + q.s0, q.ns, off,
-                                                                         bk.get(), BIG_BLOCK_MAX);
-      });
-      launch(c, "big_ends", 16.0 * q.ns, [&] {
-        k_big_ends<<<grid_for(c, q.ns, 256), 256, 0, c.stream>>>(big_p + q.s0, q.ns, rowlen_p, off,
-                                                                 bend.get());
-      });
-      size_t tmp = 0;
-      CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, bk.get(), bk2.get(), (int)q.cnt, (int)q.ns, off,
-                                            bend.get(), c.stream));
-      void* p = c.cub_scratch(tmp);
-      launch(c, "big_sort", 32.0 * q.cnt, [&] {
-        CK(cub::DeviceSegmentedSort::SortKeys(p, tmp, bk.get(), bk2.get(), (int)q.cnt, (int)q.ns, off,
-                                              bend.get(), c.stream));
-      });
-      const bool counting = r.tadj == nullptr;  // first pass of a two-pass contraction
-      if (counting) {
-        launch(c, "big_count_block", 12.0 * q.cnt, [&] {
-          k_big_count_block<<<grid_for(c, q.ns * BIG_BT, BIG_BT), BIG_BT, 0, c.stream>>>(r, big_p + q.s0,
-                                                                                        q.ns);
-        });
-      } else {
-        launch(c, "big_sort_block", 20.0 * q.cnt, [&] {
-          k_big_sort_block<<<grid_for(c, q.ns * BIG_BT, BIG_BT), BIG_BT, 0, c.stream>>>(
-              r, big_p + q.s0, q.ns, off, cbits, bk2.get());
-        });
-      }
-      launch(c, "big_dedup", 16.0 * q.cnt, [&] {
-        k_big_dedup<<<grid_for(c, q.ns * 256, 256), 256, 0, c.stream>>>(
-            r, big_p + q.s0, q.ns, off, bk2.get(), counting ? BIG_BLOCK_MAX : 0);
-      });
-    }
-  };
-  run_big(rm);
+  LongRows longrows(c, big_p, (int64_t)nbig, rowlen_p, nc);
+  longrows.run(rm);
   // final offsets
   cg_->offs.alloc(nc + 1, c.stream);
   {
@@ -2199,7 +2233,7 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
     launch(c, "contract_rows", 12.0 * g.nnz + 8.0 * cnnz + 16.0 * nc, [&] {
       k_merge_rows<<<grid_for(c, nc * 32, 256), 256, 0, c.stream>>>(r2);
     });
-    run_big(r2);
+    longrows.run(r2);
   } else {
     launch(c, "copy_rows", 16.0 * cnnz + 16.0 * nc, [&] {
       k_copy_rows<<<grid_for(c, nc * 32, 256), 256, 0, c.stream>>>(toff_p, cg_->offs.get(), tadj_p,
@@ -2209,6 +2243,466 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
   mark("copy");
   finalize_graph(c, *cg_);
   mark("finalize");
+  return cg_;
+}
+
+// ===========================================================================
+// 1D-distributed finest level: every rank holds the rows of
+// its block [lo, hi) (DGraph::partial) plus the complete offsets and vertex
+// weights. The throughput-mode matching and the contraction run on the owned
+// rows with exchanges over the communicator, and produce exactly the
+// replicated run's matching and coarse level -- which every rank then holds
+// whole (the coarser levels are small enough to replicate, as north_star's
+// "coarse levels gathered" allows).
+// ===========================================================================
+namespace {
+
+__global__ void k_pack_props(const int32_t* __restrict__ elist, const unsigned long long* __restrict__ ecnt,
+                             const int32_t* __restrict__ prop, int2* out) {
+  const int64_t cnt = (int64_t)*ecnt;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = elist[i];
+    out[i] = make_int2(v, prop[v]);
+  }
+}
+
+__global__ void k_unpack_props(const int2* __restrict__ in, int64_t cnt, int32_t* prop) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x)
+    prop[in[i].x] = in[i].y;
+}
+
+// mutual proposals among this rank's proposers (v < u: the pair's owner)
+__global__ void k_accept_pairs(const int32_t* __restrict__ elist, const unsigned long long* __restrict__ ecnt,
+                               const int32_t* __restrict__ prop, int2* pairs,
+                               unsigned long long* npairs) {
+  const int64_t cnt = (int64_t)*ecnt;
+  const int64_t lim = (cnt + 31) / 32 * 32;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < lim;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int v = 0, u = 0;
+    bool take = false;
+    if (i < cnt) {
+      v = elist[i];
+      u = prop[v];
+      take = v < u && prop[u] == v;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    unsigned long long base = 0;
+    if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(npairs, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (take) pairs[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = make_int2(v, u);
+  }
+}
+
+__global__ void k_unpack_pairs(const int2* __restrict__ in, int64_t cnt, int32_t* partner) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    partner[in[i].x] = in[i].y;
+    partner[in[i].y] = in[i].x;
+  }
+}
+
+// [first position >= lo, first position >= hi) of an ascending list
+__global__ void k_list_range(const int32_t* __restrict__ list, int64_t cnt, int64_t lo, int64_t hi,
+                             int64_t* out) {
+  if (threadIdx.x > 1) return;
+  const int64_t key = threadIdx.x == 0 ? lo : hi;
+  int64_t a = 0, b = cnt;
+  while (a < b) {
+    const int64_t m = (a + b) / 2;
+    if (list[m] < key) a = m + 1;
+    else b = m;
+  }
+  out[threadIdx.x] = a;
+}
+
+// this rank's free vertices
+__global__ void k_owned_free(const int32_t* __restrict__ partner, int64_t lo, int64_t hi,
+                             int32_t* out, unsigned long long* cnt) {
+  const int64_t span = (hi - lo + 31) / 32 * 32;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < span;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = lo + i;
+    const bool f = v < hi && partner[v] < 0;
+    const unsigned m = __ballot_sync(0xffffffffu, f);
+    unsigned long long base = 0;
+    if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(cnt, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (f) out[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = (int32_t)v;
+  }
+}
+
+// owned rows b whose representative partner[b] < b lives on a lower rank
+__global__ void k_export_rows(const int32_t* __restrict__ partner, const int64_t* __restrict__ offs,
+                              int64_t lo, int64_t hi, int32_t* ids, int64_t* lens,
+                              unsigned long long* cnt) {
+  const int64_t span = (hi - lo + 31) / 32 * 32;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < span;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = lo + i;
+    bool f = false;
+    if (b < hi) {
+      const int a = partner[b];
+      f = a < b && a < lo;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, f);
+    unsigned long long base = 0;
+    if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(cnt, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (f) {
+      const unsigned long long q = base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u));
+      ids[q] = (int32_t)b;
+      lens[q] = offs[b + 1] - offs[b];
+    }
+  }
+}
+
+__global__ void k_gather_rows(const int32_t* __restrict__ ids, const int64_t* __restrict__ eoff,
+                              int64_t nr, GView g, int2* out) {
+  for (int64_t r = blockIdx.x; r < nr; r += gridDim.x) {
+    const int b = ids[r];
+    const int64_t s = g.offs[b], d = g.offs[b + 1] - s, o = eoff[r];
+    for (int64_t j = threadIdx.x; j < d; j += blockDim.x) out[o + j] = make_int2(g.adj[s + j], g.ew[s + j]);
+  }
+}
+
+// imported rows: position of each row's entries, split into adj / ew
+__global__ void k_import_rows(const int32_t* __restrict__ ids, const int64_t* __restrict__ eoff,
+                              int64_t nr, const int2* __restrict__ ent, int64_t ne, int64_t* imp_pos,
+                              int32_t* imp_adj, int32_t* imp_ew) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nr; r += stride)
+    imp_pos[ids[r]] = eoff[r];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += stride) {
+    imp_adj[e] = ent[e].x;
+    imp_ew[e] = ent[e].y;
+  }
+}
+
+// gather `bytes` of every rank, rank-major, into `out` (resized); total bytes
+int64_t gather_all(Ctx& c, const void* d, int64_t bytes, DBuf<uint8_t>& out) {
+  std::vector<int64_t> counts;
+  c.comm->allgatherv(c, d, bytes, out, counts);
+  int64_t t = 0;
+  for (int64_t x : counts) t += x;
+  return t;
+}
+
+}  // namespace
+
+// The replicated device_match_fast, round for round, over the owned rows.
+static void device_match_fast_dist(Ctx& c, const DGraph& g, int32_t* partner) {
+  JET_REQUIRE(c.comm, JET_EINVAL, "a distributed level needs a communicator");
+  const int64_t n = g.n, lo = g.row_lo, hi = g.row_hi;
+  launch(c, "fill", 4.0 * n, [&] {
+    k_fill<<<grid_for(c, n, 256), 256, 0, c.stream>>>(partner, n, -1);
+  });
+  const GView gv = view(g);
+  int32_t* prop_p = c.scratch<int32_t>(10, n);
+  int32_t* elist_p = c.scratch<int32_t>(11, std::max<int64_t>(1, hi - lo));
+  DBuf<unsigned long long> cnt(4, c.stream);
+  DBuf<int2> send(std::max<int64_t>(1, hi - lo), c.stream);
+  DBuf<uint8_t> recv;
+  // this rank's hub rows (the hub tier list restricted to the block)
+  const int64_t nh_all = g.bin_cnt[BIN_BLOCK];
+  const int32_t* hubs = nullptr;
+  int64_t nh = 0;
+  if (nh_all) {
+    DBuf<int64_t> r(2, c.stream);
+    const int32_t* hl = tier_list(g, BIN_BLOCK);
+    JET_REQUIRE(hl, JET_EINTERNAL, "identity hub tier on a distributed level");
+    k_list_range<<<1, 32, 0, c.stream>>>(hl, nh_all, lo, hi, r.get());
+    CK(cudaGetLastError());
+    int64_t hr[2];
+    d2h(c, hr, r.get(), 2);
+    c.sync();
+    hubs = hl + hr[0];
+    nh = hr[1] - hr[0];
+  }
+  constexpr int MAXR = 48, RG = 4;
+  int low_rounds = 0;
+  bool quit = false;
+  for (int round = 0; round < MAXR; ++round) {
+    dzero(c, cnt.get(), 4);
+    const unsigned salt = 0x5bd1e995u * (unsigned)(round + 1);
+    launch(c, "propose", (g.unit_ew ? 8.0 : 12.0) * (double)g.local_nnz(), [&] {
+      if (g.unit_ew)
+        k_propose_fast<true><<<grid_for(c, hi - lo, 256), 256, 0, c.stream>>>(
+            gv, hi, partner, prop_p, elist_p, cnt.get(), salt, nullptr, lo);
+      else
+        k_propose_fast<false><<<grid_for(c, hi - lo, 256), 256, 0, c.stream>>>(
+            gv, hi, partner, prop_p, elist_p, cnt.get(), salt, nullptr, lo);
+    });
+    if (nh) {
+      const unsigned hg = (unsigned)std::min<int64_t>(nh, 4LL * c.num_sms);
+      launch(c, "propose_hub", 0.0, [&] {
+        if (g.unit_ew)
+          k_propose_fast_hub<true><<<hg, 256, 0, c.stream>>>(gv, hubs, nh, partner, prop_p, elist_p,
+                                                             cnt.get(), salt, nullptr);
+        else
+          k_propose_fast_hub<false><<<hg, 256, 0, c.stream>>>(gv, hubs, nh, partner, prop_p, elist_p,
+                                                              cnt.get(), salt, nullptr);
+      });
+    }
+    // halo 1: every rank's proposals
+    unsigned long long np_local = 0;
+    d2h(c, &np_local, cnt.get(), 1);
+    c.sync();
+    launch(c, "shard_pack", 8.0 * (double)np_local, [&] {
+      k_pack_props<<<grid_for(c, (int64_t)np_local, 256), 256, 0, c.stream>>>(elist_p, cnt.get(), prop_p,
+                                                                             send.get());
+    });
+    const int64_t np = gather_all(c, send.get(), (int64_t)np_local * 8, recv) / 8;
+    launch(c, "shard_unpack", 8.0 * (double)np, [&] {
+      k_unpack_props<<<grid_for(c, np, 256), 256, 0, c.stream>>>((const int2*)recv.get(), np, prop_p);
+    });
+    // accept the mutual ones this rank owns; halo 2: every rank's pairs
+    launch(c, "accept", 12.0 * (double)np_local, [&] {
+      k_accept_pairs<<<grid_for(c, (int64_t)np_local, 256), 256, 0, c.stream>>>(
+          elist_p, cnt.get(), prop_p, send.get(), cnt.get() + 1);
+    });
+    unsigned long long pr_local = 0;
+    d2h(c, &pr_local, cnt.get() + 1, 1);
+    c.sync();
+    const int64_t pr = gather_all(c, send.get(), (int64_t)pr_local * 8, recv) / 8;
+    launch(c, "shard_unpack", 8.0 * (double)pr, [&] {
+      k_unpack_pairs<<<grid_for(c, pr, 256), 256, 0, c.stream>>>((const int2*)recv.get(), pr, partner);
+    });
+    // the replicated path's stopping rule (device_match_fast), same rounds
+    if (np == 0 || pr == 0) break;
+    low_rounds = (unsigned long long)pr * 200 < (unsigned long long)np ? low_rounds + 1 : 0;
+    quit |= low_rounds >= 2;
+    if (quit && round % RG == RG - 1) break;
+  }
+  // leaf pairing of every rank's leftovers, sorted and paired on every rank
+  int32_t* left_p = c.scratch<int32_t>(13, std::max<int64_t>(1, hi - lo));
+  dzero(c, cnt.get(), 1);
+  launch(c, "th_leftovers", 8.0 * (hi - lo), [&] {
+    k_owned_free<<<grid_for(c, hi - lo, 256), 256, 0, c.stream>>>(partner, lo, hi, left_p, cnt.get());
+  });
+  unsigned long long nl_local = 0;
+  d2h(c, &nl_local, cnt.get(), 1);
+  c.sync();
+  int vb = 1;
+  while ((1LL << vb) <= n) ++vb;
+  DBuf<unsigned long long> kl(std::max<unsigned long long>(1, nl_local), c.stream);
+  if (nl_local)
+    launch(c, "leaf_keys", 16.0 * (double)nl_local, [&] {
+      k_leaf_keys<<<grid_for(c, (int64_t)nl_local * 32, 256), 256, 0, c.stream>>>(gv, left_p, (int64_t)nl_local,
+                                                                                 vb, kl.get());
+    });
+  const int64_t nl = gather_all(c, kl.get(), (int64_t)nl_local * 8, recv) / 8;
+  if (nl >= 2) {
+    DBuf<unsigned long long> k1(nl, c.stream);
+    const unsigned long long* k0 = (const unsigned long long*)recv.get();
+    size_t tmp = 0;
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k0, k1.get(), (int)nl, 0, 2 * vb, c.stream));
+    void* p = c.cub_scratch(tmp);
+    launch(c, "leaf_sort", 32.0 * nl, [&] {
+      CK(cub::DeviceRadixSort::SortKeys(p, tmp, k0, k1.get(), (int)nl, 0, 2 * vb, c.stream));
+    });
+    launch(c, "leaf_pair", 16.0 * nl, [&] {
+      k_leaf_pair<<<grid_for(c, nl, 256), 256, 0, c.stream>>>(k1.get(), nl, vb, n, partner);
+    });
+  }
+  launch(c, "singletons", 8.0 * n, [&] {
+    k_singletons<<<grid_for(c, n, 256), 256, 0, c.stream>>>(partner, n);
+  });
+}
+
+// The contraction of a distributed level: every rank merges the coarse rows
+// whose representative it owns (importing the partner rows that live on
+// higher ranks), then the coarse rows of all ranks are gathered -- coarse ids
+// are ascending in the representative, so the ranks' ranges are contiguous
+// and in rank order. The result equals device_contract's, on every rank.
+static std::unique_ptr<DGraph> device_contract_dist(Ctx& c, const DGraph& g, const int32_t* partner,
+                                                    int32_t* vmap) {
+  JET_REQUIRE(c.comm, JET_EINVAL, "a distributed level needs a communicator");
+  const int64_t n = g.n, lo = g.row_lo, hi = g.row_hi;
+  int32_t* flag_p = c.scratch<int32_t>(0, n);
+  int32_t* cid_p = c.scratch<int32_t>(1, n);
+  launch(c, "is_rep", 8.0 * n, [&] {
+    k_is_rep<<<grid_for(c, n, 256), 256, 0, c.stream>>>(partner, n, flag_p);
+  });
+  {
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag_p, cid_p, (int)n, c.stream));
+    void* p = c.cub_scratch(tmp);
+    launch(c, "rep_scan", 8.0 * n, [&] {
+      CK(cub::DeviceScan::ExclusiveSum(p, tmp, flag_p, cid_p, (int)n, c.stream));
+    });
+  }
+  int32_t last[4] = {0, 0, 0, 0};
+  d2h(c, &last[0], cid_p + n - 1, 1);
+  d2h(c, &last[1], flag_p + n - 1, 1);
+  if (lo < n) d2h(c, &last[2], cid_p + lo, 1);
+  if (hi < n) d2h(c, &last[3], cid_p + hi, 1);
+  c.sync();
+  const int64_t nc = (int64_t)last[0] + last[1];
+  const int64_t c_lo = lo < n ? last[2] : nc, c_hi = hi < n ? last[3] : nc;
+  auto cg_ = std::make_unique<DGraph>();
+  cg_->n = nc;
+  cg_->vw.alloc(nc, c.stream);
+  int32_t* mem_a_p = c.scratch<int32_t>(2, nc);
+  int32_t* mem_b_p = c.scratch<int32_t>(3, nc);
+  int64_t* rowlen_p = c.scratch<int64_t>(4, nc + 1);
+  int64_t* cdeg_p = c.scratch<int64_t>(6, nc + 1);
+  DBuf<unsigned> ovf(1, c.stream);
+  dzero(c, ovf.get(), 1);
+  CoarseMap cm{partner, cid_p, g.offs.get(), g.vw.get(), vmap, cg_->vw.get(),
+               mem_a_p, mem_b_p, rowlen_p, ovf.get()};
+  launch(c, "coarse_map", 24.0 * n, [&] {
+    k_coarse_map<<<grid_for(c, n, 256), 256, 0, c.stream>>>(cm, n);
+  });
+  // import the partner rows of this rank's representatives
+  DBuf<int32_t> xids(std::max<int64_t>(1, hi - lo), c.stream);
+  DBuf<int64_t> xlen(std::max<int64_t>(1, hi - lo) + 1, c.stream), xoff(std::max<int64_t>(1, hi - lo) + 1, c.stream);
+  DBuf<unsigned long long> xc(1, c.stream);
+  dzero(c, xc.get(), 1);
+  launch(c, "export_rows", 12.0 * (hi - lo), [&] {
+    k_export_rows<<<grid_for(c, hi - lo, 256), 256, 0, c.stream>>>(partner, g.offs.get(), lo, hi, xids.get(),
+                                                                   xlen.get(), xc.get());
+  });
+  unsigned long long nx = 0;
+  d2h(c, &nx, xc.get(), 1);
+  c.sync();
+  DBuf<uint8_t> r_ids, r_lens, r_ent;
+  const int64_t nimp = gather_all(c, xids.get(), (int64_t)nx * 4, r_ids) / 4;
+  gather_all(c, xlen.get(), (int64_t)nx * 8, r_lens);
+  int64_t xe = 0;
+  {
+    dzero(c, xlen.get() + nx, 1);
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, xlen.get(), xoff.get(), (int)(nx + 1), c.stream));
+    void* p = c.cub_scratch(tmp);
+    launch(c, "export_scan", 16.0 * (double)nx, [&] {
+      CK(cub::DeviceScan::ExclusiveSum(p, tmp, xlen.get(), xoff.get(), (int)(nx + 1), c.stream));
+    });
+    d2h(c, &xe, xoff.get() + nx, 1);
+    c.sync();
+  }
+  DBuf<int2> xent(std::max<int64_t>(1, xe), c.stream);
+  const GView gv = view(g);
+  if (nx)
+    launch(c, "export_gather", 16.0 * (double)xe, [&] {
+      k_gather_rows<<<grid_for(c, (int64_t)nx * 128, 128), 128, 0, c.stream>>>(xids.get(), xoff.get(),
+                                                                             (int64_t)nx, gv, xent.get());
+    });
+  const int64_t ne = gather_all(c, xent.get(), xe * 8, r_ent) / 8;
+  DBuf<int64_t> ioff(nimp + 1, c.stream);
+  DBuf<int64_t> imp_pos(n, c.stream);
+  DBuf<int32_t> imp_adj(std::max<int64_t>(1, ne), c.stream), imp_ew(std::max<int64_t>(1, ne), c.stream);
+  if (nimp) {
+    DBuf<int64_t> l2(nimp + 1, c.stream);
+    CK(cudaMemcpyAsync(l2.get(), r_lens.get(), (size_t)nimp * 8, cudaMemcpyDeviceToDevice, c.stream));
+    dzero(c, l2.get() + nimp, 1);
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, l2.get(), ioff.get(), (int)(nimp + 1), c.stream));
+    void* p = c.cub_scratch(tmp);
+    launch(c, "import_scan", 16.0 * nimp, [&] {
+      CK(cub::DeviceScan::ExclusiveSum(p, tmp, l2.get(), ioff.get(), (int)(nimp + 1), c.stream));
+    });
+    launch(c, "import_rows", 16.0 * ne, [&] {
+      k_import_rows<<<grid_for(c, std::max(nimp, ne), 256), 256, 0, c.stream>>>(
+          (const int32_t*)r_ids.get(), ioff.get(), nimp, (const int2*)r_ent.get(), ne, imp_pos.get(),
+          imp_adj.get(), imp_ew.get());
+    });
+  }
+  // merge the owned coarse rows [c_lo, c_hi) into a staging area sized by them
+  const int64_t ncl = c_hi - c_lo;
+  DBuf<int64_t> toff(ncl + 1, c.stream);
+  {
+    dzero(c, rowlen_p + nc, 1);
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, rowlen_p + c_lo, toff.get(), (int)(ncl + 1), c.stream));
+    void* p = c.cub_scratch(tmp);
+    launch(c, "rowlen_scan", 16.0 * ncl, [&] {
+      CK(cub::DeviceScan::ExclusiveSum(p, tmp, rowlen_p + c_lo, toff.get(), (int)(ncl + 1), c.stream));
+    });
+  }
+  int64_t T = 0;
+  d2h(c, &T, toff.get() + ncl, 1);
+  c.sync();
+  DBuf<int32_t> tadj(std::max<int64_t>(1, T), c.stream), tew(std::max<int64_t>(1, T), c.stream);
+  int32_t* big_p = c.scratch<int32_t>(9, std::max<int64_t>(1, ncl));
+  DBuf<unsigned long long> big_cnt(1, c.stream);
+  dzero(c, big_cnt.get(), 1);
+  dzero(c, cdeg_p, nc + 1);
+  RowMerge rm{g.offs.get(), g.adj.get(), g.ew.get(), vmap, mem_a_p, mem_b_p, toff.get() - c_lo,
+              rowlen_p, tadj.get(), tew.get(), cdeg_p, big_p, big_cnt.get(), ovf.get(), nc, 1};
+  rm.c_lo = c_lo;
+  rm.c_hi = c_hi;
+  rm.row_lo = lo;
+  rm.row_hi = hi;
+  rm.ent_lo = g.ent_lo;
+  rm.imp_pos = imp_pos.get();
+  rm.imp_adj = imp_adj.get();
+  rm.imp_ew = imp_ew.get();
+  if (ncl > 0)
+    launch(c, "contract_rows", 12.0 * T + 8.0 * T, [&] {
+      k_merge_rows<<<grid_for(c, ncl * 32, 256), 256, 0, c.stream>>>(rm);
+    });
+  unsigned long long nbig = 0;
+  d2h(c, &nbig, big_cnt.get(), 1);
+  c.sync();
+  if (nbig) {
+    LongRows lr(c, big_p, (int64_t)nbig, rowlen_p, nc);
+    lr.run(rm);
+  }
+  // this rank's coarse rows, compacted, then every rank's
+  DBuf<int64_t> loff(ncl + 1, c.stream);
+  {
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cdeg_p + c_lo, loff.get(), (int)(ncl + 1), c.stream));
+    void* p = c.cub_scratch(tmp);
+    launch(c, "cdeg_scan", 16.0 * ncl, [&] {
+      CK(cub::DeviceScan::ExclusiveSum(p, tmp, cdeg_p + c_lo, loff.get(), (int)(ncl + 1), c.stream));
+    });
+  }
+  int64_t lnnz = 0;
+  d2h(c, &lnnz, loff.get() + ncl, 1);
+  c.sync();
+  DBuf<int32_t> ladj, lew;
+  ladj.alloc(std::max<int64_t>(1, lnnz), c.stream);
+  lew.alloc(std::max<int64_t>(1, lnnz), c.stream);
+  if (ncl > 0)
+    launch(c, "copy_rows", 16.0 * lnnz, [&] {
+      k_copy_rows<<<grid_for(c, ncl * 32, 256), 256, 0, c.stream>>>(toff.get(), loff.get(), tadj.get(),
+                                                                   tew.get(), ladj.get(), lew.get(), ncl);
+    });
+  DBuf<uint8_t> gdeg, gadj, gew;
+  const int64_t nrow = gather_all(c, cdeg_p + c_lo, ncl * 8, gdeg) / 8;
+  const int64_t cnnz = gather_all(c, ladj.get(), lnnz * 4, gadj) / 4;
+  gather_all(c, lew.get(), lnnz * 4, gew);
+  JET_REQUIRE(nrow == nc, JET_EINTERNAL, "distributed contraction lost coarse rows");
+  unsigned hovf = 0;
+  d2h(c, &hovf, ovf.get(), 1);
+  c.sync();
+  hovf = (unsigned)comm_max(c, (int64_t)hovf);
+  JET_REQUIRE(!(hovf & 1u), JET_EUNSUPPORTED, "coarse vertex weight exceeds int32");
+  JET_REQUIRE(!(hovf & 2u), JET_EUNSUPPORTED, "coarse edge weight exceeds int32");
+  cg_->offs.alloc(nc + 1, c.stream);
+  {
+    DBuf<int64_t> d2(nc + 1, c.stream);
+    CK(cudaMemcpyAsync(d2.get(), gdeg.get(), (size_t)nc * 8, cudaMemcpyDeviceToDevice, c.stream));
+    dzero(c, d2.get() + nc, 1);
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, d2.get(), cg_->offs.get(), (int)(nc + 1), c.stream));
+    void* p = c.cub_scratch(tmp);
+    launch(c, "coarse_offs", 16.0 * nc, [&] {
+      CK(cub::DeviceScan::ExclusiveSum(p, tmp, d2.get(), cg_->offs.get(), (int)(nc + 1), c.stream));
+    });
+  }
+  cg_->nnz = cnnz;
+  cg_->adj.alloc(cnnz > 0 ? cnnz : 1, c.stream);
+  cg_->ew.alloc(cnnz > 0 ? cnnz : 1, c.stream);
+  if (cnnz) {
+    CK(cudaMemcpyAsync(cg_->adj.get(), gadj.get(), (size_t)cnnz * 4, cudaMemcpyDeviceToDevice, c.stream));
+    CK(cudaMemcpyAsync(cg_->ew.get(), gew.get(), (size_t)cnnz * 4, cudaMemcpyDeviceToDevice, c.stream));
+  }
+  finalize_graph(c, *cg_);
   return cg_;
 }
 
@@ -2308,7 +2802,9 @@ void device_build_hierarchy(Ctx& c, const DGraph& g0, int64_t target, Hierarchy&
       c.sync();
       t0 = wall_s();
     }
-    if (fast)
+    if (fine->partial())  // distributed finest level (throughput mode only)
+      device_match_fast_dist(c, *fine, partner.get());
+    else if (fast)
       device_match_fast(c, *fine, partner.get());
     else
       device_match(c, *fine, partner.get());
@@ -2318,7 +2814,8 @@ void device_build_hierarchy(Ctx& c, const DGraph& g0, int64_t target, Hierarchy&
     }
     DBuf<int32_t> vmap(fine->n, c.stream);
     const int lv = h.size();  // the level being built
-    auto coarse = contract_level(c, h, lv, *fine, partner.get(), vmap.get());
+    auto coarse = fine->partial() ? device_contract_dist(c, *fine, partner.get(), vmap.get())
+                                  : contract_level(c, h, lv, *fine, partner.get(), vmap.get());
     if (dbg) {
       c.sync();
       fprintf(stderr, "COARSEN n=%lld match=%.2fms contract=%.2fms resident=%.2fGB\n", (long long)fine->n,

@@ -27,6 +27,23 @@ void Comm::allreduce_sum(Ctx& c, unsigned long long* d, int64_t count) {
   CK(cudaGetLastError());
 }
 
+static int64_t comm_reduce(Ctx& c, int64_t v, bool mx) {
+  if (!c.comm || c.comm->size == 1) return v;
+  DBuf<int64_t> d(1, c.stream);
+  h2d(c, d.get(), &v, 1);
+  DBuf<uint8_t> recv;
+  std::vector<int64_t> counts;
+  c.comm->allgatherv(c, d.get(), (int64_t)sizeof(int64_t), recv, counts);
+  std::vector<int64_t> all(c.comm->size);
+  d2h(c, all.data(), reinterpret_cast<const int64_t*>(recv.get()), c.comm->size);
+  c.sync();
+  int64_t r = mx ? all[0] : 0;
+  for (int64_t x : all) r = mx ? std::max(r, x) : r + x;
+  return r;
+}
+int64_t comm_max(Ctx& c, int64_t v) { return comm_reduce(c, v, true); }
+int64_t comm_sum(Ctx& c, int64_t v) { return comm_reduce(c, v, false); }
+
 void LocalGroup::barrier() {
   std::unique_lock<std::mutex> lk(m);
   const int64_t gen = generation;

@@ -150,6 +150,13 @@ struct DGraph {
   int64_t bin_nnz[NBINS] = {};
   bool identity = false;
   int identity_bin = -1;
+  // 1D-distributed level: this rank stores only the rows of
+  // [row_lo, row_hi) -- adj/ew hold the entries [offs[row_lo], offs[row_hi]),
+  // starting at ent_lo -- while offs and vw are complete (O(n) per rank).
+  // row_hi < 0: every row is local. nnz is always the global entry count.
+  int64_t row_lo = 0, row_hi = -1, ent_lo = 0;
+  bool partial() const { return row_hi >= 0; }
+  int64_t local_nnz() const { return partial() ? (int64_t)adj.n : nnz; }
 };
 
 struct Ctx;
@@ -258,6 +265,11 @@ struct Ctx {
     cub_tmp.release();
   }
 };
+
+// Max / sum of a host scalar over the ranks of c.comm (the value itself
+// without a communicator); a device round trip through the transport.
+int64_t comm_max(Ctx& c, int64_t v);
+int64_t comm_sum(Ctx& c, int64_t v);
 
 void ctx_retain(Ctx* c);
 void ctx_release(Ctx* c);  // tears the context down at the last reference

@@ -33,8 +33,11 @@ void refine_level(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, int64_t
                   DBuf<int32_t>& keep) {
   // sharded levels run the host-driven passes: the exchange
   // steps are collectives between ranks, outside any kernel
-  const bool sharded = c.comm && (c.comm->size > 1 || c.shard_single) && g.n >= c.shard_min_n &&
-                       cfg.afterburner != 0;
+  // a distributed level (DGraph::partial) holds only its own rows: sharded
+  const bool sharded = g.partial() || (c.comm && (c.comm->size > 1 || c.shard_single) &&
+                                       g.n >= c.shard_min_n && cfg.afterburner != 0);
+  JET_REQUIRE(!g.partial() || (c.comm && cfg.afterburner != 0), JET_EUNSUPPORTED,
+              "a distributed level needs a communicator and the afterburner");
   if (!sharded && !c.host_levels &&
       refine_level_device(c, w, g, parts, cut, cfg, finest, level, st, keep))
     return;
@@ -199,6 +202,9 @@ void check_partition_args(const DGraph& g, const jet_config& cfg) {
 void run_partition(Ctx& c, const DGraph& g0, const jet_config& cfg, int32_t* parts_out,
                    int64_t* pw_out, jet_run_stats* st) {
   check_partition_args(g0, cfg);
+  JET_REQUIRE(!g0.partial() || !cfg.deterministic, JET_EUNSUPPORTED,
+              "a distributed graph partitions in throughput mode (the deterministic matching "
+              "follows the reference's sequential scan)");
   const int k = cfg.k;
   const double t0 = now_s();
   const long long nsync0 = c.nsync;

@@ -198,7 +198,7 @@ void finalize_graph(Ctx& c, DGraph& g) {
   if (g.n > 0) {
     launch(c, "level_stats", 8.0 * g.n + 4.0 * g.n + 4.0 * g.nnz, [&] {
       k_level_stats<<<grid_for(c, g.n > g.nnz ? g.n : g.nnz, 256), 256, 0, c.stream>>>(
-          g.offs.get(), g.vw.get(), g.ew.get(), g.n, g.nnz, g.tm, st.get());
+          g.offs.get(), g.vw.get(), g.ew.get(), g.n, g.local_nnz(), g.tm, st.get());
     });
   }
   LevelStats h;
@@ -209,7 +209,8 @@ void finalize_graph(Ctx& c, DGraph& g) {
   g.min_vw = g.n > 0 ? (int64_t)h.min_vw : 1;
   g.max_deg = (int64_t)h.max_deg;
   g.max_ew = (int64_t)h.max_ew;
-  g.unit_ew = g.nnz == 0 || h.max_ew <= 1;
+  if (g.partial()) g.max_ew = comm_max(c, g.max_ew);  // the other ranks' entries
+  g.unit_ew = g.nnz == 0 || g.max_ew <= 1;
   g.max_wdeg = g.max_deg * (g.max_ew > 0 ? g.max_ew : 1);  // upper bound
   JET_REQUIRE(g.max_wdeg < (1LL << (63 - KBITS)), JET_EUNSUPPORTED,
               "weighted degree too large for 64-bit gain keys");
@@ -266,7 +267,8 @@ static void staged_upload(Ctx& c, const void* src, size_t bytes, F&& consume) {
 
 std::unique_ptr<DGraph> upload_graph(Ctx& c, int64_t n, const int64_t* offs,
                                      const void* adj, int adt, const void* ew,
-                                     int edt, const void* vw, int vdt) {
+                                     int edt, const void* vw, int vdt,
+                                     int64_t row_lo, int64_t row_hi) {
   JET_REQUIRE(n >= 1, JET_EINVAL, "graph must have at least one vertex");
   JET_REQUIRE(n < (1LL << 31) - 1, JET_EUNSUPPORTED, "n must be < 2^31");
   JET_REQUIRE(offs, JET_EINVAL, "row_offsets is NULL");
@@ -277,9 +279,21 @@ std::unique_ptr<DGraph> upload_graph(Ctx& c, int64_t n, const int64_t* offs,
   auto g = std::make_unique<DGraph>();
   g->n = n;
   g->nnz = nnz;
+  int64_t lnnz = nnz;  // entries stored on this rank
+  if (row_hi >= 0) {
+    JET_REQUIRE(0 <= row_lo && row_lo <= row_hi && row_hi <= n, JET_EINVAL, "bad row block");
+    g->row_lo = row_lo;
+    g->row_hi = row_hi;
+    g->ent_lo = offs[row_lo];
+    lnnz = offs[row_hi] - offs[row_lo];
+  }
   g->offs.alloc(n + 1, c.stream);
-  g->adj.alloc(nnz > 0 ? nnz : 1, c.stream);
-  g->ew.alloc(nnz > 0 ? nnz : 1, c.stream);
+  g->adj.alloc(lnnz > 0 ? lnnz : 1, c.stream);
+  g->ew.alloc(lnnz > 0 ? lnnz : 1, c.stream);
+  if (row_hi >= 0) {  // local_nnz() reads the buffer lengths
+    g->adj.n = (size_t)lnnz;
+    g->ew.n = (size_t)lnnz;
+  }
   g->vw.alloc(n, c.stream);
   DBuf<unsigned> bad(1, c.stream);
   dzero(c, bad.get(), 1);
@@ -342,8 +356,8 @@ std::unique_ptr<DGraph> upload_graph(Ctx& c, int64_t n, const int64_t* offs,
     });
   };
   const long long I32MAX = 2147483647LL;
-  put(adj, adt, g->adj.get(), nnz, 0, n - 1, BAD_ADJ);
-  put(ew, edt, g->ew.get(), nnz, 1, I32MAX, BAD_EW);
+  put(adj, adt, g->adj.get(), lnnz, 0, n - 1, BAD_ADJ);
+  put(ew, edt, g->ew.get(), lnnz, 1, I32MAX, BAD_EW);
   put(vw, vdt, g->vw.get(), n, 1, I32MAX, BAD_VW);
   unsigned hbad = 0;
   d2h(c, &hbad, bad.get(), 1);

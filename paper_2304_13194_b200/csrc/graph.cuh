@@ -13,8 +13,10 @@ struct GView {
   const int32_t* __restrict__ vw;
   int64_t n;
 };
+// A partial (distributed) level's adj/ew are shifted so global entry indices
+// offs[v] .. offs[v+1] address the local rows; only local rows may be read.
 inline GView view(const DGraph& g) {
-  return GView{g.offs.get(), g.adj.get(), g.ew.get(), g.vw.get(), g.n};
+  return GView{g.offs.get(), g.adj.get() - g.ent_lo, g.ew.get() - g.ent_lo, g.vw.get(), g.n};
 }
 
 // Launch KERNEL<G, UNIT> for a runtime tier width G in {4,8,16,32}.
@@ -42,9 +44,12 @@ inline const int32_t* tier_list(const DGraph& g, int t) {
 }
 
 void finalize_graph(Ctx& c, DGraph& g);
+// row_hi >= 0: a 1D-distributed level -- adj/ew hold only the entries of
+// rows [row_lo, row_hi) (the caller passes that slice); offs and vw complete.
 std::unique_ptr<DGraph> upload_graph(Ctx& c, int64_t n, const int64_t* offs,
                                      const void* adj, int adt, const void* ew,
-                                     int edt, const void* vw, int vdt);
+                                     int edt, const void* vw, int vdt,
+                                     int64_t row_lo = 0, int64_t row_hi = -1);
 int64_t device_cutsize(Ctx& c, const DGraph& g, const int32_t* parts);
 void device_part_weights(Ctx& c, const DGraph& g, const int32_t* parts, int k,
                          int64_t* d_pw);

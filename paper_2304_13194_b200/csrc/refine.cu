@@ -358,13 +358,18 @@ __global__ void k_iota(int32_t* p, int64_t lo, int64_t n) {
 
 void build_shard_lists(Ctx& c, const DGraph& g, int rank, int size, ShardLists& s) {
   s.scratch.ensure((size_t)size + 1 + 2 * NBINS, c.stream);
-  k_shard_bounds<<<1, 1024, 0, c.stream>>>(g.offs.get(), g.n, size, s.scratch.get());
-  CK(cudaGetLastError());
-  std::vector<int64_t> b(size + 1);
-  d2h(c, b.data(), s.scratch.get(), size + 1);
-  c.sync();
-  s.lo = b[rank];
-  s.hi = b[rank + 1];
+  if (g.partial()) {  // a distributed level: the block it was given
+    s.lo = g.row_lo;
+    s.hi = g.row_hi;
+  } else {
+    k_shard_bounds<<<1, 1024, 0, c.stream>>>(g.offs.get(), g.n, size, s.scratch.get());
+    CK(cudaGetLastError());
+    std::vector<int64_t> b(size + 1);
+    d2h(c, b.data(), s.scratch.get(), size + 1);
+    c.sync();
+    s.lo = b[rank];
+    s.hi = b[rank + 1];
+  }
   unsigned long long cnts[NBINS] = {};
   for (int t = 0; t < NBINS; ++t) {
     s.list[t] = nullptr;
