@@ -99,6 +99,7 @@ typedef struct {
   int32_t iterations, lp_passes, weak_passes, strong_passes, rebalance_stuck;
   int64_t moves;
   double seconds;
+  int32_t distributed; /* 1: this rank held only its block of the level's rows */
 } jet_level_stats;
 
 #define JET_MAX_LEVELS 64

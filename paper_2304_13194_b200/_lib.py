@@ -63,6 +63,7 @@ class LevelStats(C.Structure):
         ("balanced_in", i32), ("balanced", i32), ("iterations", i32),
         ("lp_passes", i32), ("weak_passes", i32), ("strong_passes", i32),
         ("rebalance_stuck", i32), ("moves", i64), ("seconds", C.c_double),
+        ("distributed", i32),
     ]
 
 

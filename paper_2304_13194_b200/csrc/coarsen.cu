@@ -2514,9 +2514,11 @@ static void device_match_fast_dist(Ctx& c, const DGraph& g, int32_t* partner) {
 
 // The contraction of a distributed level: every rank merges the coarse rows
 // whose representative it owns (importing the partner rows that live on
-// higher ranks), then the coarse rows of all ranks are gathered -- coarse ids
-// are ascending in the representative, so the ranks' ranges are contiguous
-// and in rank order. The result equals device_contract's, on every rank.
+// higher ranks). Coarse ids are ascending in the representative, so the
+// ranks' coarse ranges are contiguous and in rank order: a large coarse level
+// stays distributed on those ranges (complete offsets and vertex weights,
+// own rows), a small one is gathered whole. Either way it equals
+// device_contract's result.
 static std::unique_ptr<DGraph> device_contract_dist(Ctx& c, const DGraph& g, const int32_t* partner,
                                                     int32_t* vmap) {
   JET_REQUIRE(c.comm, JET_EINVAL, "a distributed level needs a communicator");
@@ -2674,9 +2676,16 @@ static std::unique_ptr<DGraph> device_contract_dist(Ctx& c, const DGraph& g, con
     });
   DBuf<uint8_t> gdeg, gadj, gew;
   const int64_t nrow = gather_all(c, cdeg_p + c_lo, ncl * 8, gdeg) / 8;
-  const int64_t cnnz = gather_all(c, ladj.get(), lnnz * 4, gadj) / 4;
-  gather_all(c, lew.get(), lnnz * 4, gew);
   JET_REQUIRE(nrow == nc, JET_EINTERNAL, "distributed contraction lost coarse rows");
+  const int64_t cnnz_all = comm_sum(c, lnnz);
+  // large coarse levels stay distributed (their owned rows only); smaller
+  // ones are gathered whole on every rank
+  const bool keep = nc > 4096 && (nc >= c.shard_min_n || cnnz_all >= 64 * c.shard_min_n);
+  int64_t cnnz = cnnz_all;
+  if (!keep) {
+    cnnz = gather_all(c, ladj.get(), lnnz * 4, gadj) / 4;
+    gather_all(c, lew.get(), lnnz * 4, gew);
+  }
   unsigned hovf = 0;
   d2h(c, &hovf, ovf.get(), 1);
   c.sync();
@@ -2696,11 +2705,25 @@ static std::unique_ptr<DGraph> device_contract_dist(Ctx& c, const DGraph& g, con
     });
   }
   cg_->nnz = cnnz;
-  cg_->adj.alloc(cnnz > 0 ? cnnz : 1, c.stream);
-  cg_->ew.alloc(cnnz > 0 ? cnnz : 1, c.stream);
-  if (cnnz) {
-    CK(cudaMemcpyAsync(cg_->adj.get(), gadj.get(), (size_t)cnnz * 4, cudaMemcpyDeviceToDevice, c.stream));
-    CK(cudaMemcpyAsync(cg_->ew.get(), gew.get(), (size_t)cnnz * 4, cudaMemcpyDeviceToDevice, c.stream));
+  if (keep) {  // the coarse rows [c_lo, c_hi): a distributed level again
+    int64_t e0 = 0;
+    if (c_lo < nc) d2h(c, &e0, cg_->offs.get() + c_lo, 1);
+    else e0 = cnnz;
+    c.sync();
+    cg_->row_lo = c_lo;
+    cg_->row_hi = c_hi;
+    cg_->ent_lo = e0;
+    cg_->adj = std::move(ladj);
+    cg_->ew = std::move(lew);
+    cg_->adj.n = (size_t)lnnz;
+    cg_->ew.n = (size_t)lnnz;
+  } else {
+    cg_->adj.alloc(cnnz > 0 ? cnnz : 1, c.stream);
+    cg_->ew.alloc(cnnz > 0 ? cnnz : 1, c.stream);
+    if (cnnz) {
+      CK(cudaMemcpyAsync(cg_->adj.get(), gadj.get(), (size_t)cnnz * 4, cudaMemcpyDeviceToDevice, c.stream));
+      CK(cudaMemcpyAsync(cg_->ew.get(), gew.get(), (size_t)cnnz * 4, cudaMemcpyDeviceToDevice, c.stream));
+    }
   }
   finalize_graph(c, *cg_);
   return cg_;

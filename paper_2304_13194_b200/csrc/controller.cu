@@ -318,6 +318,7 @@ void run_partition(Ctx& c, const DGraph& g0, const jet_config& cfg, int32_t* par
     jet_level_stats& L = S.levels[li++];
     memset(&L, 0, sizeof(L));
     L.level = level;
+    L.distributed = g.partial() ? 1 : 0;
     L.n = g.n;
     L.m = g.nnz / 2;
     L.cut_in = cut;

@@ -130,9 +130,10 @@ def test_sharded_rmat24_equals_unsharded():
         assert np.array_equal(parts, ref_parts)
 
 
-def _run_distributed(g, cfg, size):
+def _run_distributed(g, cfg, size, shard_min=None):
     """Each local rank uploads only its row block (DeviceGraph.upload_block):
-    the finest level's matching, contraction and refinement run distributed."""
+    the finest level's matching, contraction and refinement run distributed
+    (and those of every coarse level of >= shard_min vertices)."""
     from paper_2304_13194_b200 import dist as jd
     group = _lib.LocalGroup(size)
     ctxs = [_lib.Context(0) for _ in range(size)]
@@ -142,6 +143,8 @@ def _run_distributed(g, cfg, size):
     def work(r):
         try:
             ctxs[r].attach_local(group, r)
+            if shard_min is not None:
+                ctxs[r].set_shard_min_vertices(shard_min)
             dg = _lib.DeviceGraph.upload_block(g, int(b[r]), int(b[r + 1]), ctxs[r])
             blocks[r] = dg.block()
             out[r] = partition_resident(dg, g, cfg, want_parts=True)
@@ -160,17 +163,24 @@ def _run_distributed(g, cfg, size):
     return out, blocks, b
 
 
-@pytest.mark.parametrize("name,size", [("grid27_32", 2), ("grid27_32", 3), ("rmat16", 2)])
-def test_distributed_finest_level_equals_replicated(name, size):
+@pytest.mark.parametrize("name,size,smin", [("grid27_32", 2, None), ("grid27_32", 3, None),
+                                            ("rmat16", 2, None), ("grid27_32", 3, 1000),
+                                            ("rmat16", 3, 1000)])
+def test_distributed_levels_equal_replicated(name, size, smin):
     """Throughput mode on a 1D-distributed graph (every rank stores only its
-    rows): same partition as the replicated run, bit for bit, and each rank
-    holds only its block's entries."""
+    rows; with smin=1000 the coarse levels above 4096 vertices stay
+    distributed too): same partition as the replicated run, bit for bit, and
+    each rank holds only its block's entries."""
     g = gen.grid27_graph(32) if name.startswith("grid") else gen.rmat_graph(16, 16, 0)
     cfg = J.RefinerConfig(k=16, imbalance=0.03, seed=0, deterministic=False)
     ref_parts, ref_pw, ref_st = partition_resident(_lib.DeviceGraph.upload(g), g, cfg)
-    res, blocks, b = _run_distributed(g, cfg, size)
+    res, blocks, b = _run_distributed(g, cfg, size, smin)
     offs = np.asarray(g.row_offsets)
     for r, ((parts, pw, st), (lo, hi, ent)) in enumerate(zip(res, blocks)):
+        dist_levels = [st.levels[i].level for i in range(st.n_levels) if st.levels[i].distributed]
+        assert 0 in dist_levels
+        if smin is not None:
+            assert len(dist_levels) >= 2, dist_levels
         assert (lo, hi) == (b[r], b[r + 1])
         assert ent == offs[hi] - offs[lo] < offs[-1]
         assert st.cutsize == ref_st.cutsize
