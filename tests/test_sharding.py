@@ -186,3 +186,35 @@ def test_distributed_levels_equal_replicated(name, size, smin):
         assert st.cutsize == ref_st.cutsize
         assert np.array_equal(pw, ref_pw)
         assert np.array_equal(parts, ref_parts)
+
+
+def test_nccl_transport_distributed_single_rank():
+    """The distributed path (block upload, halo exchanges, coarse gathers)
+    over the NCCL transport with one rank holding the whole block."""
+    g = gen.grid27_graph(24)
+    cfg = J.RefinerConfig(k=8, imbalance=0.03, seed=0, deterministic=False)
+    ref_parts, _, ref_st = partition_resident(_lib.DeviceGraph.upload(g), g, cfg)
+    ctx = _lib.Context(0)
+    ctx.attach_nccl(_lib.nccl_unique_id(), 0, 1)
+    ctx.set_shard_min_vertices(1000)
+    dg = _lib.DeviceGraph.upload_block(g, 0, g.n, ctx)
+    parts, _, st = partition_resident(dg, g, cfg)
+    assert st.levels[st.n_levels - 1].distributed == 1  # L0 (uncoarsened last)
+    dg.free()
+    ctx.detach()
+    assert st.cutsize == ref_st.cutsize
+    assert np.array_equal(parts, ref_parts)
+
+
+def test_distributed_rmat24_equals_replicated():
+    """R-MAT 2^24 ef16, k=64, throughput mode, two local ranks each storing
+    half the rows (levels >= 2^20 vertices distributed)."""
+    g = gen.rmat_graph(24, 16, 0)
+    cfg = J.RefinerConfig(k=64, imbalance=0.03, seed=0, deterministic=False)
+    ref_parts, ref_pw, ref_st = partition_resident(_lib.DeviceGraph.upload(g), g, cfg)
+    res, blocks, b = _run_distributed(g, cfg, 2)
+    for (parts, pw, st), (lo, hi, ent) in zip(res, blocks):
+        assert ent < int(np.asarray(g.row_offsets)[-1])
+        assert st.cutsize == ref_st.cutsize
+        assert np.array_equal(pw, ref_pw)
+        assert np.array_equal(parts, ref_parts)
