@@ -177,8 +177,10 @@ void jet_graph_free(jet_graph* g);
  * moves and the evicted sets. The apply step walks the owned moved rows
  * only; the doubled cut delta and the k part-weight deltas are summed over
  * the ranks by one ncclAllReduce (k + 1 words) and every rank commits the
- * gathered move set. Coarsening still runs replicated on every rank, and
- * smaller levels run unsharded. Every rank computes the same partition,
+ * gathered move set. With a graph uploaded per rank (jet_graph_upload_block,
+ * throughput mode) the matching and contraction run distributed as well and
+ * large coarse levels stay distributed; otherwise coarsening runs replicated.
+ * Smaller levels run unsharded. Every rank computes the same partition,
  * bit-identical to the unsharded run.
  * NCCL (one process per GPU): rank 0 calls jet_comm_nccl_id, the id is
  * broadcast out of band (torch.distributed), every rank attaches.

@@ -4,8 +4,9 @@ One process per GPU under torchrun. torch.distributed is only the bootstrap:
 rank 0 creates the NCCL unique id, every rank receives it through a
 broadcast and attaches its context to the communicator; the exchange steps
 then run inside libjet over NCCL (csrc/comm.cu). Every rank computes the same
-partition. `shard_bounds` mirrors the device-side block split (csrc/refine.cu
-k_shard_bounds) for host-side checks.
+partition. `shard_bounds` is the block split (balanced by entries, as
+csrc/refine.cu k_shard_bounds): rank r uploads rows [b_r, b_{r+1}) with
+`_lib.DeviceGraph.upload_block` for a distributed partition.
 """
 
 from __future__ import annotations
