@@ -2381,6 +2381,39 @@ __global__ void k_import_rows(const int32_t* __restrict__ ids, const int64_t* __
   }
 }
 
+// owner rank of each export's representative; per-destination counts
+__global__ void k_export_dest(const int32_t* __restrict__ ids, int64_t nx,
+                              const int32_t* __restrict__ partner, const int64_t* __restrict__ bnd,
+                              int size, int32_t* dest, unsigned long long* dcount) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nx;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = partner[ids[i]];
+    int lo = 0, hi = size;  // last r with bnd[r] <= a
+    while (hi - lo > 1) {
+      const int m = (lo + hi) / 2;
+      if (bnd[m] <= a) lo = m;
+      else hi = m;
+    }
+    dest[i] = lo;
+    atomicAdd(dcount + lo, 1ull);
+  }
+}
+
+// exports grouped by destination rank (order inside a group is immaterial:
+// the receiver indexes rows by id)
+__global__ void k_export_group(const int32_t* __restrict__ ids, const int64_t* __restrict__ lens,
+                               const int32_t* __restrict__ dest, int64_t nx,
+                               const int64_t* __restrict__ doff, unsigned long long* dfill,
+                               int32_t* gids, int64_t* glens) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nx;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int d = dest[i];
+    const int64_t q = doff[d] + (int64_t)atomicAdd(dfill + d, 1ull);
+    gids[q] = ids[i];
+    glens[q] = lens[i];
+  }
+}
+
 // gather `bytes` of every rank, rank-major, into `out` (resized); total bytes
 int64_t gather_all(Ctx& c, const void* d, int64_t bytes, DBuf<uint8_t>& out) {
   std::vector<int64_t> counts;
@@ -2570,29 +2603,76 @@ static std::unique_ptr<DGraph> device_contract_dist(Ctx& c, const DGraph& g, con
   unsigned long long nx = 0;
   d2h(c, &nx, xc.get(), 1);
   c.sync();
-  DBuf<uint8_t> r_ids, r_lens, r_ent;
-  const int64_t nimp = gather_all(c, xids.get(), (int64_t)nx * 4, r_ids) / 4;
-  gather_all(c, xlen.get(), (int64_t)nx * 8, r_lens);
+  // group the exports by the rank that owns their representative and send
+  // each rank only its own imports (all-to-all)
+  const int size = c.comm->size;
+  std::vector<int64_t> bnd(size + 1);
+  {
+    DBuf<uint8_t> rl;
+    DBuf<int64_t> mylo(1, c.stream);
+    h2d(c, mylo.get(), &lo, 1);
+    gather_all(c, mylo.get(), 8, rl);
+    d2h(c, bnd.data(), reinterpret_cast<const int64_t*>(rl.get()), size);
+    c.sync();
+    bnd[size] = n;
+  }
+  DBuf<int64_t> bnd_d(size + 1, c.stream), doff_d(size + 1, c.stream);
+  h2d(c, bnd_d.get(), bnd.data(), size + 1);
+  DBuf<int32_t> xdest(std::max<int64_t>(1, (int64_t)nx), c.stream), gids(std::max<int64_t>(1, (int64_t)nx), c.stream);
+  DBuf<int64_t> glens(std::max<int64_t>(1, (int64_t)nx) + 1, c.stream);
+  DBuf<unsigned long long> dcnt(2 * size, c.stream);
+  dzero(c, dcnt.get(), 2 * size);
+  if (nx)
+    launch(c, "export_dest", 16.0 * (double)nx, [&] {
+      k_export_dest<<<grid_for(c, (int64_t)nx, 256), 256, 0, c.stream>>>(xids.get(), (int64_t)nx, partner,
+                                                                        bnd_d.get(), size, xdest.get(),
+                                                                        dcnt.get());
+    });
+  std::vector<unsigned long long> hcnt(size);
+  d2h(c, hcnt.data(), dcnt.get(), size);
+  c.sync();
+  std::vector<int64_t> doff(size + 1, 0), scnt(size);
+  for (int r = 0; r < size; ++r) doff[r + 1] = doff[r] + (int64_t)hcnt[r];
+  h2d(c, doff_d.get(), doff.data(), size + 1);
+  if (nx)
+    launch(c, "export_group", 24.0 * (double)nx, [&] {
+      k_export_group<<<grid_for(c, (int64_t)nx, 256), 256, 0, c.stream>>>(
+          xids.get(), xlen.get(), xdest.get(), (int64_t)nx, doff_d.get(), dcnt.get() + size, gids.get(),
+          glens.get());
+    });
   int64_t xe = 0;
   {
-    dzero(c, xlen.get() + nx, 1);
+    dzero(c, glens.get() + nx, 1);
     size_t tmp = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, xlen.get(), xoff.get(), (int)(nx + 1), c.stream));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, glens.get(), xoff.get(), (int)(nx + 1), c.stream));
     void* p = c.cub_scratch(tmp);
     launch(c, "export_scan", 16.0 * (double)nx, [&] {
-      CK(cub::DeviceScan::ExclusiveSum(p, tmp, xlen.get(), xoff.get(), (int)(nx + 1), c.stream));
+      CK(cub::DeviceScan::ExclusiveSum(p, tmp, glens.get(), xoff.get(), (int)(nx + 1), c.stream));
     });
-    d2h(c, &xe, xoff.get() + nx, 1);
-    c.sync();
   }
+  std::vector<int64_t> eb(size + 1);  // entry offsets at the group boundaries
+  for (int r = 0; r <= size; ++r) d2h(c, &eb[r], xoff.get() + doff[r], 1);
+  c.sync();
+  xe = eb[size];
   DBuf<int2> xent(std::max<int64_t>(1, xe), c.stream);
   const GView gv = view(g);
   if (nx)
     launch(c, "export_gather", 16.0 * (double)xe, [&] {
-      k_gather_rows<<<grid_for(c, (int64_t)nx * 128, 128), 128, 0, c.stream>>>(xids.get(), xoff.get(),
+      k_gather_rows<<<grid_for(c, (int64_t)nx * 128, 128), 128, 0, c.stream>>>(gids.get(), xoff.get(),
                                                                              (int64_t)nx, gv, xent.get());
     });
-  const int64_t ne = gather_all(c, xent.get(), xe * 8, r_ent) / 8;
+  DBuf<uint8_t> r_ids, r_lens, r_ent;
+  std::vector<int64_t> rc;
+  for (int r = 0; r < size; ++r) scnt[r] = (doff[r + 1] - doff[r]) * 4;
+  c.comm->alltoallv(c, gids.get(), scnt, r_ids, rc);
+  int64_t nimp = 0;
+  for (int64_t x : rc) nimp += x / 4;
+  for (int r = 0; r < size; ++r) scnt[r] = (doff[r + 1] - doff[r]) * 8;
+  c.comm->alltoallv(c, glens.get(), scnt, r_lens, rc);
+  for (int r = 0; r < size; ++r) scnt[r] = (eb[r + 1] - eb[r]) * 8;
+  c.comm->alltoallv(c, xent.get(), scnt, r_ent, rc);
+  int64_t ne = 0;
+  for (int64_t x : rc) ne += x / 8;
   DBuf<int64_t> ioff(nimp + 1, c.stream);
   DBuf<int64_t> imp_pos(n, c.stream);
   DBuf<int32_t> imp_adj(std::max<int64_t>(1, ne), c.stream), imp_ew(std::max<int64_t>(1, ne), c.stream);

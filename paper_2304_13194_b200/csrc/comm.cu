@@ -78,6 +78,29 @@ void LocalComm::allgatherv(Ctx& c, const void* dsend, int64_t bytes, DBuf<uint8_
   g->barrier();  // no rank reuses its send buffer before every copy is done
 }
 
+void LocalComm::alltoallv(Ctx& c, const void* dsend, const std::vector<int64_t>& scounts,
+                          DBuf<uint8_t>& recv, std::vector<int64_t>& rcounts) {
+  c.sync();  // the send buffer is complete
+  g->ptrs[rank] = dsend;
+  g->sc[rank] = scounts;
+  g->barrier();
+  rcounts.assign(size, 0);
+  int64_t total = 0;
+  for (int s = 0; s < size; ++s) total += (rcounts[s] = g->sc[s][rank]);
+  recv.ensure((size_t)std::max<int64_t>(total, 1), c.stream);
+  int64_t off = 0;
+  for (int s = 0; s < size; ++s) {
+    int64_t src = 0;  // rank s's bytes for ranks before this one
+    for (int r = 0; r < rank; ++r) src += g->sc[s][r];
+    if (rcounts[s])
+      CK(cudaMemcpyAsync(recv.get() + off, static_cast<const uint8_t*>(g->ptrs[s]) + src,
+                         (size_t)rcounts[s], cudaMemcpyDeviceToDevice, c.stream));
+    off += rcounts[s];
+  }
+  c.sync();
+  g->barrier();  // no rank reuses its send buffer before every copy is done
+}
+
 // ---- NCCL, opened at run time (no link-time dependency) -------------------
 namespace {
 typedef struct {
@@ -89,6 +112,8 @@ typedef int (*PCommInitRank)(NcclComm_t*, int, NcclId, int);
 typedef int (*PAllGather)(const void*, void*, size_t, int, NcclComm_t, cudaStream_t);
 typedef int (*PAllReduce)(const void*, void*, size_t, int, int, NcclComm_t, cudaStream_t);
 typedef int (*PCommDestroy)(NcclComm_t);
+typedef int (*PSendRecv)(void*, size_t, int, int, NcclComm_t, cudaStream_t);
+typedef int (*PGroup)();
 typedef const char* (*PGetErrorString)(int);
 constexpr int NCCL_INT8 = 0, NCCL_UINT64 = 5, NCCL_SUM = 0;
 
@@ -98,6 +123,8 @@ struct NcclApi {
   PCommInitRank init = nullptr;
   PAllGather allgather = nullptr;
   PAllReduce allreduce = nullptr;
+  PSendRecv send = nullptr, recv = nullptr;
+  PGroup group_start = nullptr, group_end = nullptr;
   PCommDestroy destroy = nullptr;
   PGetErrorString err = nullptr;
   bool load() {
@@ -111,9 +138,14 @@ struct NcclApi {
     init = (PCommInitRank)dlsym(h, "ncclCommInitRank");
     allgather = (PAllGather)dlsym(h, "ncclAllGather");
     allreduce = (PAllReduce)dlsym(h, "ncclAllReduce");
+    send = (PSendRecv)dlsym(h, "ncclSend");
+    recv = (PSendRecv)dlsym(h, "ncclRecv");
+    group_start = (PGroup)dlsym(h, "ncclGroupStart");
+    group_end = (PGroup)dlsym(h, "ncclGroupEnd");
     destroy = (PCommDestroy)dlsym(h, "ncclCommDestroy");
     err = (PGetErrorString)dlsym(h, "ncclGetErrorString");
-    return get_id && init && allgather && allreduce && destroy;
+    return get_id && init && allgather && allreduce && send && recv && group_start && group_end &&
+           destroy;
   }
 };
 NcclApi& nccl() {
@@ -132,6 +164,35 @@ struct NcclComm : Comm {
   DBuf<uint8_t> stage, padded;
   ~NcclComm() override {
     if (comm) nccl().destroy(comm);
+  }
+  void alltoallv(Ctx& c, const void* dsend, const std::vector<int64_t>& scounts,
+                 DBuf<uint8_t>& recv, std::vector<int64_t>& rcounts) override {
+    // counts: all-gather every rank's send-count row, read this rank's column
+    cnt.ensure((size_t)size * (size + 1), c.stream);
+    h2d(c, cnt.get() + (size_t)size * size, scounts.data(), size);
+    nck(nccl().allgather(cnt.get() + (size_t)size * size, cnt.get(), sizeof(int64_t) * size, NCCL_INT8,
+                         comm, c.stream),
+        "ncclAllGather(counts)");
+    std::vector<int64_t> m((size_t)size * size);
+    d2h(c, m.data(), cnt.get(), (size_t)size * size);
+    c.sync();
+    rcounts.assign(size, 0);
+    int64_t total = 0;
+    for (int s = 0; s < size; ++s) total += (rcounts[s] = m[(size_t)s * size + rank]);
+    recv.ensure((size_t)std::max<int64_t>(total, 1), c.stream);
+    nck(nccl().group_start(), "ncclGroupStart");
+    int64_t so = 0, ro = 0;
+    for (int p = 0; p < size; ++p) {
+      if (scounts[p])
+        nck(nccl().send(const_cast<uint8_t*>(static_cast<const uint8_t*>(dsend)) + so, (size_t)scounts[p],
+                        NCCL_INT8, p, comm, c.stream),
+            "ncclSend");
+      if (rcounts[p])
+        nck(nccl().recv(recv.get() + ro, (size_t)rcounts[p], NCCL_INT8, p, comm, c.stream), "ncclRecv");
+      so += scounts[p];
+      ro += rcounts[p];
+    }
+    nck(nccl().group_end(), "ncclGroupEnd");
   }
   void allreduce_sum(Ctx& c, unsigned long long* d, int64_t count) override {
     if (count <= 0) return;

@@ -23,6 +23,11 @@ struct Comm {
   // c.stream) into `recv`, rank-major and compact; counts[r] = rank r's bytes.
   virtual void allgatherv(Ctx& c, const void* dsend, int64_t bytes, DBuf<uint8_t>& recv,
                           std::vector<int64_t>& counts) = 0;
+  // Personalised exchange: scounts[r] bytes of `dsend` (rank-major, packed)
+  // go to rank r; rank s's bytes for this rank arrive rank-major in `recv`,
+  // rcounts[s] = their length.
+  virtual void alltoallv(Ctx& c, const void* dsend, const std::vector<int64_t>& scounts,
+                         DBuf<uint8_t>& recv, std::vector<int64_t>& rcounts) = 0;
   // In-place sum over ranks of a device array of 64-bit words (two's
   // complement: signed deltas sum correctly). NCCL: ncclAllReduce on the
   // context stream; the local group: gather + local sum.
@@ -38,7 +43,8 @@ struct LocalGroup {
   int64_t generation = 0;
   std::vector<const void*> ptrs;
   std::vector<int64_t> bytes;
-  explicit LocalGroup(int n) : size(n), ptrs(n, nullptr), bytes(n, 0) {}
+  std::vector<std::vector<int64_t>> sc;  // alltoallv: every rank's send counts
+  explicit LocalGroup(int n) : size(n), ptrs(n, nullptr), bytes(n, 0), sc(n) {}
   void barrier();
 };
 
@@ -50,6 +56,8 @@ struct LocalComm : Comm {
   }
   void allgatherv(Ctx& c, const void* dsend, int64_t bytes, DBuf<uint8_t>& recv,
                   std::vector<int64_t>& counts) override;
+  void alltoallv(Ctx& c, const void* dsend, const std::vector<int64_t>& scounts,
+                 DBuf<uint8_t>& recv, std::vector<int64_t>& rcounts) override;
 };
 
 // Returns nullptr (and sets the error) when libnccl cannot be opened.
