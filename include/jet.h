@@ -89,6 +89,8 @@ typedef struct {
                                    k >= patience_min_k (0: off) */
   int32_t patience_from_level;
   int32_t patience_min_k;
+  int32_t initpart_device;  /* 1: initial partitioning on the device (one block
+                               per restart), else on the host; same result */
 } jet_config;
 
 typedef struct {

@@ -53,7 +53,7 @@ class JetConfig(C.Structure):
         ("seed", C.c_uint64), ("coarse_target", i32), ("restarts", i32),
         ("afterburner", i32), ("locking", i32), ("deterministic", i32),
         ("verbose", i32), ("throughput_patience", i32), ("patience_from_level", i32),
-        ("patience_min_k", i32),
+        ("patience_min_k", i32), ("initpart_device", i32),
     ]
 
 

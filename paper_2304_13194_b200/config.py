@@ -45,6 +45,11 @@ class RefinerConfig:
     throughput_patience: int = 4
     patience_from_level: int = 0
     patience_min_k: int = 32
+    # initial partitioning of the coarsest level (initpart.py:30-94) on the
+    # device, one thread block per restart, instead of the host; the same
+    # partition either way. Off by default: greedy growing is a chain of n
+    # dependent steps, each a block-wide reduction on the device.
+    device_initial_partition: bool = False
 
     def __post_init__(self):
         if self.k < 1:
@@ -102,4 +107,5 @@ def to_c(config: RefinerConfig, total_weight: int) -> _lib.JetConfig:
         throughput_patience=getattr(config, "throughput_patience", 0),
         patience_from_level=getattr(config, "patience_from_level", 0),
         patience_min_k=getattr(config, "patience_min_k", 0),
+        initpart_device=int(bool(getattr(config, "device_initial_partition", False))),
     )

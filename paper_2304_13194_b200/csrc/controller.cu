@@ -6,6 +6,7 @@
 #include "comm.cuh"
 #include "coarsen.cuh"
 #include "initpart.h"
+#include "initpart_dev.cuh"
 #include "rng.h"
 #include <algorithm>
 #include <chrono>
@@ -277,21 +278,32 @@ void run_partition(Ctx& c, const DGraph& g0, const jet_config& cfg, int32_t* par
 
   const int top = h.size() - 1;
   const DGraph& gc = h.level(top);
-  HostGraph hg;
-  download_host_graph(c, gc, hg);
-  std::vector<int32_t> ip = host_initial_partition(hg, k, cfg.limit, cfg.seed, cfg.restarts);
   Workspace w;
   w.ensure(c, g0.n, k);
   w.h_pw.assign(k, 0);
-  int64_t cut2 = 0;
-  for (int64_t v = 0; v < hg.n; ++v) {
-    w.h_pw[ip[v]] += hg.vw[v];
-    for (int64_t j = hg.offs[v]; j < hg.offs[v + 1]; ++j)
-      if (ip[v] != ip[hg.adj[j]]) cut2 += hg.ew[j];
-  }
-  int64_t cut = cut2 / 2;
+  int64_t cut = 0;
   DBuf<int32_t> pa(g0.n, c.stream), pb(g0.n, c.stream), keep(g0.n, c.stream);
-  h2d(c, pa.get(), ip.data(), hg.n);
+  // initial partition: one block per restart on the device (initpart_dev.cu)
+  // when asked for and within its limits, else the host restatement
+  // (initpart.cpp); both reproduce initpart.py:30-94 exactly
+  if (cfg.initpart_device && device_initial_partition(c, gc, k, cfg.limit, cfg.seed, cfg.restarts,
+                                                      pa.get())) {
+    device_part_weights(c, gc, pa.get(), k, w.d_pw());
+    d2h(c, w.h_pw.data(), w.d_pw(), k);
+    cut = device_cutsize(c, gc, pa.get());  // synchronises
+  } else {
+    HostGraph hg;
+    download_host_graph(c, gc, hg);
+    std::vector<int32_t> ip = host_initial_partition(hg, k, cfg.limit, cfg.seed, cfg.restarts);
+    int64_t cut2 = 0;
+    for (int64_t v = 0; v < hg.n; ++v) {
+      w.h_pw[ip[v]] += hg.vw[v];
+      for (int64_t j = hg.offs[v]; j < hg.offs[v + 1]; ++j)
+        if (ip[v] != ip[hg.adj[j]]) cut2 += hg.ew[j];
+    }
+    cut = cut2 / 2;
+    h2d(c, pa.get(), ip.data(), hg.n);
+  }
   const double t2 = now_s();
   S.t_initial = t2 - t1;
 
