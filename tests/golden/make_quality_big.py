@@ -53,8 +53,8 @@ if __name__ == "__main__":
             generators.geometric_graph(spec[1], spec[2], spec[3])
         tg = time.time() - t
         globals()["_G"], globals()["_K"] = g, k
-        if len(seeds) == 1:
-            res = [_one(seeds[0])]
+        if len(seeds) == 1 or "--serial" in sys.argv:
+            res = [_one(sd) for sd in seeds]
         else:  # spawn, not fork: the oracle's OpenMP runtime does not survive a fork
             with mp.get_context("spawn").Pool(min(len(seeds), 4), initializer=_init,
                                               initargs=(g, k)) as pool:
