@@ -1299,6 +1299,10 @@ __device__ __forceinline__ bool fast_round_dead(const unsigned long long* prev) 
   return prev && (prev[0] == 0 || prev[1] == 0);
 }
 
+#ifndef PROPOSE_BATCH
+#define PROPOSE_BATCH 4
+#endif
+
 template <bool UNIT>
 __global__ void __launch_bounds__(256)
     k_propose_fast(GView g, int64_t n, const int32_t* __restrict__ partner, int32_t* prop,
@@ -1325,30 +1329,71 @@ __global__ void __launch_bounds__(256)
     const bool hub = deg > WARP_TIER_MAX_DEG;
     unsigned live_m = __ballot_sync(0xffffffffu, live && deg > 0 && !hub);
     int my_u = -1;
+    // PB rows per step, their loads interleaved: a row's adjacency load and
+    // the dependent partner[] gather are two L2/HBM round trips, and one row
+    // at a time left each warp waiting on 2 x 32 of them in sequence
+    constexpr int PB = PROPOSE_BATCH;
     while (live_m) {
-      const int r = __ffs(live_m) - 1;
-      live_m &= live_m - 1;
-      const int rv = (int)(base + r);
-      const int64_t rb = __shfl_sync(0xffffffffu, beg, r);
-      const int rd = __shfl_sync(0xffffffffu, deg, r);
-      unsigned bw = 0, bh = 0;
-      int bu = -1;
-      for (int j = lane; j < rd; j += 32) {
-        const int u = g.adj[rb + j];
-        if (partner[u] >= 0) continue;
-        const unsigned w = UNIT ? 1u : (unsigned)g.ew[rb + j];
-        const unsigned h = edge_hash(rv, u, salt);
-        if (w > bw || (w == bw && (h > bh || (h == bh && u < bu)))) {
-          bw = w;
-          bh = h;
-          bu = u;
+      int rr[PB], rd[PB];
+      int64_t rb[PB];
+      int maxd = 0;
+#pragma unroll
+      for (int q = 0; q < PB; ++q) {
+        rr[q] = -1;
+        rd[q] = 0;
+        rb[q] = 0;
+        if (live_m) {
+          const int r = __ffs(live_m) - 1;
+          live_m &= live_m - 1;
+          rr[q] = r;
+        }
+        const int src = rr[q] < 0 ? 0 : rr[q];
+        const int64_t b_ = __shfl_sync(0xffffffffu, beg, src);
+        const int d_ = __shfl_sync(0xffffffffu, deg, src);
+        if (rr[q] >= 0) {
+          rb[q] = b_;
+          rd[q] = d_;
+          maxd = max(maxd, d_);
         }
       }
-      const unsigned mw = __reduce_max_sync(0xffffffffu, bw);
-      const unsigned mh = __reduce_max_sync(0xffffffffu, bw == mw ? bh : 0u);
-      const unsigned mu = __reduce_min_sync(0xffffffffu, (bw == mw && bh == mh && bu >= 0)
-                                                              ? (unsigned)bu : 0xffffffffu);
-      if (lane == r) my_u = mw ? (int)mu : -1;
+      unsigned bw[PB], bh[PB];
+      int bu[PB];
+#pragma unroll
+      for (int q = 0; q < PB; ++q) {
+        bw[q] = 0;
+        bh[q] = 0;
+        bu[q] = -1;
+      }
+      for (int j = lane; j < maxd; j += 32) {
+        int u[PB], pu[PB];
+        unsigned w[PB];
+#pragma unroll
+        for (int q = 0; q < PB; ++q) {
+          u[q] = j < rd[q] ? g.adj[rb[q] + j] : -1;
+          w[q] = UNIT ? 1u : (j < rd[q] ? (unsigned)g.ew[rb[q] + j] : 0u);
+        }
+#pragma unroll
+        for (int q = 0; q < PB; ++q) pu[q] = u[q] >= 0 ? partner[u[q]] : 0;
+#pragma unroll
+        for (int q = 0; q < PB; ++q) {
+          if (u[q] < 0 || pu[q] >= 0) continue;
+          const unsigned h = edge_hash((int)(base + rr[q]), u[q], salt);
+          if (w[q] > bw[q] || (w[q] == bw[q] && (h > bh[q] || (h == bh[q] && u[q] < bu[q])))) {
+            bw[q] = w[q];
+            bh[q] = h;
+            bu[q] = u[q];
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < PB; ++q) {
+        if (rr[q] < 0) break;  // warp-uniform
+        const unsigned mw = __reduce_max_sync(0xffffffffu, bw[q]);
+        const unsigned mh = __reduce_max_sync(0xffffffffu, bw[q] == mw ? bh[q] : 0u);
+        const unsigned mu = __reduce_min_sync(0xffffffffu, (bw[q] == mw && bh[q] == mh && bu[q] >= 0)
+                                                                ? (unsigned)bu[q] : 0xffffffffu);
+        if (lane == rr[q]) my_u = mw ? (int)mu : -1;
+      }
     }
     if (live && !hub) prop[v] = my_u;
     warp_append(live && !hub && my_u >= 0, v, elist, ecnt);
@@ -1548,10 +1593,10 @@ static void device_match_fast(Ctx& c, const DGraph& g, int32_t* partner) {
         const unsigned salt = 0x5bd1e995u * (unsigned)(round + 1);
         launch(c, "propose", (g.unit_ew ? 8.0 : 12.0) * g.nnz + 12.0 * n, [&] {
           if (g.unit_ew)
-            k_propose_fast<true><<<grid_for(c, n, 256), 256, 0, c.stream>>>(
+            k_propose_fast<true><<<grid_res(c, k_propose_fast<true>, n, 256), 256, 0, c.stream>>>(
                 gv, n, partner, prop_p, elist_p, rc, salt, prev);
           else
-            k_propose_fast<false><<<grid_for(c, n, 256), 256, 0, c.stream>>>(
+            k_propose_fast<false><<<grid_res(c, k_propose_fast<false>, n, 256), 256, 0, c.stream>>>(
                 gv, n, partner, prop_p, elist_p, rc, salt, prev);
         });
         if (g.bin_cnt[BIN_BLOCK]) {
@@ -2197,27 +2242,35 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
   launch(c, "contract_rows", 12.0 * g.nnz + 8.0 * T + 16.0 * nc, [&] {
     k_merge_rows<<<grid_for(c, nc * 32, 256), 256, 0, c.stream>>>(rm);
   });
-  unsigned long long nbig = 0;
-  d2h(c, &nbig, big_cnt.get(), 1);
-  c.sync();
-  mark("alloc+rows");
-  LongRows longrows(c, big_p, (int64_t)nbig, rowlen_p, nc);
-  longrows.run(rm);
-  // final offsets
+  // final offsets: scanned right away, read back together with the long-row
+  // count -- one host wait per level when there are no long rows (meshes);
+  // otherwise the long rows are merged and the scan is redone
   cg_->offs.alloc(nc + 1, c.stream);
-  {
+  auto cdeg_scan = [&] {
     size_t tmp = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cdeg_p, cg_->offs.get(), (int)(nc + 1), c.stream));
     void* p = c.cub_scratch(tmp);
     launch(c, "cdeg_scan", 16.0 * nc, [&] {
       CK(cub::DeviceScan::ExclusiveSum(p, tmp, cdeg_p, cg_->offs.get(), (int)(nc + 1), c.stream));
     });
-  }
+  };
+  cdeg_scan();
+  unsigned long long nbig = 0;
   int64_t cnnz = 0;
   unsigned hovf = 0;
+  d2h(c, &nbig, big_cnt.get(), 1);
   d2h(c, &cnnz, cg_->offs.get() + nc, 1);
   d2h(c, &hovf, ovf.get(), 1);
   c.sync();
+  mark("alloc+rows");
+  LongRows longrows(c, big_p, (int64_t)nbig, rowlen_p, nc);
+  if (nbig) {
+    longrows.run(rm);
+    cdeg_scan();
+    d2h(c, &cnnz, cg_->offs.get() + nc, 1);
+    d2h(c, &hovf, ovf.get(), 1);
+    c.sync();
+  }
   JET_REQUIRE(!(hovf & 1u), JET_EUNSUPPORTED, "coarse vertex weight exceeds int32");
   JET_REQUIRE(!(hovf & 2u), JET_EUNSUPPORTED, "coarse edge weight exceeds int32");
   cg_->nnz = cnnz;
@@ -2462,10 +2515,10 @@ static void device_match_fast_dist(Ctx& c, const DGraph& g, int32_t* partner) {
     const unsigned salt = 0x5bd1e995u * (unsigned)(round + 1);
     launch(c, "propose", (g.unit_ew ? 8.0 : 12.0) * (double)g.local_nnz(), [&] {
       if (g.unit_ew)
-        k_propose_fast<true><<<grid_for(c, hi - lo, 256), 256, 0, c.stream>>>(
+        k_propose_fast<true><<<grid_res(c, k_propose_fast<true>, hi - lo, 256), 256, 0, c.stream>>>(
             gv, hi, partner, prop_p, elist_p, cnt.get(), salt, nullptr, lo);
       else
-        k_propose_fast<false><<<grid_for(c, hi - lo, 256), 256, 0, c.stream>>>(
+        k_propose_fast<false><<<grid_res(c, k_propose_fast<false>, hi - lo, 256), 256, 0, c.stream>>>(
             gv, hi, partner, prop_p, elist_p, cnt.get(), salt, nullptr, lo);
     });
     if (nh) {

@@ -306,6 +306,18 @@ inline unsigned grid_for(const Ctx& c, int64_t work_threads, int block,
   return (unsigned)(b < cap ? b : cap);
 }
 
+// Resident blocks per SM of `kern` at this block size (cached per kernel).
+int resident_blocks(const void* kern, int block, size_t smem);
+
+// grid_for capped at the blocks that are resident at once: a grid-stride
+// kernel whose grid exceeds residency runs a second, partial wave with the
+// same per-warp share of the work, so part of the GPU idles at the end.
+template <class K>
+inline unsigned grid_res(const Ctx& c, K* kern, int64_t work_threads, int block,
+                         size_t smem = 0) {
+  return grid_for(c, work_threads, block, resident_blocks((const void*)kern, block, smem));
+}
+
 template <class T>
 inline void h2d(Ctx& c, T* dst, const T* src, size_t count) {
   if (count) CK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, c.stream));

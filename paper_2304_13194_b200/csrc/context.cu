@@ -13,6 +13,20 @@ static thread_local std::string g_last_error;
 
 void set_last_error(const std::string& s) { g_last_error = s; }
 
+int resident_blocks(const void* kern, int block, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t>, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(kern, block, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem));
+  if (per_sm < 1) per_sm = 1;
+  cache.emplace(key, per_sm);
+  return per_sm;
+}
+
 void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
   cudaGetLastError();
   std::string m = std::string("CUDA error '") + cudaGetErrorString(e) + "' in " +

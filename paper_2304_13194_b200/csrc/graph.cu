@@ -197,7 +197,7 @@ void finalize_graph(Ctx& c, DGraph& g) {
   CK(cudaMemsetAsync(&st.get()->min_vw, 0xff, sizeof(unsigned long long), c.stream));
   if (g.n > 0) {
     launch(c, "level_stats", 8.0 * g.n + 4.0 * g.n + 4.0 * g.nnz, [&] {
-      k_level_stats<<<grid_for(c, g.n > g.nnz ? g.n : g.nnz, 256), 256, 0, c.stream>>>(
+      k_level_stats<<<grid_res(c, k_level_stats, g.n > g.nnz ? g.n : g.nnz, 256), 256, 0, c.stream>>>(
           g.offs.get(), g.vw.get(), g.ew.get(), g.n, g.local_nnz(), g.tm, st.get());
     });
   }

@@ -129,3 +129,16 @@ def test_grid27_sizes():
             for a in (-1, 0, 1) for b in (-1, 0, 1) for c in (-1, 0, 1) if (a, b, c) != (0, 0, 0)) // 2
     assert g.n == n and g.m == m
     assert np.all(np.diff(g.adjacency[g.row_offsets[1]:g.row_offsets[2]]) > 0)
+
+
+@pytest.mark.parametrize("shape", [(5, 5, 5), (3, 4, 6), (1, 7, 2)])
+def test_grid27_matches_reference_preprocess(shape):
+    """grid27_graph builds the 27-point CSR directly; the golden is the
+    reference's preprocess (graph.py:132-200) of the raw stencil pairs
+    (tests/golden/make_grid27.py)."""
+    d = np.load(Path(__file__).parent / "golden" / "grid27.npz")
+    g = gen.grid27_graph(*shape)
+    key = "%dx%dx%d" % shape
+    for attr, suffix in (("row_offsets", "offs"), ("adjacency", "adj"),
+                         ("edge_weights", "ew"), ("vertex_weights", "vw")):
+        assert np.array_equal(getattr(g, attr), d[f"{key}_{suffix}"]), attr
