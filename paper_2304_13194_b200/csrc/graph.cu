@@ -464,11 +464,6 @@ void device_project(Ctx& c, const int32_t* vmap, const int32_t* pc, int32_t* pf,
 }
 
 // int64 <-> int32 helpers for the per-kernel entry points
-__global__ void k_widen(const int32_t* __restrict__ in, int64_t* __restrict__ out, int64_t n) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
-    out[i] = in[i];
-}
 
 void upload_i64_as_i32(Ctx& c, const int64_t* host, int64_t n, int32_t* dst,
                        long long lo, long long hi, const char* what) {
@@ -486,14 +481,42 @@ void upload_i64_as_i32(Ctx& c, const int64_t* host, int64_t n, int32_t* dst,
   JET_REQUIRE(!hb, JET_EINVAL, std::string(what) + " out of range");
 }
 
+// int32 -> int64 on the host cores, out of pinned memory (the caller's
+// pages are first touched here, by all threads)
+static void parallel_widen(int64_t* dst, const int32_t* src, int64_t count) {
+  const int64_t piece = (int64_t)1 << 18;
+  const int64_t np = (count + piece - 1) / piece;
+#pragma omp parallel for schedule(static) num_threads(std::min<int>(upload_threads(), omp_get_num_procs()))
+  for (int64_t i = 0; i < np; ++i) {
+    const int64_t b = i * piece, e = std::min(count, b + piece);
+    for (int64_t j = b; j < e; ++j) dst[j] = src[j];
+  }
+}
+
+// Device int32 -> host int64: the int32 words cross PCIe into the pinned
+// ring (half the bytes of a device-side widen, and no pageable staging by the
+// driver) and are widened by the host threads, chunk i while chunk i+1 is
+// in flight.
 void download_i32_as_i64(Ctx& c, const int32_t* dsrc, int64_t n, int64_t* host) {
   if (n <= 0) return;
-  DBuf<int64_t> s(n, c.stream);
-  launch(c, "widen", 12.0 * n, [&] {
-    k_widen<<<grid_for(c, n, 256), 256, 0, c.stream>>>(dsrc, s.get(), n);
-  });
-  d2h(c, host, s.get(), n);
-  c.sync();
+  c.ensure_upload_ring();
+  const int64_t per = (int64_t)(Ctx::UPLOAD_CHUNK / sizeof(int32_t));
+  const int64_t nch = (n + per - 1) / per;
+  auto enqueue = [&](int64_t i) {
+    const int b = (int)(i % Ctx::UPLOAD_BUFS);
+    const int64_t len = std::min(per, n - i * per);
+    CK(cudaMemcpyAsync(c.up_host[b], dsrc + i * per, (size_t)len * sizeof(int32_t),
+                       cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaEventRecord(c.up_ev[b], c.stream));
+  };
+  for (int64_t i = 0; i < std::min<int64_t>(nch, Ctx::UPLOAD_BUFS); ++i) enqueue(i);
+  for (int64_t i = 0; i < nch; ++i) {
+    const int b = (int)(i % Ctx::UPLOAD_BUFS);
+    CK(cudaEventSynchronize(c.up_ev[b]));
+    parallel_widen(host + i * per, static_cast<const int32_t*>(c.up_host[b]),
+                   std::min(per, n - i * per));
+    if (i + Ctx::UPLOAD_BUFS < nch) enqueue(i + Ctx::UPLOAD_BUFS);
+  }
 }
 
 }  // namespace jet
