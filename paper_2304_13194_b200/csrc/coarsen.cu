@@ -397,7 +397,8 @@ struct TwoHopF {
 
 __device__ __forceinline__ void thf_queue(const TwoHopF& t, int ci, int round, int32_t* out,
                                           unsigned long long* ocnt) {
-  if (atomicExch(&t.cflag[ci], round) != round) out[atomicAdd(ocnt, 1ull)] = ci;
+  // aggregated over the lanes queueing together (one hot counter)
+  warp_append(atomicExch(&t.cflag[ci], round) != round, ci, out, ocnt);
 }
 
 __global__ void __launch_bounds__(1024)
@@ -1033,19 +1034,29 @@ __global__ void __launch_bounds__(1024) k_resolve_frontier(Frontier F) {
       if (threadIdx.x == 0) s_ndef = 0;
       __syncthreads();
       const int64_t i = b0 + threadIdx.x;
+      int x = -1, beg = 0, len = 0;
       if (i < 2 * L) {
         const int v = fin[i >> 1];
-        const int x = (i & 1) ? F.prop[v] : v;
-        const int beg = F.ioff[x], end = F.ioff[x + 1];
-        if (end - beg > FR_SHORT) {
+        x = (i & 1) ? F.prop[v] : v;
+        beg = F.ioff[x];
+        len = F.ioff[x + 1] - beg;
+        if (len > FR_SHORT) {
           const int d = atomicAdd(&s_ndef, 1);
           s_def[d] = x;  // d < blockDim <= FR_DEFER
-        } else {
-          for (int q = beg; q < end; ++q) {
-            const int y = fr_other(F, (int)(F.inc[q] & 0xffffffffu), x);
-            if (touch(y)) F.aff[atomicAdd(F.fcnt + 2 + par, 1ull)] = y;
-          }
+          len = 0;
         }
+      }
+      // short lists: the warp walks its lanes' lists in step, so each step's
+      // appends share one atomic (per-lane appends on the one counter
+      // serialised in L2)
+      const int maxlen = __reduce_max_sync(0xffffffffu, (unsigned)len);
+      for (int j = 0; j < maxlen; ++j) {
+        int y = -1;
+        if (j < len) {
+          y = fr_other(F, (int)(F.inc[beg + j] & 0xffffffffu), x);
+          if (!touch(y)) y = -1;
+        }
+        warp_append(y >= 0, y, F.aff, F.fcnt + 2 + par);
       }
       __syncthreads();
       for (int d = wib; d < s_ndef; d += nwb) {
@@ -1072,6 +1083,7 @@ __global__ void __launch_bounds__(1024) k_resolve_frontier(Frontier F) {
       if (threadIdx.x == 0) s_ndef = 0;
       __syncthreads();
       const int64_t i = b0 + threadIdx.x;
+      int qh = -1;  // head edge to queue for the next round
       if (i < A && F.partner[F.aff[i]] >= 0) {  // matched this round
         F.head[F.aff[i]] = F.ioff[F.aff[i] + 1];
       } else if (i < A) {
@@ -1085,11 +1097,12 @@ __global__ void __launch_bounds__(1024) k_resolve_frontier(Frontier F) {
             const int hz = fr_first_live_t(F, fr_other(F, h, y), FR_SHORT, &pz);
             if (hz == -2) defer = true;
             else if (hz == h && atomicExch(&F.qflag[h], round) != round)
-              fout[atomicAdd(F.fcnt + (cur ^ 1), 1ull)] = h;
+              qh = h;
           }
         }
         if (defer) s_def[atomicAdd(&s_ndef, 1)] = y;
       }
+      warp_append(qh >= 0, qh, fout, F.fcnt + (cur ^ 1));
       __syncthreads();
       for (int d = wib; d < s_ndef; d += nwb) {
         const int y = s_def[d];
