@@ -659,7 +659,11 @@ static void two_hop(Ctx& c, const DGraph& g, int32_t* partner) {
   // few leftovers (meshes): the full-pass rounds are cheaper than the
   // frontier bookkeeping; many (skewed graphs: 10^5-10^6 leftovers under hub
   // centres, hundreds of rounds) -> frontier
-  if (!old_th && nl > 16384) {
+  static const int64_t th_frontier_min = [] {
+    const char* e = getenv("JET_TH_FRONTIER_MIN");
+    return e ? (int64_t)atoll(e) : (int64_t)16384;
+  }();
+  if (!old_th && nl > th_frontier_min) {
     int32_t* ints = c.scratch<int32_t>(25, 2 * n + 5 * nc + nl + 64);
     unsigned long long* tc = c.scratch<unsigned long long>(26, 8);
     dzero(c, tc, 8);
