@@ -15,6 +15,7 @@
 // rows merged per coarse vertex, sorted by neighbour and de-duplicated with
 // summed weights, self loops dropped.
 #include "coarsen.cuh"
+#include "small_ops.cuh"
 #include "comm.cuh"
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
@@ -575,12 +576,14 @@ static void two_hop(Ctx& c, const DGraph& g, int32_t* partner) {
   {
     cub::CountingInputIterator<int32_t> it(0);
     IsFree op{partner};
-    size_t tmp = 0;
-    CK(cub::DeviceSelect::If(nullptr, tmp, it, left_p, nsel.get(), (int)n, op, c.stream));
-    void* p = c.cub_scratch(tmp);
-    launch(c, "th_leftovers", 8.0 * n, [&] {
-      CK(cub::DeviceSelect::If(p, tmp, it, left_p, nsel.get(), (int)n, op, c.stream));
-    });
+    if (!small_select(c, "th_leftovers", op, n, left_p, nsel.get())) {
+      size_t tmp = 0;
+      CK(cub::DeviceSelect::If(nullptr, tmp, it, left_p, nsel.get(), (int)n, op, c.stream));
+      void* p = c.cub_scratch(tmp);
+      launch(c, "th_leftovers", 8.0 * n, [&] {
+        CK(cub::DeviceSelect::If(p, tmp, it, left_p, nsel.get(), (int)n, op, c.stream));
+      });
+    }
   }
   int64_t nl = 0;
   d2h(c, &nl, nsel.get(), 1);
@@ -591,6 +594,7 @@ static void two_hop(Ctx& c, const DGraph& g, int32_t* partner) {
   launch(c, "th_deg", 20.0 * nl, [&] {
     k_leftover_deg<<<grid_for(c, nl, 256), 256, 0, c.stream>>>(left_p, nl, g.offs.get(), deg.get());
   });
+  if (!small_exclusive_sum(c, "th_scan", deg.get(), poff.get(), (int64_t)(nl + 1)))
   {
     size_t tmp = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, deg.get(), poff.get(), (int)(nl + 1), c.stream));
@@ -641,6 +645,7 @@ static void two_hop(Ctx& c, const DGraph& g, int32_t* partner) {
   d2h(c, &nc, nruns.get(), 1);
   c.sync();
   dzero(c, ccnt.get() + nc, 1);
+  if (!small_exclusive_sum(c, "th_scan", ccnt.get(), coff.get(), (int64_t)(nc + 1)))
   {
     size_t tmp = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ccnt.get(), coff.get(), (int)(nc + 1), c.stream));
@@ -1553,12 +1558,14 @@ static void leaf_match(Ctx& c, const DGraph& g, int32_t* partner) {
   {
     cub::CountingInputIterator<int32_t> it(0);
     IsFree op{partner};
-    size_t tmp = 0;
-    CK(cub::DeviceSelect::If(nullptr, tmp, it, left_p, nsel.get(), (int)n, op, c.stream));
-    void* p = c.cub_scratch(tmp);
-    launch(c, "th_leftovers", 8.0 * n, [&] {
-      CK(cub::DeviceSelect::If(p, tmp, it, left_p, nsel.get(), (int)n, op, c.stream));
-    });
+    if (!small_select(c, "th_leftovers", op, n, left_p, nsel.get())) {
+      size_t tmp = 0;
+      CK(cub::DeviceSelect::If(nullptr, tmp, it, left_p, nsel.get(), (int)n, op, c.stream));
+      void* p = c.cub_scratch(tmp);
+      launch(c, "th_leftovers", 8.0 * n, [&] {
+        CK(cub::DeviceSelect::If(p, tmp, it, left_p, nsel.get(), (int)n, op, c.stream));
+      });
+    }
   }
   int64_t nl = 0;
   d2h(c, &nl, nsel.get(), 1);
@@ -1572,12 +1579,14 @@ static void leaf_match(Ctx& c, const DGraph& g, int32_t* partner) {
   launch(c, "leaf_keys", 16.0 * nl, [&] {
     k_leaf_keys<<<grid_for(c, nl * 32, 256), 256, 0, c.stream>>>(gv, left_p, nl, vb, k0);
   });
-  size_t tmp = 0;
-  CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k0, k1, (int)nl, 0, 2 * vb, c.stream));
-  void* p = c.cub_scratch(tmp);
-  launch(c, "leaf_sort", 32.0 * nl, [&] {
-    CK(cub::DeviceRadixSort::SortKeys(p, tmp, k0, k1, (int)nl, 0, 2 * vb, c.stream));
-  });
+  if (!small_sort_keys(c, "leaf_sort", k0, k1, nl, 2 * vb)) {
+    size_t tmp = 0;
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k0, k1, (int)nl, 0, 2 * vb, c.stream));
+    void* p = c.cub_scratch(tmp);
+    launch(c, "leaf_sort", 32.0 * nl, [&] {
+      CK(cub::DeviceRadixSort::SortKeys(p, tmp, k0, k1, (int)nl, 0, 2 * vb, c.stream));
+    });
+  }
   launch(c, "leaf_pair", 16.0 * nl, [&] {
     k_leaf_pair<<<grid_for(c, nl, 256), 256, 0, c.stream>>>(k1, nl, vb, n, partner);
   });
@@ -2202,6 +2211,7 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
   launch(c, "is_rep", 8.0 * n, [&] {
     k_is_rep<<<grid_for(c, n, 256), 256, 0, c.stream>>>(partner, n, flag_p);
   });
+  if (!small_exclusive_sum(c, "rep_scan", flag_p, cid_p, (int64_t)(n)))
   {
     size_t tmp = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag_p, cid_p, (int)n, c.stream));
@@ -2233,6 +2243,7 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
   });
   dzero(c, rowlen_p + nc, 1);
   dzero(c, cdeg_p + nc, 1);
+  if (!small_exclusive_sum(c, "rowlen_scan", rowlen_p, toff_p, (int64_t)(nc + 1)))
   {
     size_t tmp = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, rowlen_p, toff_p, (int)(nc + 1), c.stream));
@@ -2264,6 +2275,7 @@ std::unique_ptr<DGraph> device_contract(Ctx& c, const DGraph& g, const int32_t* 
   // otherwise the long rows are merged and the scan is redone
   cg_->offs.alloc(nc + 1, c.stream);
   auto cdeg_scan = [&] {
+    if (small_exclusive_sum(c, "cdeg_scan", cdeg_p, cg_->offs.get(), (int64_t)(nc + 1))) return;
     size_t tmp = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cdeg_p, cg_->offs.get(), (int)(nc + 1), c.stream));
     void* p = c.cub_scratch(tmp);
@@ -2631,6 +2643,7 @@ static std::unique_ptr<DGraph> device_contract_dist(Ctx& c, const DGraph& g, con
   launch(c, "is_rep", 8.0 * n, [&] {
     k_is_rep<<<grid_for(c, n, 256), 256, 0, c.stream>>>(partner, n, flag_p);
   });
+  if (!small_exclusive_sum(c, "rep_scan", flag_p, cid_p, (int64_t)(n)))
   {
     size_t tmp = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag_p, cid_p, (int)n, c.stream));
@@ -2805,6 +2818,7 @@ static std::unique_ptr<DGraph> device_contract_dist(Ctx& c, const DGraph& g, con
   }
   // this rank's coarse rows, compacted, then every rank's
   DBuf<int64_t> loff(ncl + 1, c.stream);
+  if (!small_exclusive_sum(c, "cdeg_scan", cdeg_p + c_lo, loff.get(), (int64_t)(ncl + 1)))
   {
     size_t tmp = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cdeg_p + c_lo, loff.get(), (int)(ncl + 1), c.stream));

@@ -3,6 +3,7 @@
 // graph.py:240-242, projection driver.py:32-45).
 #include "common.cuh"
 #include "graph.cuh"
+#include "small_ops.cuh"
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
 #include <algorithm>
@@ -235,12 +236,14 @@ void finalize_graph(Ctx& c, DGraph& g) {
     int32_t* out = g.bin_store.get() + base;
     cub::CountingInputIterator<int32_t> it(0);
     TierIs op{g.offs.get(), t, g.tm};
-    size_t tmp = 0;
-    CK(cub::DeviceSelect::If(nullptr, tmp, it, out, nsel.get(), (int)g.n, op, c.stream));
-    void* p = c.cub_scratch(tmp);
-    launch(c, "tier_select", 16.0 * g.n, [&] {
-      CK(cub::DeviceSelect::If(p, tmp, it, out, nsel.get(), (int)g.n, op, c.stream));
-    });
+    if (!small_select(c, "tier_select", op, g.n, out, nsel.get())) {
+      size_t tmp = 0;
+      CK(cub::DeviceSelect::If(nullptr, tmp, it, out, nsel.get(), (int)g.n, op, c.stream));
+      void* p = c.cub_scratch(tmp);
+      launch(c, "tier_select", 16.0 * g.n, [&] {
+        CK(cub::DeviceSelect::If(p, tmp, it, out, nsel.get(), (int)g.n, op, c.stream));
+      });
+    }
     g.bin_list[t] = out;
     base += g.bin_cnt[t];
   }
