@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstring>
 #include <omp.h>
+#include <emmintrin.h>
 #include <climits>
 #include <cstdlib>
 
@@ -64,12 +65,29 @@ static bool parallel_narrow(int32_t* dst, const int64_t* src, int64_t count, lon
       mn = LLONG_MAX;
       mx = LLONG_MIN;
     }
-    for (int64_t j = b; j < e; ++j) {
+    // non-temporal 16-byte stores into the pinned buffer: no read-for-
+    // ownership of the destination lines (the staging is host-memory bound)
+    int64_t j = b;
+    for (; j < e && ((uintptr_t)(dst + j) & 15); ++j) {
       const long long x = src[j];
       mn = x < mn ? x : mn;
       mx = x > mx ? x : mx;
       dst[j] = (int32_t)x;
     }
+    for (; j + 4 <= e; j += 4) {
+      const long long x0 = src[j], x1 = src[j + 1], x2 = src[j + 2], x3 = src[j + 3];
+      mn = std::min(mn, std::min(std::min(x0, x1), std::min(x2, x3)));
+      mx = std::max(mx, std::max(std::max(x0, x1), std::max(x2, x3)));
+      _mm_stream_si128(reinterpret_cast<__m128i*>(dst + j),
+                       _mm_set_epi32((int)x3, (int)x2, (int)x1, (int)x0));
+    }
+    for (; j < e; ++j) {
+      const long long x = src[j];
+      mn = x < mn ? x : mn;
+      mx = x > mx ? x : mx;
+      dst[j] = (int32_t)x;
+    }
+    _mm_sfence();
     if (mn < lo || mx > hi) bad = 1;
   }
   if (all_one) *all_one = check_ones && !notone;
