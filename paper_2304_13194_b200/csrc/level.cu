@@ -95,6 +95,7 @@ struct LevelArgs {
   unsigned long long* Hs;
   unsigned long long* CH;
   int32_t* ext;        // weighted external degree per vertex (boundary iff > 0)
+  int bnd_sweeps;      // later Jetlp sweeps visit only the boundary rows (collected first)
   int32_t* blists;     // per-tier boundary rows (segments as cand_lists)
   int32_t* wdeg;       // weighted degrees (written by the first Jetlp sweep; weighted levels)
   int32_t* opidx;
@@ -796,7 +797,7 @@ __global__ void __launch_bounds__(LV_BLOCK, LV_MIN_BLOCKS) k_level(LevelArgs A) 
         a.wdeg = A.ext ? A.wdeg : nullptr;
         return a;
       };
-      const bool bnd = ext_ok;
+      const bool bnd = ext_ok && A.bnd_sweeps;
       if (bnd) {
         const int32_t* ext = A.ext;
         collect_tiled([&](int v) { return __ldcg(ext + v) != 0; },
@@ -1148,6 +1149,11 @@ bool refine_level_device(Ctx& c, Workspace& w, const DGraph& g, int32_t* parts, 
   S.blists.ensure(w.cap_n, c.stream);
   // (external degrees are int32: levels with weighted degrees >= 2^31 sweep in full)
   A.ext = (getenv("JET_FULL_SWEEPS") || g.max_wdeg >= (1LL << 31)) ? nullptr : S.ext.get();
+  static const int64_t bnd_min_n = [] {
+    const char* e = getenv("JET_BND_MIN_N");
+    return e ? (int64_t)atoll(e) : (int64_t)0;
+  }();
+  A.bnd_sweeps = g.n > bnd_min_n;
   A.blists = S.blists.get();
   S.wdeg.ensure(g.n, c.stream);
   A.wdeg = g.unit_ew ? nullptr : S.wdeg.get();
